@@ -1,0 +1,126 @@
+/*
+ * vnm.h — C ABI of the B200-native V:N:M sparse linear layer (arXiv 2410.16135).
+ *
+ * The method (§3 "Preliminary"; App. A):
+ *   S_{V:N:M}: within every V x M block of W keep the 4 columns whose L1 norm of importance scores is
+ *   largest, then keep the 2 largest scores of each row among those 4.  The deployment
+ *   path pads W, converts it to the compressed form A_n / A_i1 / A_i2, and runs
+ *   the V:N:M SpMM on sparse tensor cores.
+ *
+ * Conventions (all calls):
+ *   - Every data pointer is a DEVICE pointer owned by the caller (e.g. a torch tensor); the library
+ *     allocates no device memory and keeps no state besides a host-side cache of TMA descriptors.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - Argument / shape / alignment errors are detected on the host and returned before any launch.
+ *     Data-dependent errors (a mask that violates the V:N:M pattern) are written to `d_status`.
+ *   - bf16 tensors are passed as uint16_t bit patterns.  Leading dimensions (ld*) are in ELEMENTS.
+ *   - Inputs must be finite; NaN/Inf behaviour is unspecified.
+ *   - Identical inputs give byte-identical outputs.
+ *   - Thread-safe.
+ *
+ * Padding: W, score and X^T are read with their logical extents and are zero outside;
+ * all packed outputs use the padded geometry of vnm_geom.  Padded rows/columns are pruned like real
+ * ones (their scores are 0), pad blocks (nb <= b < nb_pad) hold values 0, col_idx {0,1,2,3} and the
+ * 2:4 nibble 0x4; mask bits at columns >= cols_p are 0.  See DESIGN.md §4 for every layout.
+ */
+#ifndef VNM_H_
+#define VNM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* vnm_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    VNM_OK = 0,
+    VNM_ERR_ARG = -1,         /* NULL pointer where one is required, bad enum value              */
+    VNM_ERR_SHAPE = -2,       /* V, M, rows, cols, T, ld out of range                            */
+    VNM_ERR_ALIGN = -3,       /* pointer not 16-byte aligned / ld not a multiple of 8 (4 for fp32) */
+    VNM_ERR_UNSUPPORTED = -4, /* valid per the method but not implemented (e.g. vnm_spmm V != 64)  */
+    VNM_ERR_CUDA = -5         /* a CUDA launch / driver call failed                              */
+} vnm_status;
+
+typedef enum { VNM_F32 = 0, VNM_BF16 = 1 } vnm_dtype;
+
+/* Padded geometry.  N (=2) is implicit ("N≡2").
+ *   rows_p = ceil(rows/V)*V      cols_p = ceil(cols/M)*M      nb = cols_p/M (column blocks per row)
+ *   nb_pad = ceil(nb/8)*8        (one u32 of metadata = 8 blocks = one 32-wide sparse MMA K step)
+ *   ld_val = 2*nb_pad (bf16)     ld_meta = nb_pad/8 (u32)     ld_mask = ceil(cols_p/32) (u32)     */
+typedef struct {
+    int32_t rows, cols, V, M;
+    int32_t rows_p, cols_p, nb, nb_pad;
+    int32_t ld_val, ld_meta, ld_mask;
+} vnm_geom;
+
+/* The compressed form (App. A).  Borrowed device pointers:
+ *   values  (A_n)  bf16 [rows_p][ld_val]       the 2 kept values of each block of each row, left to right
+ *   col_idx (A_i1) u8   [rows_p/V][nb_pad][4]  the block's 4 column indices (0..M-1), strictly ascending
+ *   meta    (A_i2) u32  [rows_p][ld_meta]      nibble (b%8) of word b/8 = pos_lo | pos_hi<<2, pos in 0..3
+ *                                              indexes col_idx, pos_lo < pos_hi
+ * A_i1 lists the columns that carry the block's nonzeros; when fewer than 4 do (always possible,
+ * e.g. V = 1) it is completed with the lowest-index remaining columns (reading Q19), so the
+ * packed form is a function of the mask alone.                                                        */
+typedef struct {
+    vnm_geom g;
+    uint16_t* values;
+    uint8_t* col_idx;
+    uint32_t* meta;
+} vnm_packed;
+
+/* Host, pure.  Ranges: rows, cols >= 0; V a power of two in [1, 256]; 4 <= M <= 32.
+ * VNM_ERR_SHAPE otherwise.                                                                             */
+vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_geom* out);
+
+/* Bytes of one buffer for geometry g: which = 0 values, 1 col_idx, 2 meta, 3 mask.  0 on bad input.   */
+size_t vnm_bytes(const vnm_geom* g, int which);
+
+/* S_{V:N:M} (§3) -> mask bits.
+ *   W      bf16 [g->rows][ldw], 16-B aligned, ldw % 8 == 0, ldw >= cols
+ *   score  fp32 [g->rows][lds] or NULL (NULL = ABS criterion, e = |W|); 16-B aligned, lds % 4 == 0
+ *   mask   u32  [rows_p][ld_mask] (written completely)
+ * Importance e = |score| (or |W|); column L1 summed in fp32 in the canonical stride-halving tree order
+ * (Q3); ties at both steps go to the smaller index.                                */
+vnm_status vnm_prune(const uint16_t* W, int64_t ldw, const float* score, int64_t lds, const vnm_geom* g,
+                     uint32_t* mask, vnm_stream_t stream);
+
+/* Compress W with a given mask into A_n / A_i1 / A_i2.
+ *   W, ldw as above; mask u32 [rows_p][ld_mask]; out->g must equal *g and its pointers must be set.
+ *   d_status: NULL or one int32 in device memory; receives 0 if the mask is a valid V:N:M mask, else
+ *   1 + (vb*nb + b) of the first (lowest-index) invalid block (a row without exactly 2 bits in the
+ *   block, or more than 4 columns carrying bits), or 1 + (rows_p/V)*nb if a bit is set at a column
+ *   >= cols_p.  The packed outputs are unspecified when the mask is invalid.                            */
+vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, const vnm_geom* g,
+                        vnm_packed* out, int32_t* d_status, vnm_stream_t stream);
+
+/* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.      */
+vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
+                              const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
+
+/* The V:N:M SpMM (App. A):  Y^T[o][t] = sum_k W'[o][k] * X^T[k][t],  W' = unpack(P).
+ *   XT  bf16 [P->g.cols][ldx]  feature-major activations (tokens contiguous), 16-B aligned, ldx % 8 == 0
+ *   T   tokens, 0 <= T <= ldx
+ *   YT  [P->g.rows][ldy]  fp32 (y_dtype VNM_F32) or bf16 (VNM_BF16, round-to-nearest-even), 16-B aligned,
+ *       ldy % 8 == 0, ldy >= T; only rows < g.rows and columns < T are written.
+ * bf16 x bf16 products, fp32 accumulation on the sparse tensor cores (tcgen05.mma.sp).
+ * Supported: V == 64 (VNM_ERR_UNSUPPORTED otherwise; V = 128 is the next step).
+ * workspace: optional device scratch (16-B aligned) used by the small-T split-K plan; pass NULL/0 to
+ * let the library choose a plan without it (vnm_spmm_workspace_bytes gives the size it can use).     */
+vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,
+                    vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
+
+size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T);
+
+/* Human-readable text of a status (static storage).                                                   */
+const char* vnm_status_string(vnm_status s);
+
+/* Number of kernel launches the library issued since load (for the bench's gpu_launches count).       */
+uint64_t vnm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VNM_H_ */

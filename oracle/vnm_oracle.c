@@ -176,8 +176,8 @@ static int mask_bit(const uint32_t* mask, const vnmo_geom* g, int32_t r, int32_t
 }
 
 /* O6: pack.  Returns 0, or 1 + (vb*nb + b) of the first block whose mask is not a valid V:N:M mask
- * (a row without exactly 2 bits, more than 4 columns carrying bits), or 1 + rows_p/V*nb when a bit
- * is set at a column >= cols_p.  A_i1 = the columns carrying the block's bits, ascending; when fewer
+ * (a row without exactly 2 bits, more than 4 columns carrying bits); if every block is valid but a
+ * bit is set at a column >= cols_p, 1 + rows_p/V*nb.  A_i1 = the columns carrying the block's bits, ascending; when fewer
  * than 4 columns carry bits it is completed with the lowest-index remaining columns (reading Q19). */
 int vnmo_pack(const uint16_t* W, int64_t ldw, const uint32_t* mask,
               int32_t rows, int32_t cols, int32_t V, int32_t M,
@@ -188,10 +188,6 @@ int vnmo_pack(const uint16_t* W, int64_t ldw, const uint32_t* mask,
     if (M > 64) return VNMO_ERR_SHAPE;
     if (!W || !mask || !values || !col_idx || !meta) return VNMO_ERR_ARG;
     const int32_t nvb = g.rows_p / V;
-    /* bits beyond cols_p */
-    for (int32_t r = 0; r < g.rows_p; ++r)
-        for (int32_t c = g.cols_p; c < g.ld_mask * 32; ++c)
-            if (mask_bit(mask, &g, r, c)) return 1 + nvb * g.nb;
     int64_t first_bad = -1;
     for (int32_t vb = 0; vb < nvb && first_bad < 0; ++vb) {
         for (int32_t b = 0; b < g.nb_pad; ++b) {
@@ -240,6 +236,10 @@ int vnmo_pack(const uint16_t* W, int64_t ldw, const uint32_t* mask,
         }
     }
     if (first_bad >= 0) return (int)(1 + first_bad);
+    /* bits beyond cols_p (checked after the blocks: the status is the lowest error index) */
+    for (int32_t r = 0; r < g.rows_p; ++r)
+        for (int32_t c = g.cols_p; c < g.ld_mask * 32; ++c)
+            if (mask_bit(mask, &g, r, c)) return 1 + nvb * g.nb;
     return VNMO_OK;
 }
 

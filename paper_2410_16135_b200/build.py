@@ -1,0 +1,49 @@
+"""Build the in-tree CUDA libraries with nvcc for sm_100a (no JIT, no torch extension machinery).
+
+  libvnm.so        the product: C ABI of include/vnm.h (api.cpp + prune.cu + spmm.cu)
+  libvnm_probe.so  test-only hardware probes / microbenchmarks (probes.cu)
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
+         "-Xptxas", "-warn-spills"]
+
+LIBS = {
+    "libvnm.so": ["api.cpp", "prune.cu", "spmm.cu"],
+    "libvnm_probe.so": ["probes.cu"],
+}
+
+
+def _stale(out: str, srcs: list[str]) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    deps.append(os.path.join(HERE, "..", "include", "vnm.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    for lib, files in LIBS.items():
+        srcs = [os.path.join(CSRC, f) for f in files]
+        out = os.path.join(HERE, lib)
+        if not force and not _stale(out, srcs):
+            continue
+        tmp = out + f".tmp{os.getpid()}"
+        cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp, *srcs, "-lcudart"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+        os.replace(tmp, out)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,185 @@
+// api.cpp — the C ABI declared in include/vnm.h: host-side validation, geometry, dispatch.
+// Every argument / shape / alignment error is returned before any launch; nothing here allocates
+// device memory.
+#include <atomic>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vnm_internal.h"
+
+namespace vnm {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace vnm
+
+namespace {
+
+bool is_pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+int32_t ceil_to(int32_t a, int32_t m) { return ((a + m - 1) / m) * m; }
+
+bool same_geom(const vnm_geom& a, const vnm_geom& b) {
+    return a.rows == b.rows && a.cols == b.cols && a.V == b.V && a.M == b.M && a.rows_p == b.rows_p &&
+           a.cols_p == b.cols_p && a.nb == b.nb && a.nb_pad == b.nb_pad && a.ld_val == b.ld_val &&
+           a.ld_meta == b.ld_meta && a.ld_mask == b.ld_mask;
+}
+
+vnm_status check_geom(const vnm_geom* g) {
+    if (!g) return VNM_ERR_ARG;
+    vnm_geom ref;
+    if (vnm_geometry(g->rows, g->cols, g->V, g->M, &ref) != VNM_OK) return VNM_ERR_SHAPE;
+    if (!same_geom(ref, *g)) return VNM_ERR_SHAPE;
+    return VNM_OK;
+}
+
+vnm_status check_w(const uint16_t* W, int64_t ldw, const vnm_geom* g) {
+    if (g->rows > 0 && g->cols > 0 && !W) return VNM_ERR_ARG;
+    if (ldw < g->cols || ldw < 0) return VNM_ERR_SHAPE;
+    if (W && (!aligned16(W) || (ldw % 8) != 0)) return VNM_ERR_ALIGN;
+    return VNM_OK;
+}
+
+vnm_status check_score(const float* s, int64_t lds, const vnm_geom* g) {
+    if (!s) return VNM_OK;
+    if (lds < g->cols) return VNM_ERR_SHAPE;
+    if (!aligned16(s) || (lds % 4) != 0) return VNM_ERR_ALIGN;
+    return VNM_OK;
+}
+
+vnm_status check_packed(const vnm_packed* P, const vnm_geom* g) {
+    if (!P) return VNM_ERR_ARG;
+    if (!same_geom(P->g, *g)) return VNM_ERR_SHAPE;
+    if (g->rows_p > 0 && g->nb_pad > 0 && (!P->values || !P->col_idx || !P->meta)) return VNM_ERR_ARG;
+    if ((P->values && !aligned16(P->values)) || (P->col_idx && !aligned16(P->col_idx)) ||
+        (P->meta && !aligned16(P->meta)))
+        return VNM_ERR_ALIGN;
+    return VNM_OK;
+}
+
+vnm_status from_launch(int rc) {
+    if (rc == 0) return VNM_OK;
+    if (rc == vnm::kLaunchUnsupported) return VNM_ERR_UNSUPPORTED;
+    return VNM_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_geom* out) {
+    if (!out) return VNM_ERR_ARG;
+    if (rows < 0 || cols < 0 || !is_pow2(V) || V > 256 || M < 4 || M > 32) return VNM_ERR_SHAPE;
+    if (rows > (1 << 30) || cols > (1 << 30)) return VNM_ERR_SHAPE;
+    vnm_geom g;
+    g.rows = rows;
+    g.cols = cols;
+    g.V = V;
+    g.M = M;
+    g.rows_p = ceil_to(rows, V);
+    g.cols_p = ceil_to(cols, M);
+    g.nb = g.cols_p / M;
+    g.nb_pad = ceil_to(g.nb, 8);
+    g.ld_val = 2 * g.nb_pad;
+    g.ld_meta = g.nb_pad / 8;
+    g.ld_mask = (g.cols_p + 31) / 32;
+    *out = g;
+    return VNM_OK;
+}
+
+size_t vnm_bytes(const vnm_geom* g, int which) {
+    if (check_geom(g) != VNM_OK) return 0;
+    const size_t rp = static_cast<size_t>(g->rows_p);
+    switch (which) {
+        case 0: return rp * static_cast<size_t>(g->ld_val) * 2;
+        case 1: return rp / static_cast<size_t>(g->V) * static_cast<size_t>(g->nb_pad) * 4;
+        case 2: return rp * static_cast<size_t>(g->ld_meta) * 4;
+        case 3: return rp * static_cast<size_t>(g->ld_mask) * 4;
+        default: return 0;
+    }
+}
+
+vnm_status vnm_prune(const uint16_t* W, int64_t ldw, const float* score, int64_t lds, const vnm_geom* g,
+                     uint32_t* mask, vnm_stream_t stream) {
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if ((s = check_w(W, ldw, g))) return s;
+    if ((s = check_score(score, lds, g))) return s;
+    if (g->rows_p == 0 || g->ld_mask == 0) return VNM_OK;
+    if (!mask) return VNM_ERR_ARG;
+    if (!aligned16(mask)) return VNM_ERR_ALIGN;
+    if (!W && !score) return VNM_ERR_ARG;
+    vnm::PruneLaunch L{g, W, ldw, score, lds, nullptr, mask, nullptr, nullptr, nullptr, nullptr};
+    if (!W) return VNM_ERR_ARG;
+    return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, const vnm_geom* g, vnm_packed* out,
+                        int32_t* d_status, vnm_stream_t stream) {
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if ((s = check_w(W, ldw, g))) return s;
+    if ((s = check_packed(out, g))) return s;
+    if (g->rows_p == 0 || g->nb_pad == 0) {
+        if (d_status) cudaMemsetAsync(d_status, 0, sizeof(int32_t), reinterpret_cast<cudaStream_t>(stream));
+        return VNM_OK;
+    }
+    if (!mask || !W) return VNM_ERR_ARG;
+    if (!aligned16(mask)) return VNM_ERR_ALIGN;
+    if (d_status && (reinterpret_cast<uintptr_t>(d_status) & 3u)) return VNM_ERR_ALIGN;
+    vnm::PruneLaunch L{g, W, ldw, nullptr, 0, mask, nullptr, out->values, out->col_idx, out->meta, d_status};
+    return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds, const vnm_geom* g,
+                              vnm_packed* out, uint32_t* mask, vnm_stream_t stream) {
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if ((s = check_w(W, ldw, g))) return s;
+    if ((s = check_score(score, lds, g))) return s;
+    if ((s = check_packed(out, g))) return s;
+    if (mask && !aligned16(mask)) return VNM_ERR_ALIGN;
+    if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
+    if (!W) return VNM_ERR_ARG;
+    vnm::PruneLaunch L{g, W, ldw, score, lds, nullptr, mask, out->values, out->col_idx, out->meta, nullptr};
+    return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,
+                    vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
+    if (!P) return VNM_ERR_ARG;
+    const vnm_geom* g = &P->g;
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if ((s = check_packed(P, g))) return s;
+    if (y_dtype != VNM_F32 && y_dtype != VNM_BF16) return VNM_ERR_ARG;
+    if (T < 0 || ldx < T || ldy < T) return VNM_ERR_SHAPE;
+    if (g->V != 64) return VNM_ERR_UNSUPPORTED;
+    if (T == 0 || g->rows == 0) return VNM_OK;
+    if (!YT) return VNM_ERR_ARG;
+    if (g->cols > 0 && !XT) return VNM_ERR_ARG;
+    if ((XT && !aligned16(XT)) || !aligned16(YT) || (ldx % 8) != 0 || (ldy % 8) != 0) return VNM_ERR_ALIGN;
+    if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
+    vnm::SpmmLaunch L{P, XT, ldx, T, YT, ldy, y_dtype, workspace, workspace ? workspace_bytes : 0};
+    return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T) {
+    if (check_geom(g) != VNM_OK || T < 0) return 0;
+    return vnm::spmm_workspace_bytes(*g, T);
+}
+
+const char* vnm_status_string(vnm_status s) {
+    switch (s) {
+        case VNM_OK: return "ok";
+        case VNM_ERR_ARG: return "invalid argument (null pointer or bad enum)";
+        case VNM_ERR_SHAPE: return "shape out of range (V, M, rows, cols, T or leading dimension)";
+        case VNM_ERR_ALIGN: return "misaligned pointer or leading dimension";
+        case VNM_ERR_UNSUPPORTED: return "configuration not supported by this build";
+        case VNM_ERR_CUDA: return "CUDA launch / driver error";
+        default: return "unknown status";
+    }
+}
+
+uint64_t vnm_launch_count(void) { return vnm::g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

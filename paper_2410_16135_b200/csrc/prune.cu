@@ -1,0 +1,402 @@
+// prune.cu — the V:N:M mask + compression pass for sm_100a.
+//
+// S_{V:N:M} (§3 "Pruning of V:N:M sparsity"):
+//   1) importance e = |score| (ABS: e = |W|)
+//   2) per V x M block, column L1 of e over the V rows; keep the 4 largest
+//   3) per row, keep the 2 largest e among the 4 kept columns
+// followed by the compressed-format conversion A_n / A_i1 / A_i2 (App. A).
+//
+// Design (B200): one CTA = a tile of RT rows (RT = max(V, 32)) x CB column blocks (CB*M columns).
+//   load   : the W (and score) tile is staged into shared memory with 16-byte cp.async
+//            (coalesced, zero-fill past the logical extent = implicit padding);
+//   compute: Lb = min(8, V) lanes own one block; each lane holds rows j, j+Lb, ... of the block, sums
+//            them with an in-lane halving tree, then Lb-lane xor butterflies finish the canonical
+//            stride-halving tree (Q3) — bit-identical in every lane to the oracle's order;
+//            top-4 by a running insertion list (ties -> smaller column), per-row top-2 (ties -> smaller
+//            position), all integer / compare work in registers;
+//   store  : outputs are staged in shared memory and written row-wise with 16-byte stores.
+// The pass is HBM-bound: algorithmic bytes per weight element = 2 (W) [+4 score] + (4 + 0.5)/M
+// (values + meta) + 4/(V M) (col_idx) + 1/8 (mask).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "vnm_internal.h"
+
+namespace vnm {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+struct PruneArgs {
+    const uint16_t* W;
+    int64_t ldw;
+    const float* score;
+    int64_t lds;
+    const uint32_t* mask_in;  // FROM_MASK
+    uint32_t* mask_out;       // may be null
+    uint16_t* values;         // may be null (mask-only prune)
+    uint8_t* col_idx;
+    uint32_t* meta;
+    int32_t* status;  // FROM_MASK, may be null
+    int32_t rows, cols, M, rows_p, cols_p, nb, nb_pad, ld_val, ld_meta, ld_mask;
+    int32_t CB;  // column blocks per CTA (32, 16 or 8)
+};
+
+__device__ __forceinline__ float bf16_abs_to_f32(uint16_t h) {
+    return __uint_as_float(static_cast<uint32_t>(h & 0x7FFFu) << 16);
+}
+
+template <int V>
+struct Shape {
+    static constexpr int Lb = V < 8 ? V : 8;  // lanes per block
+    static constexpr int RPL = V / Lb;        // rows per lane
+    static constexpr int RT = V < 32 ? 32 : V;
+    static constexpr int IPW = 32 / Lb;  // items per warp pass
+};
+
+template <int LB>
+__device__ __forceinline__ float butterfly_sum(float v) {
+#pragma unroll
+    for (int s = LB / 2; s >= 1; s >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, s);
+    return v;
+}
+template <int LB>
+__device__ __forceinline__ uint32_t butterfly_or(uint32_t v) {
+#pragma unroll
+    for (int s = LB / 2; s >= 1; s >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, s);
+    return v;
+}
+
+template <int V, bool FROM_MASK, bool HAS_SCORE>
+__global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a) {
+    using S = Shape<V>;
+    constexpr int RT = S::RT, Lb = S::Lb, RPL = S::RPL, IPW = S::IPW;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int CB = a.CB, M = a.M;
+    const int tile_cols = CB * M;
+    const int pitch_w = tile_cols + 8;  // bf16 elements; +16 B breaks row-to-row bank aliasing
+    const int pitch_s = tile_cols + 4;  // fp32
+    const int mwords = tile_cols / 32;  // mask words per row in this tile
+    const int b0 = blockIdx.x * CB;
+    const int r0 = blockIdx.y * RT;
+    const int c0 = b0 * M;
+
+    // ---- shared memory carve-up
+    uint8_t* p = smem;
+    uint16_t* sW = reinterpret_cast<uint16_t*>(p);
+    p += static_cast<size_t>(RT) * pitch_w * 2;
+    float* sS = reinterpret_cast<float*>(p);
+    if (HAS_SCORE) p += static_cast<size_t>(RT) * pitch_s * 4;
+    uint32_t* sM = reinterpret_cast<uint32_t*>(p);
+    if (FROM_MASK) p += static_cast<size_t>(RT) * mwords * 4;
+    uint16_t* sVal = reinterpret_cast<uint16_t*>(p);
+    p += static_cast<size_t>(RT) * 2 * CB * 2;
+    uint32_t* sBits = reinterpret_cast<uint32_t*>(p);
+    p += static_cast<size_t>(RT) * CB * 4;
+    uint32_t* sCi = reinterpret_cast<uint32_t*>(p);
+    p += static_cast<size_t>(RT / V) * CB * 4;
+    uint8_t* sNib = p;
+
+    // ---- load the tile (zero-filled outside rows x cols)
+    {
+        const int chunks = tile_cols / 8;  // 16-byte chunks of bf16 per row
+        for (int i = threadIdx.x; i < RT * chunks; i += kThreads) {
+            const int r = i / chunks, ch = i % chunks;
+            const int gr = r0 + r, gc = c0 + ch * 8;
+            int bytes = (gr < a.rows) ? (a.cols - gc) * 2 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            const uint16_t* src = bytes ? a.W + static_cast<int64_t>(gr) * a.ldw + gc : a.W;
+            cp_async_16(sW + r * pitch_w + ch * 8, src, static_cast<uint32_t>(bytes));
+        }
+        if (HAS_SCORE) {
+            const int schunks = tile_cols / 4;
+            for (int i = threadIdx.x; i < RT * schunks; i += kThreads) {
+                const int r = i / schunks, ch = i % schunks;
+                const int gr = r0 + r, gc = c0 + ch * 4;
+                int bytes = (gr < a.rows) ? (a.cols - gc) * 4 : 0;
+                bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+                const float* src = bytes ? a.score + static_cast<int64_t>(gr) * a.lds + gc : a.score;
+                cp_async_16(sS + r * pitch_s + ch * 4, src, static_cast<uint32_t>(bytes));
+            }
+        }
+        cp_async_commit();
+        if (FROM_MASK) {
+            const int w0 = c0 / 32;
+            for (int i = threadIdx.x; i < RT * mwords; i += kThreads) {
+                const int r = i / mwords, w = i % mwords;
+                const int gr = r0 + r, gw = w0 + w;
+                sM[i] = (gr < a.rows_p && gw < a.ld_mask) ? a.mask_in[static_cast<int64_t>(gr) * a.ld_mask + gw] : 0u;
+            }
+            // bits at columns >= cols_p (only the last word of a row can hold them)
+            if (a.status && (a.cols_p % 32) != 0) {
+                const int lw = a.ld_mask - 1;
+                if (lw >= w0 && lw < w0 + mwords) {
+                    const uint32_t over = ~((1u << (a.cols_p % 32)) - 1u);
+                    for (int r = threadIdx.x; r < RT; r += kThreads) {
+                        const int gr = r0 + r;
+                        if (gr < a.rows_p && (a.mask_in[static_cast<int64_t>(gr) * a.ld_mask + lw] & over))
+                            atomicMin(a.status, 1 + (a.rows_p / V) * a.nb);
+                    }
+                }
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+
+    // ---- compute: items (vb_local, b_local), IPW per warp pass
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int g = lane / Lb, j = lane % Lb;
+    const int items = (RT / V) * CB;
+    const uint32_t colmask = (M >= 32) ? 0xffffffffu : ((1u << M) - 1u);
+    for (int base = warp * IPW; base < items; base += kWarps * IPW) {
+        const int it = base + g;
+        const bool live = it < items;  // whole-warp control flow stays uniform (shuffles below)
+        const int vbl = live ? it / CB : 0, bl = live ? it % CB : 0;
+        const int b = b0 + bl;
+        const bool real = live && b < a.nb && (r0 + vbl * V) < a.rows_p;
+        const int rbase = vbl * V;  // tile-local first row of the block
+        uint32_t rowbits[RPL];      // per owned row: block-local columns kept (2 bits)
+        uint32_t uni = 0;
+        bool bad = false;
+        if (!FROM_MASK) {
+            // step 2: column L1 (canonical tree) + running top-4 (ties -> smaller column)
+            float tv[4] = {-1.f, -1.f, -1.f, -1.f};
+            int ti[4] = {0, 1, 2, 3};
+            for (int c = 0; c < M; ++c) {
+                float s[RPL];
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) {
+                    const int r = rbase + j + Lb * i;
+                    s[i] = HAS_SCORE ? fabsf(sS[r * pitch_s + bl * M + c]) : bf16_abs_to_f32(sW[r * pitch_w + bl * M + c]);
+                }
+#pragma unroll
+                for (int st = RPL / 2; st >= 1; st >>= 1)
+#pragma unroll
+                    for (int i = 0; i < st; ++i) s[i] = s[i] + s[i + st];
+                const float L = butterfly_sum<Lb>(s[0]);
+                if (L > tv[3]) {
+                    if (L > tv[2]) {
+                        tv[3] = tv[2]; ti[3] = ti[2];
+                        if (L > tv[1]) {
+                            tv[2] = tv[1]; ti[2] = ti[1];
+                            if (L > tv[0]) { tv[1] = tv[0]; ti[1] = ti[0]; tv[0] = L; ti[0] = c; }
+                            else { tv[1] = L; ti[1] = c; }
+                        } else { tv[2] = L; ti[2] = c; }
+                    } else { tv[3] = L; ti[3] = c; }
+                }
+            }
+            uint32_t km = (1u << ti[0]) | (1u << ti[1]) | (1u << ti[2]) | (1u << ti[3]);
+            int kept[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { kept[q] = __ffs(km) - 1; km &= km - 1; }
+            // step 3: per row top-2 of the kept 4 (ties -> smaller position)
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const int r = rbase + j + Lb * i;
+                float e4[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    e4[q] = HAS_SCORE ? fabsf(sS[r * pitch_s + bl * M + kept[q]])
+                                      : bf16_abs_to_f32(sW[r * pitch_w + bl * M + kept[q]]);
+                int f = 0;
+#pragma unroll
+                for (int q = 1; q < 4; ++q) if (e4[q] > e4[f]) f = q;
+                int sc = (f == 0) ? 1 : 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) if (q != f && e4[q] > e4[sc]) sc = q;
+                rowbits[i] = (1u << kept[f]) | (1u << kept[sc]);
+                uni |= rowbits[i];
+            }
+        } else {
+            // the mask decides: each row must hold exactly 2 bits in the block
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+                const int r = rbase + j + Lb * i;
+                const int cb = bl * M;  // tile-local first column
+                const uint32_t* mrow = sM + r * mwords;
+                const int w = cb / 32, sh = cb % 32;
+                uint64_t two = static_cast<uint64_t>(mrow[w]);
+                if (w + 1 < mwords) two |= static_cast<uint64_t>(mrow[w + 1]) << 32;
+                const uint32_t rb = static_cast<uint32_t>(two >> sh) & colmask;
+                rowbits[i] = rb;
+                bad |= __popc(rb) != 2;
+                uni |= rb;
+            }
+        }
+        uni = butterfly_or<Lb>(uni);
+        if (FROM_MASK) {
+            bad |= __popc(uni) > 4;
+            const bool any_bad = butterfly_or<Lb>(bad ? 1u : 0u) != 0u;
+            if (real && any_bad && j == 0 && a.status)
+                atomicMin(a.status, 1 + (blockIdx.y * (RT / V) + vbl) * a.nb + b);
+        }
+        // A_i1: columns carrying bits, completed with the lowest free columns (Q19)
+        uint32_t ci = real ? uni : 0u;
+        for (int need = 4 - __popc(ci); need > 0; --need) ci |= 1u << (__ffs(~ci & colmask) - 1);
+        if (__popc(ci) > 4) ci = 0xFu;  // invalid mask: any well-formed value
+        // outputs of the owned rows
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+            const int r = rbase + j + Lb * i;
+            uint32_t rb = real ? rowbits[i] : 0u;
+            if (__popc(rb) != 2) rb = 0u;  // pad block / invalid row
+            uint32_t nib = 0x4u;
+            uint16_t v0 = 0, v1 = 0;
+            if (rb) {
+                const int clo = __ffs(rb) - 1, chi = 31 - __clz(rb);
+                const uint32_t plo = __popc(ci & ((1u << clo) - 1u)), phi = __popc(ci & ((1u << chi) - 1u));
+                nib = plo | (phi << 2);
+                v0 = sW[r * pitch_w + bl * M + clo];
+                v1 = sW[r * pitch_w + bl * M + chi];
+            }
+            if (live) {
+                sVal[r * 2 * CB + 2 * bl + 0] = v0;
+                sVal[r * 2 * CB + 2 * bl + 1] = v1;
+                sNib[r * CB + bl] = static_cast<uint8_t>(nib);
+                sBits[r * CB + bl] = rb;
+            }
+        }
+        if (live && j == 0) {
+            uint32_t word = 0, m = ci;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { word |= static_cast<uint32_t>(__ffs(m) - 1) << (8 * q); m &= m - 1; }
+            sCi[vbl * CB + bl] = word;
+        }
+    }
+    __syncthreads();
+
+    // ---- store (row-wise, vectorised)
+    const int cbv = min(CB, a.nb_pad - b0);  // blocks of this tile inside nb_pad
+    const int rows_here = min(RT, a.rows_p - r0);
+    if (a.values && cbv > 0) {
+        // values: 2*cbv bf16 per row = cbv/2 chunks of 16 B (cbv is a multiple of 8)
+        const int vch = cbv / 4;
+        for (int i = threadIdx.x; i < rows_here * vch; i += kThreads) {
+            const int r = i / vch, ch = i % vch;
+            const uint4 v = *reinterpret_cast<const uint4*>(sVal + r * 2 * CB + ch * 8);
+            *reinterpret_cast<uint4*>(a.values + static_cast<int64_t>(r0 + r) * a.ld_val + 2 * b0 + ch * 8) = v;
+        }
+        // meta: cbv/8 words per row
+        const int mw = cbv / 8;
+        for (int i = threadIdx.x; i < rows_here * mw; i += kThreads) {
+            const int r = i / mw, w = i % mw;
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) word |= static_cast<uint32_t>(sNib[r * CB + 8 * w + q]) << (4 * q);
+            a.meta[static_cast<int64_t>(r0 + r) * a.ld_meta + b0 / 8 + w] = word;
+        }
+        // col_idx: [vb][b][4]
+        const int nvb_here = rows_here / V;
+        for (int i = threadIdx.x; i < nvb_here * cbv; i += kThreads) {
+            const int v = i / cbv, bl = i % cbv;
+            const int vbg = (r0 / V) + v;
+            reinterpret_cast<uint32_t*>(a.col_idx)[static_cast<int64_t>(vbg) * a.nb_pad + b0 + bl] = sCi[v * CB + bl];
+        }
+    }
+    if (a.mask_out) {
+        const int w0 = c0 / 32;
+        const int nw = min(mwords, a.ld_mask - w0);
+        for (int i = threadIdx.x; i < rows_here * nw; i += kThreads) {
+            const int r = i / nw, w = i % nw;
+            const int lo_col = 32 * w, hi_col = lo_col + 31;  // tile-local columns of this word
+            uint32_t word = 0;
+            for (int bl = lo_col / M; bl <= hi_col / M && bl < CB; ++bl) {
+                const uint32_t bits = sBits[r * CB + bl];
+                const int sh = bl * M - lo_col;
+                word |= sh >= 0 ? (sh < 32 ? bits << sh : 0u) : bits >> (-sh);
+            }
+            a.mask_out[static_cast<int64_t>(r0 + r) * a.ld_mask + w0 + w] = word;
+        }
+    }
+}
+
+__global__ void status_init_kernel(int32_t* s) { *s = 0x7fffffff; }
+__global__ void status_fini_kernel(int32_t* s) {
+    if (*s == 0x7fffffff) *s = 0;
+}
+
+size_t smem_bytes(int V, int M, int CB, bool from_mask, bool has_score) {
+    const int RT = V < 32 ? 32 : V;
+    const int tile_cols = CB * M;
+    size_t b = static_cast<size_t>(RT) * (tile_cols + 8) * 2;
+    if (has_score) b += static_cast<size_t>(RT) * (tile_cols + 4) * 4;
+    if (from_mask) b += static_cast<size_t>(RT) * (tile_cols / 32) * 4;
+    b += static_cast<size_t>(RT) * 2 * CB * 2 + static_cast<size_t>(RT) * CB * 4 +
+         static_cast<size_t>(RT / V) * CB * 4 + static_cast<size_t>(RT) * CB;
+    return b;
+}
+
+template <int V, bool FROM_MASK, bool HAS_SCORE>
+cudaError_t launch_t(const PruneArgs& a, size_t smem, cudaStream_t st) {
+    auto k = prune_pack_kernel<V, FROM_MASK, HAS_SCORE>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    constexpr int RT = Shape<V>::RT;
+    dim3 grid((a.nb_pad + a.CB - 1) / a.CB, (a.rows_p + RT - 1) / RT);
+    k<<<grid, kThreads, smem, st>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <bool FROM_MASK, bool HAS_SCORE>
+cudaError_t launch_v(int V, const PruneArgs& a, size_t smem, cudaStream_t st) {
+    switch (V) {
+        case 1: return launch_t<1, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 2: return launch_t<2, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 4: return launch_t<4, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 8: return launch_t<8, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 16: return launch_t<16, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 32: return launch_t<32, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 64: return launch_t<64, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 128: return launch_t<128, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 256: return launch_t<256, FROM_MASK, HAS_SCORE>(a, smem, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+// Host entry used by api.cpp.  Picks CB so that the tile fits in shared memory.
+int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
+    const vnm_geom& g = *L.g;
+    const bool from_mask = L.mask_in != nullptr;
+    const bool has_score = L.score != nullptr;
+    int CB = 0;
+    for (int cb : {32, 16, 8}) {
+        if ((cb * g.M) % 32 != 0) continue;  // whole mask words per tile
+        if (smem_bytes(g.V, g.M, cb, from_mask, has_score) > kMaxSmem) continue;
+        CB = cb;
+        break;
+    }
+    if (CB == 0) return kLaunchUnsupported;
+    PruneArgs a;
+    a.W = L.W; a.ldw = L.ldw; a.score = L.score; a.lds = L.lds;
+    a.mask_in = L.mask_in; a.mask_out = L.mask_out;
+    a.values = L.values; a.col_idx = L.col_idx; a.meta = L.meta; a.status = L.status;
+    a.rows = g.rows; a.cols = g.cols; a.M = g.M; a.rows_p = g.rows_p; a.cols_p = g.cols_p;
+    a.nb = g.nb; a.nb_pad = g.nb_pad; a.ld_val = g.ld_val; a.ld_meta = g.ld_meta; a.ld_mask = g.ld_mask;
+    a.CB = CB;
+    const size_t smem = smem_bytes(g.V, g.M, CB, from_mask, has_score);
+    cudaError_t e;
+    if (from_mask && a.status) {
+        status_init_kernel<<<1, 1, 0, stream>>>(a.status);
+        count_launch();
+    }
+    if (from_mask)
+        e = launch_v<true, false>(g.V, a, smem, stream);
+    else if (has_score)
+        e = launch_v<false, true>(g.V, a, smem, stream);
+    else
+        e = launch_v<false, false>(g.V, a, smem, stream);
+    if (e == cudaSuccess && from_mask && a.status) {
+        status_fini_kernel<<<1, 1, 0, stream>>>(a.status);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    return e == cudaSuccess ? 0 : kLaunchCudaError;
+}
+
+}  // namespace vnm

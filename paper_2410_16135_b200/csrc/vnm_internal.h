@@ -1,0 +1,46 @@
+// vnm_internal.h — host-side glue between the C ABI (api.cpp) and the kernels (prune.cu, spmm.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/vnm.h"
+
+namespace vnm {
+
+constexpr size_t kMaxSmem = 227 * 1024;
+constexpr int kLaunchUnsupported = 1;
+constexpr int kLaunchCudaError = 2;
+
+void count_launch();
+
+struct PruneLaunch {
+    const vnm_geom* g;
+    const uint16_t* W;
+    int64_t ldw;
+    const float* score;      // null => ABS
+    int64_t lds;
+    const uint32_t* mask_in; // non-null => compress from this mask
+    uint32_t* mask_out;      // may be null
+    uint16_t* values;        // may be null (mask only)
+    uint8_t* col_idx;
+    uint32_t* meta;
+    int32_t* status;         // compress only, may be null
+};
+int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream);
+
+struct SpmmLaunch {
+    const vnm_packed* P;
+    const uint16_t* XT;
+    int64_t ldx;
+    int32_t T;
+    void* YT;
+    int64_t ldy;
+    vnm_dtype y_dtype;
+    void* workspace;
+    size_t workspace_bytes;
+};
+int launch_spmm(const SpmmLaunch& L, cudaStream_t stream);
+size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
+
+}  // namespace vnm

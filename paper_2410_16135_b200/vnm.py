@@ -1,0 +1,213 @@
+"""Python binding of the C ABI in include/vnm.h (libvnm.so).  Argument marshalling only.
+
+Every step of the V:N:M path runs in the CUDA kernels of ``csrc/``; this module turns torch CUDA
+tensors into the device pointers / leading dimensions / stream the ABI takes, allocates the outputs
+with torch (the library owns no device memory), and raises on any non-OK status.  There is no CPU
+fallback: if ``libvnm.so`` is missing or a tensor is not on a CUDA device, the call raises.
+
+Names follow the paper: ``prune`` is S_{V:N:M} (§3), ``compress`` produces
+A_n / A_i1 / A_i2 (App. A), ``spmm`` is the V:N:M-sparse MM.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvnm.so")
+
+VNM_OK, VNM_ERR_ARG, VNM_ERR_SHAPE, VNM_ERR_ALIGN, VNM_ERR_UNSUPPORTED, VNM_ERR_CUDA = 0, -1, -2, -3, -4, -5
+VNM_F32, VNM_BF16 = 0, 1
+
+
+class VnmError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+class Geom(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in
+                ("rows", "cols", "V", "M", "rows_p", "cols_p", "nb", "nb_pad", "ld_val", "ld_meta", "ld_mask")]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class CPacked(ctypes.Structure):
+    _fields_ = [("g", Geom), ("values", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("meta", ctypes.c_void_p)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress", "vnm_spmm",
+           "vnm_spmm_workspace_bytes", "vnm_status_string", "vnm_launch_count"]
+
+
+def lib():
+    """Load libvnm.so (built by paper_2410_16135_b200/build.py / __graft_entry__.build())."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run `python __graft_entry__.py build` "
+                                  "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+            GP, PP = ctypes.POINTER(Geom), ctypes.POINTER(CPacked)
+            L.vnm_geometry.argtypes = [i32, i32, i32, i32, GP]
+            L.vnm_geometry.restype = ctypes.c_int
+            L.vnm_bytes.argtypes = [GP, ctypes.c_int]
+            L.vnm_bytes.restype = sz
+            L.vnm_prune.argtypes = [P, i64, P, i64, GP, P, P]
+            L.vnm_prune.restype = ctypes.c_int
+            L.vnm_compress.argtypes = [P, i64, P, GP, PP, P, P]
+            L.vnm_compress.restype = ctypes.c_int
+            L.vnm_prune_compress.argtypes = [P, i64, P, i64, GP, PP, P, P]
+            L.vnm_prune_compress.restype = ctypes.c_int
+            L.vnm_spmm.argtypes = [P, i64, i32, PP, P, i64, ctypes.c_int, P, sz, P]
+            L.vnm_spmm.restype = ctypes.c_int
+            L.vnm_spmm_workspace_bytes.argtypes = [GP, i32]
+            L.vnm_spmm_workspace_bytes.restype = sz
+            L.vnm_status_string.argtypes = [ctypes.c_int]
+            L.vnm_status_string.restype = ctypes.c_char_p
+            L.vnm_launch_count.argtypes = []
+            L.vnm_launch_count.restype = ctypes.c_uint64
+            _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return lib().vnm_status_string(s).decode()
+
+
+def launch_count() -> int:
+    return int(lib().vnm_launch_count())
+
+
+def _check(st: int, what: str) -> None:
+    if st != VNM_OK:
+        raise VnmError(st, what)
+
+
+def geometry(rows: int, cols: int, V: int, M: int) -> Geom:
+    g = Geom()
+    _check(lib().vnm_geometry(rows, cols, V, M, ctypes.byref(g)), "vnm_geometry")
+    return g
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _as_bits16(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype in (torch.bfloat16, torch.int16, torch.uint16):
+        return t
+    raise TypeError(f"expected bf16 (or its int16 bits), got {t.dtype}")
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("vnm kernels take CUDA tensors (there is no CPU path)")
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("expected a 2-D row-major tensor with unit inner stride")
+    return t.stride(0)
+
+
+@dataclass
+class Packed:
+    """The compressed V:N:M weight (App. A): A_n = values, A_i1 = col_idx, A_i2 = meta."""
+    g: Geom
+    values: torch.Tensor   # bf16 [rows_p][ld_val]
+    col_idx: torch.Tensor  # uint8 [rows_p/V][nb_pad][4]
+    meta: torch.Tensor     # int32 (u32 bits) [rows_p][ld_meta]
+
+    def c(self) -> CPacked:
+        return CPacked(self.g, self.values.data_ptr(), self.col_idx.data_ptr(), self.meta.data_ptr())
+
+    @staticmethod
+    def empty(g: Geom, device) -> "Packed":
+        return Packed(g,
+                      torch.empty((g.rows_p, g.ld_val), dtype=torch.bfloat16, device=device),
+                      torch.empty((g.rows_p // g.V, g.nb_pad, 4), dtype=torch.uint8, device=device),
+                      torch.empty((g.rows_p, g.ld_meta), dtype=torch.int32, device=device))
+
+
+def prune(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None) -> torch.Tensor:
+    """S_{V:N:M}(score or |W|) -> mask bits, int32 (u32 bits) [rows_p][ld_mask]."""
+    W = _as_bits16(W)
+    _require_cuda(W, score)
+    g = geometry(W.shape[0], W.shape[1], V, M)
+    mask = torch.empty((g.rows_p, g.ld_mask), dtype=torch.int32, device=W.device)
+    _check(lib().vnm_prune(_ptr(W), _ld(W), _ptr(score), _ld(score) if score is not None else 0, ctypes.byref(g),
+                           _ptr(mask), _stream(W.device)), "vnm_prune")
+    return mask
+
+
+def compress(W: torch.Tensor, mask: torch.Tensor, V: int, M: int, status: torch.Tensor | None = None) -> Packed:
+    """A_n / A_i1 / A_i2 from W and a V:N:M mask.  If `status` (int32[1], CUDA) is given it receives 0 or
+    1 + the index of the first invalid block (see include/vnm.h)."""
+    W = _as_bits16(W)
+    _require_cuda(W, mask, status)
+    g = geometry(W.shape[0], W.shape[1], V, M)
+    P = Packed.empty(g, W.device)
+    cp = P.c()
+    _check(lib().vnm_compress(_ptr(W), _ld(W), _ptr(mask), ctypes.byref(g), ctypes.byref(cp), _ptr(status),
+                              _stream(W.device)), "vnm_compress")
+    return P
+
+
+def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None, want_mask: bool = False):
+    """Fused S_{V:N:M} + compression in one pass over W.  Returns Packed (and the mask if asked)."""
+    W = _as_bits16(W)
+    _require_cuda(W, score)
+    g = geometry(W.shape[0], W.shape[1], V, M)
+    P = Packed.empty(g, W.device)
+    mask = torch.empty((g.rows_p, g.ld_mask), dtype=torch.int32, device=W.device) if want_mask else None
+    cp = P.c()
+    _check(lib().vnm_prune_compress(_ptr(W), _ld(W), _ptr(score), _ld(score) if score is not None else 0,
+                                    ctypes.byref(g), ctypes.byref(cp), _ptr(mask), _stream(W.device)),
+           "vnm_prune_compress")
+    return (P, mask) if want_mask else P
+
+
+def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | None = None,
+         out_dtype: torch.dtype = torch.float32, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Y^T = W' X^T on the sparse tensor cores.  XT: bf16 [cols][ldx] (feature-major, tokens contiguous).
+    Returns Y^T [rows][T] (fp32 or bf16), or writes into `out` ([rows][ldy], ldy >= T)."""
+    XT = _as_bits16(XT)
+    _require_cuda(XT, out, workspace)
+    T = XT.shape[1] if T is None else T
+    g = P.g
+    if XT.shape[0] != g.cols:
+        raise ValueError(f"XT has {XT.shape[0]} rows, the packed weight has {g.cols} input channels")
+    if out is None:
+        ldy = (T + 7) // 8 * 8
+        out = torch.empty((g.rows, ldy), dtype=out_dtype, device=XT.device)[:, :T] if ldy != T else \
+            torch.empty((g.rows, T), dtype=out_dtype, device=XT.device)
+    ydt = VNM_BF16 if out.dtype == torch.bfloat16 else VNM_F32
+    if out.dtype not in (torch.bfloat16, torch.float32):
+        raise TypeError("Y^T must be fp32 or bf16")
+    cp = P.c()
+    ws_ptr, ws_bytes = (_ptr(workspace), workspace.numel() * workspace.element_size()) if workspace is not None \
+        else (None, 0)
+    _check(lib().vnm_spmm(_ptr(XT), XT.stride(0), T, ctypes.byref(cp), _ptr(out), out.stride(0), ydt, ws_ptr,
+                          ws_bytes, _stream(XT.device)), "vnm_spmm")
+    return out
+
+
+def spmm_workspace_bytes(g: Geom, T: int) -> int:
+    return int(lib().vnm_spmm_workspace_bytes(ctypes.byref(g), T))

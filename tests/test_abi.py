@@ -1,0 +1,92 @@
+"""The C-ABI library loads and exports every symbol include/vnm.h declares; host-side validation
+(geometry arithmetic, status codes for bad arguments) — no kernel launches, no GPU needed."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle
+from paper_2410_16135_b200 import vnm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "vnm.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:vnm_status|size_t|const char\*|uint64_t)\s+(vnm_\w+)\(", src, re.M)))
+
+
+def test_exports_every_declared_symbol():
+    L = vnm.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 9, syms
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(vnm.EXPORTS) == syms
+
+
+@pytest.mark.parametrize("rows,cols,V,M", [(128, 64, 64, 8), (1152, 384, 64, 5), (11008, 4096, 64, 5),
+                                           (5, 7, 2, 5), (1, 1, 16, 5), (70, 23, 64, 5), (0, 0, 1, 4),
+                                           (4096, 11008, 64, 7), (300, 1000, 256, 32)])
+def test_geometry_matches_oracle(rows, cols, V, M):
+    g = vnm.geometry(rows, cols, V, M).as_dict()
+    assert g == oracle.geometry(rows, cols, V, M)
+
+
+@pytest.mark.parametrize("V,M", [(3, 5), (0, 5), (512, 5), (64, 3), (64, 33), (-64, 5)])
+def test_geometry_rejects(V, M):
+    with pytest.raises(vnm.VnmError) as e:
+        vnm.geometry(128, 64, V, M)
+    assert e.value.status == vnm.VNM_ERR_SHAPE
+
+
+def test_bytes():
+    g = vnm.geometry(11008, 4096, 64, 5)
+    L = vnm.lib()
+    assert L.vnm_bytes(ctypes.byref(g), 0) == g.rows_p * g.ld_val * 2
+    assert L.vnm_bytes(ctypes.byref(g), 1) == g.rows_p // 64 * g.nb_pad * 4
+    assert L.vnm_bytes(ctypes.byref(g), 2) == g.rows_p * g.ld_meta * 4
+    assert L.vnm_bytes(ctypes.byref(g), 3) == g.rows_p * g.ld_mask * 4
+    assert L.vnm_bytes(ctypes.byref(g), 9) == 0
+
+
+def test_status_codes_without_launch():
+    L = vnm.lib()
+    g = vnm.geometry(128, 64, 64, 8)
+    fake = ctypes.c_void_p(1 << 20)          # never dereferenced: validation fails first
+    odd = ctypes.c_void_p((1 << 20) + 2)     # misaligned
+    # null W
+    assert L.vnm_prune(None, 64, None, 0, ctypes.byref(g), fake, None) == vnm.VNM_ERR_ARG
+    # ldw < cols
+    assert L.vnm_prune(fake, 32, None, 0, ctypes.byref(g), fake, None) == vnm.VNM_ERR_SHAPE
+    # misaligned W / ld not multiple of 8
+    assert L.vnm_prune(odd, 64, None, 0, ctypes.byref(g), fake, None) == vnm.VNM_ERR_ALIGN
+    assert L.vnm_prune(fake, 68, None, 0, ctypes.byref(g), fake, None) == vnm.VNM_ERR_ALIGN
+    # geometry struct inconsistent with its own fields
+    bad = vnm.geometry(128, 64, 64, 8)
+    bad.nb_pad = 7
+    assert L.vnm_prune(fake, 64, None, 0, ctypes.byref(bad), fake, None) == vnm.VNM_ERR_SHAPE
+    # spmm: V other than 64 is not built yet
+    g16 = vnm.geometry(128, 64, 16, 8)
+    P = vnm.CPacked(g16, 1 << 20, 1 << 20, 1 << 20)
+    assert L.vnm_spmm(fake, 16, 16, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_ERR_UNSUPPORTED
+    P = vnm.CPacked(g, 1 << 20, 1 << 20, 1 << 20)
+    assert L.vnm_spmm(fake, 16, 16, ctypes.byref(P), fake, 16, 7, None, 0, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_spmm(fake, 8, 16, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_ERR_SHAPE
+    assert L.vnm_spmm(fake, 12, 12, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_ERR_ALIGN
+    assert L.vnm_spmm(None, 16, 16, None, fake, 16, 0, None, 0, None) == vnm.VNM_ERR_ARG
+    # compress: packed geometry must equal g
+    P2 = vnm.CPacked(vnm.geometry(128, 64, 64, 5), 1 << 20, 1 << 20, 1 << 20)
+    assert L.vnm_compress(fake, 64, fake, ctypes.byref(g), ctypes.byref(P2), None, None) == vnm.VNM_ERR_SHAPE
+    # T = 0 is a no-op
+    assert L.vnm_spmm(fake, 16, 0, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_OK
+    for s in (0, -1, -2, -3, -4, -5):
+        assert vnm.status_string(s)
+
+
+def test_no_cpu_path():
+    import torch
+    W = torch.zeros(128, 64, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        vnm.prune(W, 64, 8)

@@ -1,0 +1,124 @@
+"""GPU parity for the mask + compression pass (§8 rows a1-a5): bit-exact against the oracle.
+
+Calls go through the C ABI (paper_2410_16135_b200.vnm -> libvnm.so)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2410_16135_b200 import synth, vnm
+from tests.gpu_util import packed_np, to_dev_bf16, to_dev_f32, u32
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [
+    # rows, cols, V, M, kind
+    (128, 64, 64, 8, "int"),       # BJ config 1 (tie-heavy variant)
+    (128, 64, 64, 8, "normal"),    # BJ config 1
+    (70, 23, 64, 5, "normal"),     # ragged rows and cols
+    (200, 333, 16, 7, "wide"),
+    (37, 50, 1, 4, "int"),
+    (64, 96, 2, 6, "normal"),
+    (300, 1000, 128, 16, "outlier"),
+    (96, 200, 32, 13, "int"),
+    (40, 120, 8, 9, "wide"),
+    (260, 256, 256, 4, "normal"),
+    (128, 4096, 4, 32, "normal"),
+    (1152, 384, 64, 5, "normal"),  # DeiT-S qkv
+]
+
+
+def run_all(W, V, M, score=None):
+    rows, cols = W.shape
+    Wd = to_dev_bf16(W)
+    Sd = to_dev_f32(score) if score is not None else None
+    mask_d = vnm.prune(Wd, V, M, score=Sd)
+    P, mask2_d = vnm.prune_compress(Wd, V, M, score=Sd, want_mask=True)
+    torch.cuda.synchronize()
+    return u32(mask_d), u32(mask2_d), packed_np(P), Wd
+
+
+def check(W, V, M, score=None):
+    mask_ref = oracle.prune(W, V, M, score=score)
+    st, v_ref, c_ref, m_ref = oracle.pack(W, mask_ref, V, M)
+    assert st == 0
+    mask, mask2, (v, c, m), Wd = run_all(W, V, M, score)
+    assert np.array_equal(mask, mask_ref), "vnm_prune mask"
+    assert np.array_equal(mask2, mask_ref), "vnm_prune_compress mask"
+    assert np.array_equal(v, v_ref), "A_n values"
+    assert np.array_equal(c, c_ref), "A_i1 col_idx"
+    assert np.array_equal(m, m_ref), "A_i2 meta"
+    # vnm_compress from the oracle's mask gives the same bytes
+    status = torch.full((1,), -7, dtype=torch.int32, device="cuda")
+    P3 = vnm.compress(Wd, torch.from_numpy(mask_ref.view(np.int32)).cuda(), V, M, status=status)
+    v3, c3, m3 = packed_np(P3)
+    assert int(status.item()) == 0
+    assert np.array_equal(v3, v_ref) and np.array_equal(c3, c_ref) and np.array_equal(m3, m_ref)
+
+
+@pytest.mark.parametrize("rows,cols,V,M,kind", SMALL)
+def test_prune_compress_bitexact(rows, cols, V, M, kind):
+    W = synth.weights(rows, cols, seed=rows * 7 + cols + V + M, kind=kind)
+    check(W, V, M)
+
+
+@pytest.mark.parametrize("rows,cols,V,M,kind", [(128, 64, 64, 8, "uniform"), (70, 23, 64, 5, "signed"),
+                                                (300, 1000, 128, 16, "int"), (37, 50, 1, 4, "uniform")])
+def test_score_path_bitexact(rows, cols, V, M, kind):
+    W = synth.weights(rows, cols, seed=3)
+    S = synth.scores(rows, cols, seed=4, kind=kind)
+    check(W, V, M, score=S)
+
+
+@pytest.mark.parametrize("rows,cols,M", [(11008, 4096, 5), (4096, 11008, 5), (4096, 4096, 5), (3072, 768, 8),
+                                         (768, 3072, 8), (2304, 768, 8), (1536, 384, 5), (384, 1536, 5)])
+def test_bj_weight_shapes_bitexact(rows, cols, M):
+    """Every weight shape of BJ configs 2-5 at its (V, M), full outputs compared byte for byte."""
+    W = synth.weights(rows, cols, seed=synth.seed(4, 0) + rows, kind="outlier")
+    check(W, 64, M)
+
+
+@pytest.mark.parametrize("M", [4, 6, 7, 16])
+def test_llama_mlp_m_sweep(M):
+    W = synth.weights(11008, 4096, seed=M, kind="normal")
+    check(W, 64, M)
+
+
+def test_invalid_mask_status():
+    V, M = 64, 5
+    W = synth.weights(128, 80, seed=5)
+    mask = oracle.prune(W, V, M)
+    g = oracle.geometry(128, 80, V, M)
+    Wd = to_dev_bf16(W)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    # third bit in row 70 (V-block 1), block 9
+    bad = mask.copy()
+    dense = np.unpackbits(bad.view(np.uint8).reshape(128, -1), axis=1, bitorder="little")
+    c = [c for c in range(45, 50) if not dense[70, c]][0]
+    bad[70, c // 32] |= np.uint32(1 << (c % 32))
+    vnm.compress(Wd, torch.from_numpy(bad.view(np.int32)).cuda(), V, M, status=status)
+    exp, *_ = oracle.pack(W, bad, V, M)
+    assert int(status.item()) == exp == 1 + 1 * g["nb"] + 9
+    # a bit beyond cols_p (cols_p = 80 -> word 2 bit 16 = column 80)
+    bad2 = mask.copy()
+    bad2[3, 2] |= np.uint32(1 << 16)
+    vnm.compress(Wd, torch.from_numpy(bad2.view(np.int32)).cuda(), V, M, status=status)
+    exp2, *_ = oracle.pack(W, bad2, V, M)
+    assert int(status.item()) == exp2 == 1 + 2 * g["nb"]
+
+
+def test_determinism():
+    W = synth.weights(4096, 4096, seed=1, kind="outlier")
+    Wd = to_dev_bf16(W)
+    a = packed_np(vnm.prune_compress(Wd, 64, 5))
+    b = packed_np(vnm.prune_compress(Wd, 64, 5))
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_strided_input():
+    """W with a leading dimension larger than cols (a view into a bigger buffer)."""
+    W = synth.weights(192, 100, seed=9)
+    Wd = to_dev_bf16(W, ld=136)
+    assert Wd.stride(0) == 136
+    mask = u32(vnm.prune(Wd, 64, 5))
+    assert np.array_equal(mask, oracle.prune(W, 64, 5))

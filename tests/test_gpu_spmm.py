@@ -1,0 +1,153 @@
+"""GPU parity for the V:N:M SpMM (§8 rows a6-a8) against the oracle's fp64 product.
+
+Bar (BASELINE.json): |Y - Y_ref| <= 1e-3 * sum_k |x w| + 1e-6 per element on fp32 Y; bf16 Y adds
+2^-8 |Y_ref| (Q14).  Calls go through the C ABI."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2410_16135_b200 import synth, vnm
+from tests.gpu_util import to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+def make(rows, cols, V, M, T, seed, wkind="normal", xkind="normal"):
+    W = synth.weights(rows, cols, seed=seed, kind=wkind)
+    XT = synth.activations_t(cols, T, seed=seed + 1, kind=xkind)
+    mask, values, col_idx, meta = oracle.prune_pack(W, V, M)
+    Wm = oracle.apply_mask(W, mask, V, M)
+    return W, XT, Wm
+
+
+def gpu_y(W, XT, V, M, T, out_dtype=torch.float32):
+    P = vnm.prune_compress(to_dev_bf16(W), V, M)
+    Y = vnm.spmm(to_dev_bf16(XT), P, T=T, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return Y.float().cpu().numpy().astype(np.float64)
+
+
+def assert_within(Y, Yref, Aref, bf16=False):
+    tol = oracle.tolerance(Yref, Aref, y_is_bf16=bf16)
+    err = np.abs(Y - Yref)
+    bad = err > tol
+    assert not bad.any(), f"{bad.sum()} / {bad.size} outside tolerance; worst {np.max(err - tol)}"
+
+
+def test_config1_toy():
+    """BJ config 1: 64:2:8, W 128x64, X 16x64 (T = 16)."""
+    W, XT, Wm = make(128, 64, 64, 8, 16, seed=synth.seed(1, 0))
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, 8, 16), Yref, Aref)
+
+
+@pytest.mark.parametrize("T", [1, 2, 7, 8, 15, 16, 33, 63, 64, 65, 100, 128, 129, 200, 256, 257, 300, 513])
+def test_token_tails(T):
+    W, XT, Wm = make(192, 300, 64, 5, T, seed=T)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, 5, T), Yref, Aref)
+
+
+@pytest.mark.parametrize("rows,cols,M", [(70, 23, 5), (64, 4, 4), (128, 1, 5), (65, 1000, 7), (130, 257, 16),
+                                         (64, 2048, 8), (256, 640, 6), (64, 5000, 5), (200, 333, 32)])
+def test_shapes_and_k_tails(rows, cols, M):
+    T = 96
+    W, XT, Wm = make(rows, cols, 64, M, T, seed=rows + cols)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, M, T), Yref, Aref)
+
+
+def test_bf16_output():
+    W, XT, Wm = make(256, 512, 64, 5, 200, seed=3)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, 5, 200, out_dtype=torch.bfloat16), Yref, Aref, bf16=True)
+
+
+def test_identity_x_is_exact():
+    """Pin P10: X = I  =>  Y^T = W' exactly (each output is one weight times 1.0)."""
+    rows, cols, M = 128, 200, 5
+    W = synth.weights(rows, cols, seed=11)
+    XT = synth.f32_to_bf16_bits(np.eye(cols, dtype=np.float32))
+    mask = oracle.prune(W, 64, M)
+    Wm = synth.bf16_bits_to_f32(oracle.apply_mask(W, mask, 64, M)).astype(np.float64)
+    Y = gpu_y(W, XT, 64, M, cols)
+    assert np.array_equal(Y, Wm)
+
+
+def test_integer_inputs_exact():
+    """Integer W, X: every product and partial sum is exact in fp32 => Y equals the oracle exactly."""
+    W, XT, Wm = make(128, 400, 64, 5, 64, seed=5, wkind="int", xkind="int")
+    Yref, _ = oracle.gemm_ref(XT, Wm)
+    assert np.array_equal(gpu_y(W, XT, 64, 5, 64), Yref)
+
+
+def test_linearity():
+    """spmm(x1 + x2) == spmm(x1) + spmm(x2) within the tolerance."""
+    rows, cols, T, M = 128, 320, 80, 5
+    W = synth.weights(rows, cols, seed=21)
+    x1 = synth.activations_t(cols, T, seed=22, kind="int")
+    x2 = synth.activations_t(cols, T, seed=23, kind="int")
+    xs = synth.f32_to_bf16_bits(synth.bf16_bits_to_f32(x1) + synth.bf16_bits_to_f32(x2))
+    y = lambda x: gpu_y(W, x, 64, M, T)
+    mask = oracle.prune(W, 64, M)
+    _, A = oracle.gemm_ref(xs, oracle.apply_mask(W, mask, 64, M))
+    assert np.all(np.abs(y(xs) - (y(x1) + y(x2))) <= 2e-3 * A + 1e-6)
+
+
+def test_m4_matches_dense_24():
+    """Pin P6 on the GPU: 64:2:4 SpMM == the plain 2:4 product (W (.) M dense, fp64)."""
+    W, XT, Wm = make(256, 512, 64, 4, 128, seed=31)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, 4, 128), Yref, Aref)
+
+
+def sampled_check(rows, cols, M, T, seed, n=3000, out_dtype=torch.float32):
+    W = synth.weights(rows, cols, seed=seed, kind="outlier")
+    XT = synth.activations_t(cols, T, seed=seed + 1)
+    Wd, Xd = to_dev_bf16(W), to_dev_bf16(XT)
+    P, mask_d = vnm.prune_compress(Wd, 64, M, want_mask=True)
+    Y = vnm.spmm(Xd, P, T=T, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    mask = mask_d.cpu().numpy().view(np.uint32)
+    Wm = oracle.apply_mask(W, mask, 64, M)
+    g = synth.rng(seed + 2)
+    o = g.integers(0, rows, n)
+    t = g.integers(0, T, n)
+    # always include the corners
+    o[:4] = [0, rows - 1, 0, rows - 1]
+    t[:4] = [0, 0, T - 1, T - 1]
+    Yref, Aref = oracle.gemm_ref_sampled(XT, Wm, o, t)
+    Ys = Y.float()[torch.from_numpy(o).cuda(), torch.from_numpy(t).cuda()].cpu().numpy().astype(np.float64)
+    tol = oracle.tolerance(Yref, Aref, y_is_bf16=out_dtype == torch.bfloat16)
+    assert np.all(np.abs(Ys - Yref) <= tol)
+    # and a property that holds everywhere: finite
+    assert torch.isfinite(Y).all()
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 4096), (11008, 4096), (4096, 11008)])
+def test_llama_prefill_sampled(rows, cols):
+    """BJ config 4a at full size (T = 2048, 64:2:5), in the launch configuration bench.py times."""
+    sampled_check(rows, cols, 5, 2048, seed=rows + cols, out_dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8, 16])
+def test_llama_decode_full(T):
+    """BJ config 4b: decode batch 1-16 at 64:2:5, every output compared."""
+    rows, cols = 11008, 4096
+    W = synth.weights(rows, cols, seed=40 + T)
+    XT = synth.activations_t(cols, T, seed=50 + T)
+    mask = oracle.prune(W, 64, 5)
+    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, mask, 64, 5))
+    assert_within(gpu_y(W, XT, 64, 5, T), Yref, Aref)
+
+
+@pytest.mark.parametrize("rows,cols,M", [(1152, 384, 5), (384, 1536, 5), (3072, 768, 8), (768, 3072, 8)])
+def test_deit_sampled(rows, cols, M):
+    """BJ configs 2/3: DeiT-S @64:2:5 and DeiT-B @64:2:8 with T = 197 * 256 tokens."""
+    sampled_check(rows, cols, M, 197 * 256, seed=rows * 3 + cols, out_dtype=torch.bfloat16)
+
+
+def test_determinism():
+    W, XT, _ = make(256, 1000, 64, 5, 300, seed=77)
+    assert np.array_equal(gpu_y(W, XT, 64, 5, 300), gpu_y(W, XT, 64, 5, 300))
