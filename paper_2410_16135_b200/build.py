@@ -18,7 +18,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
 
 LIBS = {
     "libvnm.so": ["api.cpp", "prune.cu", "spmm.cu"],
-    "libvnm_probe.so": ["probes.cu"],
+    "libvnm_probe.so": ["probes.cu", "probes2.cu"],
 }
 
 
