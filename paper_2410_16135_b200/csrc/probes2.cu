@@ -150,43 +150,50 @@ __global__ void probe_gather4_kernel(const __grid_constant__ CUtensorMap tm, con
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) out[i] = s[i];
 }
 
+// MB3b: each CTA streams `iters` stages of 16 KB into a 4-stage ring.  gather: 32 gather4 per stage issued by
+// `lanes` threads (rows from a precomputed random table, 64-col chunk from a cheap hash); else one 2D tile.
 __global__ void __launch_bounds__(32, 1) bench_tma_kernel(const __grid_constant__ CUtensorMap tm, int32_t nrows,
                                                           int32_t ncolchunks, int32_t iters, int32_t gather,
-                                                          unsigned long long* cycles) {
+                                                          int32_t lanes, unsigned long long* cycles) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t bars[4];
-    if (threadIdx.x != 0) return;
+    __shared__ int32_t table[4096];
     uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    for (int s = 0; s < 4; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-    uint32_t h = 0x9E3779B9u * (blockIdx.x + 1);
+    const int lane = threadIdx.x;
+    for (int i = lane; i < 4096; i += 32) {
+        uint32_t h = (i + 1) * 2654435761u ^ (blockIdx.x * 40503u);
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        table[i] = static_cast<int32_t>(h % static_cast<uint32_t>(nrows));
+    }
+    if (lane == 0) {
+        for (int s = 0; s < 4; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const uint32_t cmask = static_cast<uint32_t>(ncolchunks - 1);
     unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
         const int s = it % 4;
         if (it >= 4) mbar_wait(&bars[s], ((it / 4) - 1) & 1);
-        mbar_arrive_expect_tx(&bars[s], 16384);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[s], 16384);
+        __syncwarp();
         uint8_t* dst = buf + s * 16384;
         if (gather) {
-            for (int g = 0; g < 32; ++g) {
-                int32_t r[4];
-                for (int q = 0; q < 4; ++q) {
-                    h = h * 1664525u + 1013904223u;
-                    r[q] = static_cast<int32_t>((h >> 8) % static_cast<uint32_t>(nrows));
-                }
-                h = h * 1664525u + 1013904223u;
-                const int32_t col = static_cast<int32_t>((h >> 8) % static_cast<uint32_t>(ncolchunks)) * 64;
-                tma_gather4(dst + g * 512, &tm, col, r[0], r[1], r[2], r[3], &bars[s]);
+            for (int g = lane; lane < lanes && g < 32; g += lanes) {
+                const int b = (it * 32 + g) * 4;
+                const int32_t col = static_cast<int32_t>(((it * 7 + g * 13) & cmask) * 64);
+                tma_gather4(dst + g * 512, &tm, col, table[b & 4095], table[(b + 1) & 4095], table[(b + 2) & 4095],
+                            table[(b + 3) & 4095], &bars[s]);
             }
-        } else {
-            h = h * 1664525u + 1013904223u;
-            const int32_t r0 = static_cast<int32_t>((h >> 8) % static_cast<uint32_t>(nrows / 128)) * 128;
-            h = h * 1664525u + 1013904223u;
-            const int32_t col = static_cast<int32_t>((h >> 8) % static_cast<uint32_t>(ncolchunks)) * 64;
+        } else if (lane == 0) {
+            const int32_t r0 = static_cast<int32_t>(((it * 2654435761u + blockIdx.x * 97u) >> 7) % static_cast<uint32_t>(nrows / 128)) * 128;
+            const int32_t col = static_cast<int32_t>(((it * 7 + blockIdx.x) & cmask) * 64);
             tma_load_2d(dst, &tm, col, r0, &bars[s]);
         }
+        __syncwarp();
     }
     for (int it = iters > 4 ? iters - 4 : 0; it < iters; ++it) mbar_wait(&bars[it % 4], (it / 4) & 1);
-    cycles[blockIdx.x] = clock64() - t0;
+    if (lane == 0) cycles[blockIdx.x] = clock64() - t0;
 }
 
 __global__ void __launch_bounds__(128, 1) probe_tmem_cp_kernel(uint32_t lbo, uint32_t sbo, uint32_t* out) {
@@ -266,13 +273,13 @@ extern "C" int vnm_probe_gather4(const uint16_t* X, int64_t rows, int64_t cols, 
 }
 
 extern "C" int vnm_probe_bench_tma(const uint16_t* X, int64_t rows, int64_t cols, int32_t iters, int32_t gather,
-                                   uint32_t nblocks, unsigned long long* cycles) {
+                                   int32_t lanes, uint32_t nblocks, unsigned long long* cycles) {
     CUtensorMap tm;
     int e = make_map(&tm, X, rows, cols, 64, gather ? 1 : 128);
     if (e) return 1000 + e;
     cudaFuncSetAttribute(bench_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 16384 + 1024);
     bench_tma_kernel<<<nblocks, 32, 4 * 16384 + 1024>>>(tm, static_cast<int32_t>(rows),
-                                                        static_cast<int32_t>(cols / 64), iters, gather, cycles);
+                                                        static_cast<int32_t>(cols / 64), iters, gather, lanes, cycles);
     return static_cast<int>(cudaGetLastError());
 }
 

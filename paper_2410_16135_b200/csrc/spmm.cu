@@ -3,20 +3,26 @@
 // retained weights and the corresponding tiles of the input matrix B ... align the data layout with
 // that of a 2:4-sparse MM").
 //
-// One CTA computes one output tile = one V-block (V = 64 rows of W) x NT tokens.  K is walked in
-// stages of 32 column blocks (= 4 sparse MMAs of logical K = 32, 8 blocks each):
-//   warp 4     TMA: the stage's A_n tile (64 rows x 64 bf16 = 128 B rows, 128B swizzle, K-major);
-//   warps 0-3  gather: the 4 kept X^T rows of each block (A_i1) -> the stage's B tile, MN-major,
-//              128B swizzle, 16-byte cp.async with zero fill (tokens >= T, channels >= K: padding);
-//              and the 2:4 metadata (A_i2) words -> TMEM in the M=64 sparse-metadata layout;
-//   warp 5     one thread issues tcgen05.mma.sp.cta_group::1.kind::f16 (M=64, N=NT) into a TMEM fp32
-//              accumulator and commits each stage back to the producers;
-//   warps 0-3  epilogue: tcgen05.ld -> fp32 / bf16 -> Y^T rows.
+// Work unit (tile) = one V-block (64 rows of W) x NT tokens.  K is walked in stages of 32 column blocks
+// (4 sparse MMAs of logical K = 32 = 8 blocks each).  Persistent CTAs (one per SM) walk the tiles in
+// token-tile-major order so the CTAs resident at any time share X^T rows in L2.  Warp roles:
+//   warps 8-15 gather: the 4 kept X^T rows of each block (A_i1) -> the stage's B tile, written straight
+//              into the MN-major 128B-swizzled UMMA layout by 16-byte cp.async (zero fill past T tokens and
+//              past the logical channels: the implicit padding of P:107-108); each thread's copies arrive
+//              on the stage barrier asynchronously (cp.async.mbarrier.arrive.noinc).  TMA tile::gather4 was
+//              measured at only 7-15 B/clk/SM (csrc/probes2.cu MB3b) and is not used;
+//   warp 16    TMA: the stage's A_n tile (64 x 64 bf16, 128B swizzle, K-major);
+//   warps 4-7  metadata: A_i2 words -> TMEM in the M=64 sparse-metadata layout (tcgen05.st);
+//   warp 17    one thread issues tcgen05.mma.sp.cta_group::1.kind::f16 M=64 N=NT into TMEM;
+//   warps 0-3  epilogue: tcgen05.ld -> fp32 / bf16 -> Y^T.
+// Two accumulators share TMEM columns: accumulator a (a = tile parity) and its metadata live in lanes
+// 16a..16a+15 of every 32-lane sub-partition, so the epilogue of tile i overlaps the MMAs of tile i+1.
 //
-// TMEM layouts used here were measured on B200 by csrc/probes.cu:
-//   D (M=64):  row m -> lane (m % 16) + 32 * (m / 16), column n.
-//   E (M=64):  the nibble of (row m, K-group g) is nibble 4*((m/8)%2) + g%4 of the 32-bit word at
-//              lane (m % 8) + 8*(g/4) + 32*(m/16), column e_addr + id2 (e_addr even).
+// TMEM layouts (measured on B200 by csrc/probes*.cu):
+//   D (M=64):  row m -> lane 16a + (m % 16) + 32 * (m / 16), column n.
+//   E (M=64):  nibble (row m, K-group g) = nibble 4*((m/8)%2) + g%4 of the word at lane
+//              16a + (m % 8) + 8*(g/4) + 32*(m/16), column e_col + id2 (e_col even).
+//   D and E must carry the same lane offset (0 or 16).
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -28,212 +34,266 @@
 namespace vnm {
 namespace {
 
-constexpr int kV = 64;                       // rows per MMA (V-block)
-constexpr int kBlocksPerStage = 32;          // column blocks per pipeline stage
+constexpr int kV = 64;
+constexpr int kBlocksPerStage = 32;
 constexpr int kMmaPerStage = kBlocksPerStage / 8;
-constexpr int kKRowsPerStage = 4 * kBlocksPerStage;  // gathered X^T rows per stage (128)
-constexpr int kThreads = 192;                // warps 0-3 gather/meta/epilogue, 4 TMA, 5 MMA
+constexpr int kKRowsPerStage = 4 * kBlocksPerStage;  // 128 gathered X^T rows per stage
+constexpr int kGatherWarps = 8;
+constexpr int kEpiWarp0 = 0, kMetaWarp0 = 4, kGatherWarp0 = 8, kProdWarp = 16, kMmaWarp = 17;
+constexpr int kThreads = 32 * 18;
 constexpr uint32_t kMetaCol = 256;
-constexpr uint32_t kABytes = kV * 128;       // 64 rows x 64 bf16
+constexpr uint32_t kABytes = kV * 128;
 
 struct SpmmArgs {
     const uint16_t* XT;
     int64_t ldx;
-    int32_t T;
+    int32_t cols;
     const uint8_t* col_idx;
     const uint32_t* meta;
     void* YT;
     int64_t ldy;
+    int32_t T;
     int32_t y_bf16;
-    int32_t rows, cols, M, nb_pad, ld_meta;
+    int32_t rows, M, nb_pad, ld_meta, nvb, ntt, ntiles;
 };
 
 template <int NT>
 struct Cfg {
     static constexpr int kBBytes = kKRowsPerStage * NT * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kStages = NT == 256 ? 3 : (NT == 128 ? 4 : 6);
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kStages = NT == 256 ? 3 : (NT == 128 ? 5 : 8);
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 512;
 };
 
+// arrive on `bar` once every cp.async this thread issued so far has landed (count pre-set in mbar_init)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <int NT>
-__global__ void __launch_bounds__(kThreads, 1) vnm_spmm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                                                               const SpmmArgs a) {
+__global__ void __launch_bounds__(kThreads, 1)
+    vnm_spmm_kernel(const __grid_constant__ CUtensorMap tmap_a, const SpmmArgs a) {
     using C = Cfg<NT>;
     constexpr int S = C::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;                            // S x 8 KB
-    uint8_t* sB = smem + S * kABytes;              // S x kBBytes
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * kABytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
     uint64_t* empty = full + S;
-    uint64_t* tmem_full = empty + S;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* meta_ready = empty + S;
+    uint64_t* tmem_full = meta_ready + S;  // [2]
+    uint64_t* tmem_empty = tmem_full + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int vb = blockIdx.x;
-    const int n0 = blockIdx.y * NT;
-    const int n_mma = a.ld_meta;                   // nb_pad / 8
+    const int n_mma = a.ld_meta;
     const int n_stage = (n_mma + kMmaPerStage - 1) / kMmaPerStage;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 128 + 1);
+            mbar_init(&full[s], 32 * kGatherWarps + 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&meta_ready[s], 4);
         }
-        mbar_init(tmem_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 4);
+        }
         fence_mbar_init();
     }
-    if (warp == 5) tmem_alloc(tmem_slot, 512);
-    if (warp == 4 && lane == 0) tma_prefetch_desc(&tmap_a);
+    if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
+    if (warp == kProdWarp && lane == 0) tma_prefetch_desc(&tmap_a);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
-        // ------------------------------------------------------------ gather + metadata producers
-        const int t = threadIdx.x;  // 0..127
-        constexpr int kChunks = NT / 8;                  // 16-byte chunks per gathered row
-        constexpr int kRowsPerPass = 128 / kChunks;      // rows covered by one pass of 128 threads
-        const int ch = t % kChunks;
-        const int r_first = t / kChunks;
-        const int nc = ch / 8, cw = ch % 8;              // 64-token chunk, 16-B chunk within it
-        const int tok = n0 + ch * 8;
-        int tok_bytes = (a.T - tok) * 2;
-        tok_bytes = tok_bytes < 0 ? 0 : (tok_bytes > 16 ? 16 : tok_bytes);
-        const uint8_t* ci_vb = a.col_idx + static_cast<int64_t>(vb) * a.nb_pad * 4;
-        // metadata lane role (lanes 0..15 of each 32-lane sub-partition are used for M = 64)
-        const int ml = lane % 16, mh = ml / 8;
-        const int row_a = vb * kV + 16 * warp + (ml % 8), row_b = row_a + 8;
-        const uint32_t* meta_a = a.meta + static_cast<int64_t>(row_a) * a.ld_meta;
-        const uint32_t* meta_b = a.meta + static_cast<int64_t>(row_b) * a.ld_meta;
-        constexpr int LAG = 1;
-        for (int it = 0; it < n_stage; ++it) {
-            const int s = it % S;
-            const uint32_t ph = (it / S) & 1;
-            mbar_wait(&empty[s], ph ^ 1);
-            uint8_t* bst = sB + s * C::kBBytes;
-            const int blk0 = it * kBlocksPerStage;
-#pragma unroll 4
-            for (int r = r_first; r < kKRowsPerStage; r += kRowsPerPass) {
-                const int blk = blk0 + r / 4;
-                const int krow = (blk < a.nb_pad) ? blk * a.M + ci_vb[blk * 4 + (r % 4)] : a.cols;
-                const int bytes = krow < a.cols ? tok_bytes : 0;
-                const uint16_t* src = bytes ? a.XT + static_cast<int64_t>(krow) * a.ldx + tok : a.XT;
-                uint8_t* dst = bst + nc * (kKRowsPerStage * 128) + (r / 8) * 1024 + sw128_offset(r % 8, cw * 16);
-                cp_async_16(dst, src, static_cast<uint32_t>(bytes));
+    if (warp >= kGatherWarp0 && warp < kGatherWarp0 + kGatherWarps) {
+        // ------------------------------------------------------------ gather producers (B = kept X^T rows)
+        // Warp pw owns blocks 4pw..4pw+3 of every stage (gathered rows 16pw..16pw+15); each lane moves 16 B
+        // (8 tokens) per cp.async, zero-filled past T (tokens) and past cols (padded channels).
+        constexpr int CPR = NT / 8;       // 16-byte chunks per gathered row
+        constexpr int RPI = 32 / CPR;     // rows per warp instruction
+        const int pw = warp - kGatherWarp0;
+        const int sub = lane / CPR, ch = lane % CPR;
+        const uint32_t dst_chunk = (ch / 8) * (kKRowsPerStage * 128);
+        int q = 0;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+            const int vb = tile % a.nvb, n0 = (tile / a.nvb) * NT;
+            const uint32_t* ci_vb = reinterpret_cast<const uint32_t*>(a.col_idx) + static_cast<int64_t>(vb) * a.nb_pad;
+            int tok_bytes = (a.T - (n0 + 8 * ch)) * 2;
+            tok_bytes = tok_bytes < 0 ? 0 : (tok_bytes > 16 ? 16 : tok_bytes);
+            const uint16_t* xt_tok = a.XT + n0 + 8 * ch;
+            for (int ks = 0; ks < n_stage; ++ks, ++q) {
+                const int s = q % S;
+                const uint32_t ph = (q / S) & 1;
+                const int blk_l = ks * kBlocksPerStage + 4 * pw + (lane & 3);
+                const uint32_t ci = (blk_l < a.nb_pad) ? __ldg(ci_vb + blk_l) : 0xFFFFFFFFu;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* bst = sB + s * C::kBBytes + dst_chunk;
+#pragma unroll
+                for (int it = 0; it < 16 / RPI; ++it) {
+                    const int rl = it * RPI + sub;             // 0..15 within the warp's rows
+                    const int r = 16 * pw + rl;                // gathered row of the stage (0..127)
+                    const uint32_t cw = __shfl_sync(0xffffffffu, ci, rl >> 2);
+                    const int blk = ks * kBlocksPerStage + (r >> 2);
+                    const int krow = blk * a.M + static_cast<int>((cw >> (8 * (r & 3))) & 0xFFu);
+                    const bool ok = cw != 0xFFFFFFFFu && krow < a.cols;
+                    const int bytes = ok ? tok_bytes : 0;
+                    const uint16_t* src = bytes ? xt_tok + static_cast<int64_t>(krow) * a.ldx : a.XT;
+                    cp_async_16(bst + (r >> 3) * 1024 + sw128_offset(r & 7, (ch & 7) * 16), src,
+                                static_cast<uint32_t>(bytes));
+                }
+                cp_async_arrive_noinc(&full[s]);
             }
-            cp_async_commit();
-            // metadata of the stage's (up to) 4 MMAs -> TMEM columns kMetaCol + 4 s + k
-            {
+        }
+    } else if (warp == kProdWarp) {
+        // ------------------------------------------------------------ TMA producer (A_n)
+        if (lane == 0) {
+            int q = 0;
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+                const int vb = tile % a.nvb;
+                for (int ks = 0; ks < n_stage; ++ks, ++q) {
+                    const int s = q % S;
+                    const uint32_t ph = (q / S) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], kABytes);
+                    tma_load_2d(sA + s * kABytes, &tmap_a, ks * (2 * kBlocksPerStage), vb * kV, &full[s]);
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int q = 0, tl = 0;
+            const uint32_t idesc0 = idesc_bf16(64, NT, true, 0, true);
+            const uint32_t idesc1 = idesc_bf16(64, NT, true, 1, true);
+            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tl) {
+                const int acc = tl & 1;
+                const uint32_t aph = (tl >> 1) & 1;
+                mbar_wait(&tmem_empty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + ((16u * acc) << 16);
+                for (int ks = 0; ks < n_stage; ++ks, ++q) {
+                    const int s = q % S;
+                    const uint32_t ph = (q / S) & 1;
+                    mbar_wait(&full[s], ph);
+                    mbar_wait(&meta_ready[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + s * kABytes);
+                    const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < kMmaPerStage; ++k) {
+                        const int mi = ks * kMmaPerStage + k;
+                        if (mi < n_mma) {
+                            const uint64_t ad = sdesc(a_base + 32 * k, 16, 1024, kLayoutSW128);
+                            const uint64_t bd = sdesc(b_base + 4096 * k, kKRowsPerStage * 128, 1024, kLayoutSW128);
+                            const uint32_t e = d_tmem + kMetaCol + 4 * s + (k & ~1);
+                            mma_sp_bf16(d_tmem, ad, bd, e, (k & 1) ? idesc1 : idesc0, mi > 0 ? 1u : 0u);
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tmem_full[acc]);
+            }
+        }
+    } else if (warp >= kMetaWarp0 && warp < kMetaWarp0 + 4) {
+        // ------------------------------------------------------------ metadata -> TMEM
+        // The slot of stage s is reused only after the MMAs that read it completed (empty[s]); lanes of the
+        // other accumulator's half are written with a don't-care pattern (no in-flight MMA reads slot s).
+        const int qd = warp - kMetaWarp0;  // TMEM sub-partition (== warp % 4)
+        const int ml = lane % 16, mh = ml / 8;
+        int q = 0, tl = 0;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tl) {
+            const int vb = tile % a.nvb;
+            const int acc = tl & 1;
+            const int row_a = vb * kV + 16 * qd + (ml % 8);
+            const uint32_t* ma = a.meta + static_cast<int64_t>(row_a) * a.ld_meta;
+            const uint32_t* mb = ma + 8 * static_cast<int64_t>(a.ld_meta);
+            const bool mine = (lane / 16) == acc;  // lanes 16*acc .. +15 carry this tile's metadata
+            for (int ks = 0; ks < n_stage; ++ks, ++q) {
+                const int s = q % S;
+                const uint32_t ph = (q / S) & 1;
                 uint32_t w[kMmaPerStage];
 #pragma unroll
                 for (int k = 0; k < kMmaPerStage; ++k) {
-                    const int mi = it * kMmaPerStage + k;
+                    const int mi = ks * kMmaPerStage + k;
                     uint32_t wa = 0x44444444u, wb = 0x44444444u;
-                    if (mi < n_mma) {
-                        wa = __ldg(meta_a + mi);
-                        wb = __ldg(meta_b + mi);
+                    if (mine && mi < n_mma) {
+                        wa = __ldg(ma + mi);
+                        wb = __ldg(mb + mi);
                     }
                     w[k] = ((wa >> (16 * mh)) & 0xFFFFu) | (((wb >> (16 * mh)) & 0xFFFFu) << 16);
-                    if (lane >= 16) w[k] = 0x44444444u;
                 }
-                tmem_st_32x32b_x4(tmem + ((32 * warp) << 16) + kMetaCol + 4 * s, w[0], w[1], w[2], w[3]);
-                tmem_wait_st();
-            }
-            if (it >= LAG) {
-                cp_async_wait<LAG>();
-                fence_proxy_async_smem();
-                tc_fence_before();
-                mbar_arrive(&full[(it - LAG) % S]);
-            }
-        }
-        cp_async_wait<0>();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        for (int it = n_stage - LAG < 0 ? 0 : n_stage - LAG; it < n_stage; ++it) mbar_arrive(&full[it % S]);
-
-        // ------------------------------------------------------------ epilogue
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-        const int row = vb * kV + 16 * warp + lane;  // valid for lane < 16
-        const bool row_ok = lane < 16 && row < a.rows;
-#pragma unroll 1
-        for (int c = 0; c < NT; c += 16) {
-            uint32_t v[16];
-            tmem_ld_32x32b_x16(tmem + ((32 * warp) << 16) + c, v);
-            tmem_wait_ld();
-            const int tcol = n0 + c;
-            if (row_ok && tcol < a.T) {
-                if (!a.y_bf16) {
-                    float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
-                    if (tcol + 16 <= a.T) {
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            reinterpret_cast<uint4*>(y)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                    } else {
-                        for (int q = 0; q < 16 && tcol + q < a.T; ++q) y[q] = __uint_as_float(v[q]);
-                    }
-                } else {
-                    uint16_t* y = reinterpret_cast<uint16_t*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
-                    uint32_t pk[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
-                        pk[q] = *reinterpret_cast<uint32_t*>(&h);
-                    }
-                    if (tcol + 16 <= a.T) {
-                        reinterpret_cast<uint4*>(y)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                        reinterpret_cast<uint4*>(y)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                    } else {
-                        for (int q = 0; q < 16 && tcol + q < a.T; ++q)
-                            y[q] = static_cast<uint16_t>((pk[q / 2] >> (16 * (q % 2))) & 0xFFFFu);
-                    }
-                }
-            }
-        }
-    } else if (warp == 4) {
-        // ------------------------------------------------------------ TMA producer for A_n
-        if (lane == 0) {
-            for (int it = 0; it < n_stage; ++it) {
-                const int s = it % S;
-                const uint32_t ph = (it / S) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], kABytes);
-                tma_load_2d(sA + s * kABytes, &tmap_a, it * (2 * kBlocksPerStage), vb * kV, &full[s]);
+                tmem_st_32x32b_x4(tmem + ((32 * qd) << 16) + kMetaCol + 4 * s, w[0], w[1], w[2], w[3]);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&meta_ready[s]);
             }
         }
-    } else {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc0 = idesc_bf16(64, NT, true, 0, true);
-            const uint32_t idesc1 = idesc_bf16(64, NT, true, 1, true);
-            for (int it = 0; it < n_stage; ++it) {
-                const int s = it % S;
-                const uint32_t ph = (it / S) & 1;
-                mbar_wait(&full[s], ph);
-                tc_fence_after();
-                const uint32_t a_base = smem_u32(sA + s * kABytes);
-                const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
+    } else if (warp < kEpiWarp0 + 4) {
+        // ------------------------------------------------------------ epilogue
+        const int qd = warp - kEpiWarp0;
+        int tl = 0;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tl) {
+            const int vb = tile % a.nvb, n0 = (tile / a.nvb) * NT;
+            const int acc = tl & 1;
+            const uint32_t aph = (tl >> 1) & 1;
+            mbar_wait(&tmem_full[acc], aph);
+            tc_fence_after();
+            const bool mine = (lane / 16) == acc;
+            const int row = vb * kV + 16 * qd + (lane % 16);
+            const bool row_ok = mine && row < a.rows;
+#pragma unroll 1
+            for (int c = 0; c < NT; c += 16) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + c, v);
+                tmem_wait_ld();
+                const int tcol = n0 + c;
+                if (row_ok && tcol < a.T) {
+                    if (!a.y_bf16) {
+                        float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
+                        if (tcol + 16 <= a.T) {
 #pragma unroll
-                for (int k = 0; k < kMmaPerStage; ++k) {
-                    const int mi = it * kMmaPerStage + k;
-                    if (mi < n_mma) {
-                        const uint64_t ad = sdesc(a_base + 32 * k, 16, 1024, kLayoutSW128);
-                        const uint64_t bd = sdesc(b_base + 4096 * k, kKRowsPerStage * 128, 1024, kLayoutSW128);
-                        const uint32_t e = tmem + kMetaCol + 4 * s + (k & ~1);
-                        mma_sp_bf16(tmem, ad, bd, e, (k & 1) ? idesc1 : idesc0, mi > 0 ? 1u : 0u);
+                            for (int k = 0; k < 4; ++k)
+                                reinterpret_cast<uint4*>(y)[k] =
+                                    make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+                                if (tcol + k < a.T) y[k] = __uint_as_float(v[k]);
+                        }
+                    } else {
+                        uint16_t* y = reinterpret_cast<uint16_t*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            __nv_bfloat162 h =
+                                __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                            pk[k] = *reinterpret_cast<uint32_t*>(&h);
+                        }
+                        if (tcol + 16 <= a.T) {
+                            reinterpret_cast<uint4*>(y)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                            reinterpret_cast<uint4*>(y)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+                                if (tcol + k < a.T) y[k] = static_cast<uint16_t>((pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+                        }
                     }
                 }
-                mma_commit(&empty[s]);
             }
-            mma_commit(tmem_full);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[acc]);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) tmem_dealloc(tmem, 512);
+    if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------------ host side
@@ -253,13 +313,38 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+bool encode_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+               uint32_t box_inner, uint32_t box_outer) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NT>
-int launch_nt(const SpmmLaunch& L, const CUtensorMap& tm, const SpmmArgs& a, cudaStream_t st) {
+int launch_nt(const SpmmLaunch& L, const CUtensorMap& ta, SpmmArgs a, cudaStream_t st) {
     auto k = vnm_spmm_kernel<NT>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NT>::kSmem) != cudaSuccess)
         return kLaunchCudaError;
-    dim3 grid(L.P->g.rows_p / kV, (L.T + NT - 1) / NT);
-    k<<<grid, kThreads, Cfg<NT>::kSmem, st>>>(tm, a);
+    a.ntt = (L.T + NT - 1) / NT;
+    a.ntiles = a.nvb * a.ntt;
+    const int grid = a.ntiles < num_sms() ? a.ntiles : num_sms();
+    k<<<grid, kThreads, Cfg<NT>::kSmem, st>>>(ta, a);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
@@ -276,35 +361,31 @@ int launch_spmm(const SpmmLaunch& L, cudaStream_t stream) {
         return cudaMemset2DAsync(L.YT, static_cast<size_t>(L.ldy) * es, 0, static_cast<size_t>(L.T) * es, g.rows,
                                  stream) == cudaSuccess ? 0 : kLaunchCudaError;
     }
-    EncodeTiledFn enc = get_encode();
-    if (!enc) return kLaunchCudaError;
-    // A_n tensor map: [rows_p][ld_val] bf16, box 64 values x 64 rows, 128B swizzle
-    CUtensorMap tm;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.ld_val), static_cast<cuuint64_t>(g.rows_p)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ld_val) * 2};
-    cuuint32_t box[2] = {64, 64};
-    cuuint32_t estr[2] = {1, 1};
-    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, L.P->values, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    // A_n: [rows_p][ld_val] bf16, box 64 values x 64 rows, 128B swizzle (values past ld_val zero-filled).
+    CUtensorMap ta;
+    if (!encode_2d(&ta, L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
+                   static_cast<uint64_t>(g.ld_val) * 2, 64, 64))
         return kLaunchCudaError;
     SpmmArgs a;
     a.XT = L.XT;
     a.ldx = L.ldx;
-    a.T = L.T;
+    a.cols = g.cols;
     a.col_idx = L.P->col_idx;
     a.meta = L.P->meta;
     a.YT = L.YT;
     a.ldy = L.ldy;
+    a.T = L.T;
     a.y_bf16 = L.y_dtype == VNM_BF16;
     a.rows = g.rows;
-    a.cols = g.cols;
     a.M = g.M;
     a.nb_pad = g.nb_pad;
     a.ld_meta = g.ld_meta;
-    if (L.T > 128) return launch_nt<256>(L, tm, a, stream);
-    if (L.T > 64) return launch_nt<128>(L, tm, a, stream);
-    return launch_nt<64>(L, tm, a, stream);
+    a.nvb = g.rows_p / kV;
+    a.ntt = 0;
+    a.ntiles = 0;
+    if (L.T > 128) return launch_nt<256>(L, ta, a, stream);
+    if (L.T > 64) return launch_nt<128>(L, ta, a, stream);
+    return launch_nt<64>(L, ta, a, stream);
 }
 
 }  // namespace vnm

@@ -20,7 +20,7 @@ def load():
     L.vnm_probe_interleave.argtypes = [P, P, P, P, u32, u32]
     L.vnm_probe_bench_mma_multi.argtypes = [u32, u32, u32, u32, u32, u32, P]
     L.vnm_probe_gather4.argtypes = [P, i64, i64, u32, P, i32, P]
-    L.vnm_probe_bench_tma.argtypes = [P, i64, i64, i32, i32, u32, P]
+    L.vnm_probe_bench_tma.argtypes = [P, i64, i64, i32, i32, i32, u32, P]
     L.vnm_probe_tmem_cp.argtypes = [u32, u32, P]
     return L
 
@@ -37,7 +37,10 @@ def interleave(L):
     B = bf16(Bn)
     A = bf16(np.tile(np.arange(1, 129, dtype=np.float32)[:, None], (1, 16)))
     E = torch.full((128, 4), 0x44444444, dtype=torch.int64).to(torch.int32).cuda()
-    for d_lane, e_lane in [(0, 0), (16, 0), (16, 16), (0, 16)]:
+    cfgs = [(0, 0), (16, 0), (16, 16), (0, 16)]
+    if len(sys.argv) > 2:
+        cfgs = [cfgs[int(sys.argv[2])]]
+    for d_lane, e_lane in cfgs:
         D = torch.zeros(128, 64, dtype=torch.float32, device="cuda")
         st = L.vnm_probe_interleave(A.data_ptr(), B.data_ptr(), E.data_ptr(), D.data_ptr(), d_lane, e_lane)
         torch.cuda.synchronize()
@@ -53,9 +56,9 @@ def interleave(L):
 def mma_multi(L):
     out = []
     nblk = torch.cuda.get_device_properties(0).multi_processor_count
-    for (m, n, nacc, mode) in [(64, 256, 1, 0), (64, 256, 2, 1), (64, 128, 1, 0), (64, 128, 2, 0), (64, 128, 4, 0),
-                               (64, 128, 2, 1), (64, 64, 4, 0), (64, 64, 2, 1), (128, 256, 1, 0), (128, 128, 2, 0),
-                               (64, 16, 4, 0), (64, 32, 4, 0)]:
+    for (m, n, nacc, mode) in [(64, 256, 1, 0), (64, 128, 1, 0), (64, 128, 2, 0), (64, 128, 4, 0),
+                               (64, 64, 1, 0), (64, 64, 4, 0), (128, 256, 1, 0), (128, 128, 2, 0), (128, 128, 1, 0),
+                               (64, 16, 4, 0), (64, 32, 4, 0), (64, 16, 1, 0), (64, 256, 2, 0)]:
         cyc = torch.zeros(nblk, dtype=torch.int64, device="cuda")
         iters = 4096
         L.vnm_probe_bench_mma_multi(m, n, 64, nacc, mode, nblk, cyc.data_ptr())
@@ -69,7 +72,7 @@ def mma_multi(L):
         r = {"M": m, "N": n, "nacc": nacc, "mode": mode, "status": st,
              "cycles_per_mma": float(np.median(cyc.cpu().numpy())) / iters,
              "effectual_tflops": 2.0 * m * n * 16 * iters * nblk / ms / 1e9}
-        print(json.dumps(r))
+        print(json.dumps(r), flush=True)
         out.append(r)
     return out
 
@@ -106,22 +109,22 @@ def tma_bw(L):
     nblk = torch.cuda.get_device_properties(0).multi_processor_count
     for (rows, cols, label) in [(4096, 2048, "l2_16MB"), (65536, 2048, "hbm_256MB")]:
         X = torch.randn(rows, cols, device="cuda").to(torch.bfloat16)
-        for gather in (1, 0):
+        for gather, lanes in ((1, 1), (1, 8), (1, 32), (0, 1)):
             for ctas in (nblk, 2 * nblk):
                 cyc = torch.zeros(ctas, dtype=torch.int64, device="cuda")
                 iters = 512
-                L.vnm_probe_bench_tma(X.data_ptr(), rows, cols, 16, gather, ctas, cyc.data_ptr())
+                L.vnm_probe_bench_tma(X.data_ptr(), rows, cols, 16, gather, lanes, ctas, cyc.data_ptr())
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                st = L.vnm_probe_bench_tma(X.data_ptr(), rows, cols, iters, gather, ctas, cyc.data_ptr())
+                st = L.vnm_probe_bench_tma(X.data_ptr(), rows, cols, iters, gather, lanes, ctas, cyc.data_ptr())
                 e1.record()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1)
                 gbs = ctas * iters * 16384 / ms / 1e6
-                r = {"src": label, "gather4": gather, "ctas": ctas, "status": st, "GBps": round(gbs, 1),
+                r = {"src": label, "gather4": gather, "lanes": lanes, "ctas": ctas, "status": st, "GBps": round(gbs, 1),
                      "bytes_per_cycle_per_sm": round(ctas * iters * 16384 / float(np.median(cyc.cpu().numpy())) / nblk, 2)}
-                print(json.dumps(r))
+                print(json.dumps(r), flush=True)
                 res.append(r)
     return res
 
@@ -147,7 +150,8 @@ def main():
     mode = sys.argv[1]
     r = globals()[mode](L)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    json.dump(r, open(os.path.join(ROOT, "gpurun_out", f"probe2_{mode}.json"), "w"), indent=1)
+    tag = mode + ("_" + sys.argv[2] if len(sys.argv) > 2 else "")
+    json.dump(r, open(os.path.join(ROOT, "gpurun_out", f"probe2_{tag}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
