@@ -164,11 +164,19 @@ def run_gpu(args):
 
     import ctypes
 
+    use_tc = T > 64 and M <= 8 and V == 64
+    if use_tc:
+        for l in layers:
+            vnm.pack_tc(l["P"])  # allocates the window-form buffers once; refilled inside every step
+
     def prune_compress(l):
         cp = l["P"].c()
         st = L.vnm_prune_compress(ctypes.c_void_p(l["W"].data_ptr()), l["W"].stride(0), None, 0,
                                   ctypes.byref(l["P"].g), ctypes.byref(cp), None, ctypes.c_void_p(stream.cuda_stream))
         assert st == 0, vnm.status_string(st)
+        if use_tc:
+            st = L.vnm_pack_tc(ctypes.byref(cp), ctypes.c_void_p(stream.cuda_stream))
+            assert st == 0, vnm.status_string(st)
 
     def spmm(l):
         cp = l["P"].c()

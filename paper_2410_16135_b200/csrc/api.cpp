@@ -14,6 +14,10 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
+// below this many tokens the weights dominate the traffic: the gather plan reads A_n (2 values / block),
+// the window plan 4 values / block
+constexpr int32_t kTcMinTokens = 64;
+
 bool is_pow2(int32_t v) { return v > 0 && (v & (v - 1)) == 0; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 int32_t ceil_to(int32_t a, int32_t m) { return ((a + m - 1) / m) * m; }
@@ -94,6 +98,15 @@ size_t vnm_bytes(const vnm_geom* g, int which) {
         case 1: return rp / static_cast<size_t>(g->V) * static_cast<size_t>(g->nb_pad) * 4;
         case 2: return rp * static_cast<size_t>(g->ld_meta) * 4;
         case 3: return rp * static_cast<size_t>(g->ld_mask) * 4;
+        case 4:
+        case 5: {
+            if (g->V != 64 || g->M > 8) return 0;
+            const size_t rows_w = (rp + 127) / 128 * 128;
+            const size_t bpm = g->M == 4 ? 8 : 4;
+            const size_t n_mma = static_cast<size_t>(g->nb_pad) / bpm;
+            const size_t n_stage = (n_mma + 3) / 4;
+            return which == 4 ? rows_w * 16 * n_mma * 2 : rows_w / 128 * n_stage * 128 * 4 * 4;
+        }
         default: return 0;
     }
 }
@@ -144,6 +157,19 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
     return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream) {
+    if (!P) return VNM_ERR_ARG;
+    const vnm_geom* g = &P->g;
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if ((s = check_packed(P, g))) return s;
+    if (g->V != 64 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
+    if (!P->values_tc || !P->meta_tc) return VNM_ERR_ARG;
+    if (!aligned16(P->values_tc) || !aligned16(P->meta_tc)) return VNM_ERR_ALIGN;
+    return from_launch(vnm::launch_pack_tc(*P, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,
                     vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
     if (!P) return VNM_ERR_ARG;
@@ -160,6 +186,9 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     if ((XT && !aligned16(XT)) || !aligned16(YT) || (ldx % 8) != 0 || (ldy % 8) != 0) return VNM_ERR_ALIGN;
     if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
     vnm::SpmmLaunch L{P, XT, ldx, T, YT, ldy, y_dtype, workspace, workspace ? workspace_bytes : 0};
+    const bool tc = P->values_tc && P->meta_tc && g->M <= 8 && g->nb_pad > 0 && T > kTcMinTokens;
+    if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
+    if (tc) return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 

@@ -287,3 +287,82 @@ extern "C" int vnm_probe_tmem_cp(uint32_t lbo, uint32_t sbo, uint32_t* out) {
     probe_tmem_cp_kernel<<<1, 128>>>(lbo, sbo, out);
     return static_cast<int>(cudaGetLastError());
 }
+
+// =====================================================================================================
+// Window probe: one sparse MMA (M = m_mma, N = 64) whose B descriptor walks K-groups of 8 rows with a
+// caller-chosen stride: B is a dense [krows x 64] tile (MN-major), either 128B-swizzled with the swizzle
+// phase taken from the ABSOLUTE row (as a TMA tile load writes it; layout 2, K-group stride = sbo) or
+// unswizzled core matrices [8-token chunk][k-row][16 B] (layout 0, K-group stride = lbo).
+// =====================================================================================================
+namespace {
+__global__ void __launch_bounds__(128, 1)
+    probe_window_kernel(const uint16_t* __restrict__ A_in,  // [128][16]
+                        const uint16_t* __restrict__ B_in,  // [krows][64]
+                        const uint32_t* __restrict__ E_in,  // [128][4]
+                        float* __restrict__ D_out,          // [128][64]
+                        uint32_t m_mma, uint32_t krows, uint32_t layout, uint32_t lbo, uint32_t sbo,
+                        uint32_t base_off, uint32_t start_row) {
+    __shared__ __align__(1024) uint8_t sA[128 * 128];
+    __shared__ __align__(1024) uint8_t sB[16384];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const uint32_t tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    for (uint32_t i = tid; i < sizeof(sA) / 4; i += 128) reinterpret_cast<uint32_t*>(sA)[i] = 0;
+    for (uint32_t i = tid; i < sizeof(sB) / 4; i += 128) reinterpret_cast<uint32_t*>(sB)[i] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < 128 * 16; i += 128) {
+        uint32_t m = i / 16, j = i % 16;
+        *reinterpret_cast<uint16_t*>(sA + (m / 8) * 1024 + sw128_offset(m % 8, 2 * j)) = A_in[i];
+    }
+    for (uint32_t i = tid; i < krows * 64; i += 128) {
+        uint32_t k = i / 64, n = i % 64;
+        uint32_t off;
+        if (layout == 2) off = (k / 8) * 1024 + sw128_offset(k % 8, 2 * n);        // row k at 128*k, phase k%8
+        else off = (n / 8) * (krows * 16) + k * 16 + (n % 8) * 2;                  // [chunk][k][8 tokens]
+        *reinterpret_cast<uint16_t*>(sB + off) = B_in[i];
+    }
+    fence_proxy_async_smem();
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc(&tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = tmem_base;
+    {
+        const uint32_t* e = E_in + (warp * 32 + lane) * 4;
+        tmem_st_32x32b_x4(tbase + ((warp * 32) << 16) + kMetaCol2, e[0], e[1], e[2], e[3]);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+        const uint64_t ad = sdesc(smem_u32(sA), 16, 1024, kLayoutSW128);
+        uint64_t bd = sdesc(smem_u32(sB) + start_row * (layout == 2 ? 128u : 16u), lbo, sbo, layout);
+        bd |= static_cast<uint64_t>(base_off & 7u) << 49;
+        mma_sp_bf16(tbase, ad, bd, tbase + kMetaCol2, idesc_bf16(m_mma, 64, true, 0, true), 0);
+        mma_commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    tc_fence_after();
+    for (uint32_t c = 0; c < 64; c += 16) {
+        uint32_t r[16];
+        tmem_ld_32x32b_x16(tbase + ((warp * 32) << 16) + c, r);
+        tmem_wait_ld();
+        for (int i = 0; i < 16; ++i) D_out[(warp * 32 + lane) * 64 + c + i] = __uint_as_float(r[i]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+
+extern "C" int vnm_probe_window(const uint16_t* A_in, const uint16_t* B_in, const uint32_t* E_in, float* D_out,
+                                uint32_t m_mma, uint32_t krows, uint32_t layout, uint32_t lbo, uint32_t sbo,
+                                uint32_t base_off, uint32_t start_row) {
+    probe_window_kernel<<<1, 128>>>(A_in, B_in, E_in, D_out, m_mma, krows, layout, lbo, sbo, base_off, start_row);
+    return static_cast<int>(cudaGetLastError());
+}

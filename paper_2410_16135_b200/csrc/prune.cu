@@ -189,25 +189,43 @@ __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a)
                 }
             }
             uint32_t km = (1u << ti[0]) | (1u << ti[1]) | (1u << ti[2]) | (1u << ti[3]);
-            int kept[4];
+            uint32_t kp = 0;  // kept columns ascending, 8 bits each
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { kept[q] = __ffs(km) - 1; km &= km - 1; }
-            // step 3: per row top-2 of the kept 4 (ties -> smaller position)
+            for (int q = 0; q < 4; ++q) { kp |= static_cast<uint32_t>(__ffs(km) - 1) << (8 * q); km &= km - 1; }
+            // step 3: per row top-2 of the kept 4 (ties -> smaller position), branch-free: key = (e, 3 - pos)
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
                 const int r = rbase + j + Lb * i;
-                float e4[4];
+                const uint16_t* wr = sW + r * pitch_w + bl * M;
+                uint16_t w4[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    e4[q] = HAS_SCORE ? fabsf(sS[r * pitch_s + bl * M + kept[q]])
-                                      : bf16_abs_to_f32(sW[r * pitch_w + bl * M + kept[q]]);
-                int f = 0;
+                for (int q = 0; q < 4; ++q) w4[q] = wr[(kp >> (8 * q)) & 0xFFu];
+                int f, sc;
+                if (HAS_SCORE) {
+                    const float* sr = sS + r * pitch_s + bl * M;
+                    unsigned long long k[4];
 #pragma unroll
-                for (int q = 1; q < 4; ++q) if (e4[q] > e4[f]) f = q;
-                int sc = (f == 0) ? 1 : 0;
+                    for (int q = 0; q < 4; ++q)
+                        k[q] = (static_cast<unsigned long long>(__float_as_uint(fabsf(sr[(kp >> (8 * q)) & 0xFFu]))) << 2) |
+                               static_cast<unsigned long long>(3 - q);
+                    const unsigned long long m01 = k[0] > k[1] ? k[0] : k[1], n01 = k[0] > k[1] ? k[1] : k[0];
+                    const unsigned long long m23 = k[2] > k[3] ? k[2] : k[3], n23 = k[2] > k[3] ? k[3] : k[2];
+                    const unsigned long long k1 = m01 > m23 ? m01 : m23;
+                    const unsigned long long lo2 = m01 > m23 ? m23 : m01, hi2 = n01 > n23 ? n01 : n23;
+                    const unsigned long long k2 = lo2 > hi2 ? lo2 : hi2;
+                    f = 3 - static_cast<int>(k1 & 3u);
+                    sc = 3 - static_cast<int>(k2 & 3u);
+                } else {
+                    uint32_t k[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) if (q != f && e4[q] > e4[sc]) sc = q;
-                rowbits[i] = (1u << kept[f]) | (1u << kept[sc]);
+                    for (int q = 0; q < 4; ++q) k[q] = (static_cast<uint32_t>(w4[q] & 0x7FFFu) << 2) | (3u - q);
+                    const uint32_t m01 = max(k[0], k[1]), n01 = min(k[0], k[1]);
+                    const uint32_t m23 = max(k[2], k[3]), n23 = min(k[2], k[3]);
+                    const uint32_t k1 = max(m01, m23), k2 = max(min(m01, m23), max(n01, n23));
+                    f = 3 - static_cast<int>(k1 & 3u);
+                    sc = 3 - static_cast<int>(k2 & 3u);
+                }
+                rowbits[i] = (1u << ((kp >> (8 * f)) & 0xFFu)) | (1u << ((kp >> (8 * sc)) & 0xFFu));
                 uni |= rowbits[i];
             }
         } else {

@@ -1,0 +1,350 @@
+// spmm_tc.cu — the V:N:M SpMM in the tensor-core "window" form (include/vnm.h values_tc / meta_tc,
+// DESIGN.md §6), for V = 64 and 4 <= M <= 8 at prefill-sized T.
+//
+// Why a second formulation.  On B200 the M = 64 sparse MMA (one V-block) runs at half the M = 128 rate
+// (csrc/probes.cu MB2), and gathering each V-block's 4 kept X^T rows per block (App. A) is bound by
+// the gather path (TMA gather4 7-15 B/clk/SM, cp.async ~27 B/clk/SM: MB3b) rather than by the MMA.  Here
+// every V x M block is an 8-channel window of the DENSE X^T tile — the sparse MMA's K-group stride is set
+// to M rows (UMMA SBO = M * 128 B; measured exact, probes2.cu "window") — so one X^T tile loaded by plain
+// 2D TMA serves all output rows: M = 128 MMAs (two V-blocks), the tile multicast across a CTA cluster.
+// Cost in tensor-core work: 8 logical K per block instead of 4, i.e. the same MMA time as the M = 64 gather
+// plan (2x K at 2x rate) for 5 <= M <= 8, with no gather at all.
+//
+// Tile = 128 output rows x NT = 192 tokens; stage = 4 MMAs (16 blocks, or 32 for M = 4).  Per CTA:
+//   warp 0     TMA: A (values_tc 128 x 64 bf16) and the stage's metadata chunk (2 KB bulk copy), plus this
+//              CTA's slice of the dense X^T tile, multicast to every CTA of the cluster;
+//   warp 1     MMA: tcgen05.cp (metadata smem -> TMEM) then 4 x tcgen05.mma.sp M=128 N=192; commits free
+//              the stage in every CTA of the cluster (multicast arrive);
+//   warps 4-7  epilogue: TMEM -> fp32 / bf16 -> Y^T (double-buffered accumulators in TMEM).
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "vnm_internal.h"
+
+namespace vnm {
+namespace {
+
+constexpr int kNT = 192;                 // tokens per tile (3 x 64-token TMA chunks)
+constexpr int kChunks = kNT / 64;
+constexpr int kThreads = 256;
+constexpr uint32_t kMetaCol = 2 * kNT;   // TMEM: acc0 [0,192), acc1 [192,384), metadata from 384
+constexpr uint32_t kABytes = 128 * 128;  // 128 rows x 64 bf16
+constexpr uint32_t kEBytes = 128 * 16;   // 128 lanes x 4 words
+
+struct TcArgs {
+    const uint32_t* meta_tc;
+    void* YT;
+    int64_t ldy;
+    int32_t T, y_bf16, rows, M;
+    int32_t n_mma, n_stage, n_rt, n_tt, n_rg, work;
+    int32_t rows_stage;  // dense X^T rows advanced per stage
+    int32_t rb;          // B rows per stage per chunk (multiple of 8 * CS)
+    int32_t stages;      // pipeline depth
+    uint32_t b_stage_bytes, stage_bytes;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* tmap, int32_t x, int32_t y, uint64_t* bar,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, "
+        "{%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t d) {
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+template <int CS>
+__global__ void __launch_bounds__(kThreads, 1)
+    vnm_spmm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                       const TcArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = a.stages;
+    // per stage: [A 16 KB][B chunks][E 2 KB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * a.stage_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* tmem_full = empty + S;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = CS > 1 ? cluster_rank() : 0u;
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    const uint16_t all = static_cast<uint16_t>((1u << CS) - 1u);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CS);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmap_a);
+        tma_prefetch_desc(&tmap_b);
+    }
+    tc_fence_before();
+    if (CS > 1) cluster_sync_all(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int rb_rank = a.rb / CS;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int q = 0;
+            for (int w = cid; w < a.work; w += ncl) {
+                const int tt = w / a.n_rg, rt = (w % a.n_rg) * CS + static_cast<int>(rank);
+                const int n0 = tt * kNT;
+                for (int st = 0; st < a.n_stage; ++st, ++q) {
+                    const int s = q % S;
+                    const uint32_t ph = (q / S) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* base = smem + s * a.stage_bytes;
+                    mbar_arrive_expect_tx(&full[s], kABytes + kEBytes + a.b_stage_bytes);
+                    tma_load_2d(base, &tmap_a, st * 64, rt * 128, &full[s]);
+                    const uint32_t* esrc = a.meta_tc + (static_cast<int64_t>(rt < a.n_rt ? rt : 0) * a.n_stage + st) * 512;
+                    bulk_load(base + kABytes + a.b_stage_bytes, esrc, kEBytes, &full[s]);
+                    const int y = st * a.rows_stage + static_cast<int>(rank) * rb_rank;
+#pragma unroll
+                    for (int c = 0; c < kChunks; ++c) {
+                        uint8_t* dst = base + kABytes + c * (a.rb * 128) + rank * (rb_rank * 128);
+                        if (CS > 1) tma_load_2d_mc(dst, &tmap_b, n0 + 64 * c, y, &full[s], all);
+                        else tma_load_2d(dst, &tmap_b, n0 + 64 * c, y, &full[s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int q = 0, tl = 0;
+            const uint32_t idesc0 = idesc_bf16(128, kNT, true, 0, true);
+            const uint32_t idesc1 = idesc_bf16(128, kNT, true, 1, true);
+            const uint32_t k_bytes = (a.M == 4 ? 32u : 4u * a.M) * 128u;  // B advance per MMA
+            const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;          // K-group (window) stride
+            for (int w = cid; w < a.work; w += ncl, ++tl) {
+                const int acc = tl & 1;
+                mbar_wait(&tmem_empty[acc], ((tl >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * kNT;
+                for (int st = 0; st < a.n_stage; ++st, ++q) {
+                    const int s = q % S;
+                    mbar_wait(&full[s], (q / S) & 1);
+                    tc_fence_after();
+                    uint8_t* base = smem + s * a.stage_bytes;
+                    tmem_cp_128x128b(tmem + kMetaCol + 4 * s, sdesc(smem_u32(base + kABytes + a.b_stage_bytes), 16, 128, 0));
+                    const uint32_t a0 = smem_u32(base), b0 = smem_u32(base + kABytes);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int mi = st * 4 + k;
+                        if (mi < a.n_mma) {
+                            const uint64_t ad = sdesc(a0 + 32 * k, 16, 1024, kLayoutSW128);
+                            const uint64_t bd = sdesc(b0 + k * k_bytes, a.rb * 128, sbo, kLayoutSW128);
+                            mma_sp_bf16(d, ad, bd, tmem + kMetaCol + 4 * s + (k & ~1), (k & 1) ? idesc1 : idesc0,
+                                        mi > 0 ? 1u : 0u);
+                        }
+                    }
+                    if (CS > 1) mma_commit_mc(&empty[s], all); else mma_commit(&empty[s]);
+                }
+                mma_commit(&tmem_full[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int qd = warp - 4;
+        int tl = 0;
+        for (int w = cid; w < a.work; w += ncl, ++tl) {
+            const int tt = w / a.n_rg, rt = (w % a.n_rg) * CS + static_cast<int>(rank);
+            const int n0 = tt * kNT;
+            const int acc = tl & 1;
+            mbar_wait(&tmem_full[acc], (tl >> 1) & 1);
+            tc_fence_after();
+            const int row = rt * 128 + 32 * qd + lane;
+            const bool row_ok = rt < a.n_rt && row < a.rows;
+#pragma unroll 1
+            for (int c = 0; c < kNT; c += 16) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + acc * kNT + c, v);
+                tmem_wait_ld();
+                const int tcol = n0 + c;
+                if (row_ok && tcol < a.T) {
+                    if (!a.y_bf16) {
+                        float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
+                        if (tcol + 16 <= a.T) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                reinterpret_cast<uint4*>(y)[k] =
+                                    make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+                                if (tcol + k < a.T) y[k] = __uint_as_float(v[k]);
+                        }
+                    } else {
+                        uint16_t* y = reinterpret_cast<uint16_t*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            __nv_bfloat162 h =
+                                __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                            pk[k] = *reinterpret_cast<uint32_t*>(&h);
+                        }
+                        if (tcol + 16 <= a.T) {
+                            reinterpret_cast<uint4*>(y)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                            reinterpret_cast<uint4*>(y)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k)
+                                if (tcol + k < a.T)
+                                    y[k] = static_cast<uint16_t>((pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        }
+    }
+    tc_fence_before();
+    if (CS > 1) cluster_sync_all(); else __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encoder() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+bool encode(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t bi,
+            uint32_t bo) {
+    EncodeTiledFn enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {bi, bo};
+    cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+template <int CS>
+int launch_cs(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
+    const vnm_geom& g = L.P->g;
+    const int rows_stage = g.M == 4 ? 128 : 16 * g.M;
+    const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // rows one stage's windows touch
+    a.rows_stage = rows_stage;
+    a.rb = (need + 8 * CS - 1) / (8 * CS) * (8 * CS);
+    a.b_stage_bytes = static_cast<uint32_t>(kChunks * a.rb * 128);
+    a.stage_bytes = kABytes + a.b_stage_bytes + kEBytes;
+    a.stage_bytes = (a.stage_bytes + 1023) / 1024 * 1024;
+    const uint32_t budget = 224 * 1024;
+    a.stages = static_cast<int>(budget / a.stage_bytes);
+    if (a.stages > 4) a.stages = 4;
+    if (a.stages < 2) return kLaunchUnsupported;
+    a.n_rg = (a.n_rt + CS - 1) / CS;
+    a.work = a.n_rg * a.n_tt;
+    CUtensorMap ta, tb;
+    const int ld_tc = 16 * a.n_mma;
+    const int rows_w = a.n_rt * 128;
+    if (!encode(&ta, L.P->values_tc, static_cast<uint64_t>(ld_tc), static_cast<uint64_t>(rows_w),
+                static_cast<uint64_t>(ld_tc) * 2, 64, 128))
+        return kLaunchCudaError;
+    if (!encode(&tb, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
+                64, static_cast<uint32_t>(a.rb / CS)))
+        return kLaunchCudaError;
+    const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + 1024 + 256;
+    auto k = vnm_spmm_tc_kernel<CS>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return kLaunchCudaError;
+    int clusters = sm_count() / CS;
+    if (clusters > a.work) clusters = a.work;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CS);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k, ta, tb, a) != cudaSuccess) return kLaunchCudaError;
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
+}
+
+}  // namespace
+
+int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream) {
+    const vnm_geom& g = L.P->g;
+    if (g.V != 64 || g.M > 8) return kLaunchUnsupported;
+    TcArgs a;
+    a.meta_tc = L.P->meta_tc;
+    a.YT = L.YT;
+    a.ldy = L.ldy;
+    a.T = L.T;
+    a.y_bf16 = L.y_dtype == VNM_BF16;
+    a.rows = g.rows;
+    a.M = g.M;
+    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+    a.n_stage = (a.n_mma + 3) / 4;
+    a.n_rt = (g.rows_p + 127) / 128;
+    a.n_tt = (L.T + kNT - 1) / kNT;
+    return launch_cs<2>(L, a, stream);
+}
+
+}  // namespace vnm

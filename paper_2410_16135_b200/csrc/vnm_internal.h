@@ -41,6 +41,8 @@ struct SpmmLaunch {
     size_t workspace_bytes;
 };
 int launch_spmm(const SpmmLaunch& L, cudaStream_t stream);
+int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream);  // window form (values_tc / meta_tc)
+int launch_pack_tc(const vnm_packed& P, cudaStream_t stream);
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 
 }  // namespace vnm

@@ -39,14 +39,15 @@ class Geom(ctypes.Structure):
 
 
 class CPacked(ctypes.Structure):
-    _fields_ = [("g", Geom), ("values", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("meta", ctypes.c_void_p)]
+    _fields_ = [("g", Geom), ("values", ctypes.c_void_p), ("col_idx", ctypes.c_void_p), ("meta", ctypes.c_void_p),
+                ("values_tc", ctypes.c_void_p), ("meta_tc", ctypes.c_void_p)]
 
 
 _lock = threading.Lock()
 _lib = None
 
-EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress", "vnm_spmm",
-           "vnm_spmm_workspace_bytes", "vnm_status_string", "vnm_launch_count"]
+EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress", "vnm_pack_tc",
+           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_status_string", "vnm_launch_count"]
 
 
 def lib():
@@ -70,6 +71,8 @@ def lib():
             L.vnm_compress.restype = ctypes.c_int
             L.vnm_prune_compress.argtypes = [P, i64, P, i64, GP, PP, P, P]
             L.vnm_prune_compress.restype = ctypes.c_int
+            L.vnm_pack_tc.argtypes = [PP, P]
+            L.vnm_pack_tc.restype = ctypes.c_int
             L.vnm_spmm.argtypes = [P, i64, i32, PP, P, i64, ctypes.c_int, P, sz, P]
             L.vnm_spmm.restype = ctypes.c_int
             L.vnm_spmm_workspace_bytes.argtypes = [GP, i32]
@@ -129,14 +132,19 @@ def _ld(t: torch.Tensor) -> int:
 
 @dataclass
 class Packed:
-    """The compressed V:N:M weight (App. A): A_n = values, A_i1 = col_idx, A_i2 = meta."""
+    """The compressed V:N:M weight (App. A): A_n = values, A_i1 = col_idx, A_i2 = meta, plus the optional
+    tensor-core window form (values_tc / meta_tc, include/vnm.h) used by vnm_spmm for large T."""
     g: Geom
     values: torch.Tensor   # bf16 [rows_p][ld_val]
     col_idx: torch.Tensor  # uint8 [rows_p/V][nb_pad][4]
     meta: torch.Tensor     # int32 (u32 bits) [rows_p][ld_meta]
+    values_tc: torch.Tensor | None = None  # bf16 [rows_w * ld_tc]
+    meta_tc: torch.Tensor | None = None    # int32 (u32 bits)
 
     def c(self) -> CPacked:
-        return CPacked(self.g, self.values.data_ptr(), self.col_idx.data_ptr(), self.meta.data_ptr())
+        return CPacked(self.g, self.values.data_ptr(), self.col_idx.data_ptr(), self.meta.data_ptr(),
+                       self.values_tc.data_ptr() if self.values_tc is not None else None,
+                       self.meta_tc.data_ptr() if self.meta_tc is not None else None)
 
     @staticmethod
     def empty(g: Geom, device) -> "Packed":
@@ -144,6 +152,26 @@ class Packed:
                       torch.empty((g.rows_p, g.ld_val), dtype=torch.bfloat16, device=device),
                       torch.empty((g.rows_p // g.V, g.nb_pad, 4), dtype=torch.uint8, device=device),
                       torch.empty((g.rows_p, g.ld_meta), dtype=torch.int32, device=device))
+
+
+def tc_bytes(g: Geom) -> tuple[int, int]:
+    L = lib()
+    return int(L.vnm_bytes(ctypes.byref(g), 4)), int(L.vnm_bytes(ctypes.byref(g), 5))
+
+
+def pack_tc(P: Packed) -> Packed:
+    """Fill the tensor-core window form of P (allocating it on P's device); V = 64, 4 <= M <= 8 only."""
+    _require_cuda(P.values)
+    nv, nm = tc_bytes(P.g)
+    if nv == 0:
+        raise VnmError(VNM_ERR_UNSUPPORTED, "vnm_pack_tc")
+    if P.values_tc is None or P.values_tc.numel() * 2 < nv:
+        P.values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=P.values.device)
+    if P.meta_tc is None or P.meta_tc.numel() * 4 < nm:
+        P.meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=P.values.device)
+    cp = P.c()
+    _check(lib().vnm_pack_tc(ctypes.byref(cp), _stream(P.values.device)), "vnm_pack_tc")
+    return P
 
 
 def prune(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None) -> torch.Tensor:
@@ -170,8 +198,10 @@ def compress(W: torch.Tensor, mask: torch.Tensor, V: int, M: int, status: torch.
     return P
 
 
-def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None, want_mask: bool = False):
-    """Fused S_{V:N:M} + compression in one pass over W.  Returns Packed (and the mask if asked)."""
+def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None, want_mask: bool = False,
+                   tc: bool = False):
+    """Fused S_{V:N:M} + compression in one pass over W.  Returns Packed (and the mask if asked); with tc=True
+    the tensor-core window form is also filled (vnm_pack_tc) when it applies (V = 64, M <= 8)."""
     W = _as_bits16(W)
     _require_cuda(W, score)
     g = geometry(W.shape[0], W.shape[1], V, M)
@@ -181,6 +211,8 @@ def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None =
     _check(lib().vnm_prune_compress(_ptr(W), _ld(W), _ptr(score), _ld(score) if score is not None else 0,
                                     ctypes.byref(g), ctypes.byref(cp), _ptr(mask), _stream(W.device)),
            "vnm_prune_compress")
+    if tc and V == 64 and M <= 8:
+        pack_tc(P)
     return (P, mask) if want_mask else P
 
 

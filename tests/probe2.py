@@ -154,5 +154,48 @@ def main():
     json.dump(r, open(os.path.join(ROOT, "gpurun_out", f"probe2_{tag}.json"), "w"), indent=1)
 
 
+
+def window(L):
+    """Overlapping K-group windows: K-group i of the MMA reads dense rows [i*w, i*w + 8)."""
+    P, u32 = ctypes.c_void_p, ctypes.c_uint32
+    L.vnm_probe_window.argtypes = [P, P, P, P, u32, u32, u32, u32, u32, u32, u32]
+    krows = 40
+    A = bf16(np.tile(2.0 ** np.arange(16, dtype=np.float32)[None, :], (128, 1)))
+    Bn = np.zeros((krows, 64), np.float32)
+    for k in range(krows):
+        Bn[k, k] = 1.0
+    B = bf16(Bn)
+    E = torch.full((128, 4), 0x44444444, dtype=torch.int64).to(torch.int32).cuda()
+    res = []
+    cfgs = [  # (m, layout, lbo, sbo, base_off, window_rows, start_row)
+        (128, 2, 16384, 1024, 0, 8, 0), (128, 2, 16384, 640, 0, 5, 0), (128, 0, 128, krows * 16, 0, 8, 0),
+        (128, 0, 80, krows * 16, 0, 5, 0), (64, 2, 16384, 640, 0, 5, 0), (64, 0, 80, krows * 16, 0, 5, 0),
+        (128, 0, 96, krows * 16, 0, 6, 0), (128, 0, 112, krows * 16, 0, 7, 0), (128, 2, 16384, 768, 0, 6, 0),
+        (128, 2, 16384, 640, 0, 5, 5), (128, 2, 16384, 640, 5, 5, 5), (128, 2, 16384, 640, 0, 5, 10),
+        (128, 2, 16384, 640, 2, 5, 10), (128, 2, 16384, 896, 0, 7, 7), (64, 2, 16384, 640, 0, 5, 5)]
+    if len(sys.argv) > 2:
+        cfgs = [cfgs[int(sys.argv[2])]]
+    for (m, layout, lbo, sbo, boff, w, r0) in cfgs:
+        D = torch.zeros(128, 64, dtype=torch.float32, device="cuda")
+        st = L.vnm_probe_window(A.data_ptr(), B.data_ptr(), E.data_ptr(), D.data_ptr(), m, krows, layout, lbo, sbo,
+                                boff, r0)
+        torch.cuda.synchronize()
+        Dn = D.cpu().numpy()
+        exp = np.zeros(64)
+        for i in range(4):
+            for p, j in ((0, 4 * i), (1, 4 * i + 1), (4, 4 * i + 2), (5, 4 * i + 3)):
+                exp[r0 + i * w + p] += 2.0 ** j
+        lane0 = Dn[0]
+        r = {"m": m, "layout": layout, "lbo": lbo, "sbo": sbo, "window_rows": w, "start_row": r0, "base_off": boff,
+             "status": st,
+             "match_lane0": bool(np.array_equal(lane0, exp)),
+             "rows_equal": bool(all(np.array_equal(Dn[l], lane0) for l in (range(128) if m == 128 else [0, 5, 32, 37]))),
+             "lane0_nonzero": {int(k): float(v) for k, v in enumerate(lane0) if v != 0},
+             "expected_nonzero": {int(k): float(v) for k, v in enumerate(exp) if v != 0}}
+        print(json.dumps(r), flush=True)
+        res.append(r)
+    return res
+
+
 if __name__ == "__main__":
     main()

@@ -21,8 +21,8 @@ def make(rows, cols, V, M, T, seed, wkind="normal", xkind="normal"):
     return W, XT, Wm
 
 
-def gpu_y(W, XT, V, M, T, out_dtype=torch.float32):
-    P = vnm.prune_compress(to_dev_bf16(W), V, M)
+def gpu_y(W, XT, V, M, T, out_dtype=torch.float32, tc=False):
+    P = vnm.prune_compress(to_dev_bf16(W), V, M, tc=tc)
     Y = vnm.spmm(to_dev_bf16(XT), P, T=T, out_dtype=out_dtype)
     torch.cuda.synchronize()
     return Y.float().cpu().numpy().astype(np.float64)
@@ -102,11 +102,11 @@ def test_m4_matches_dense_24():
     assert_within(gpu_y(W, XT, 64, 4, 128), Yref, Aref)
 
 
-def sampled_check(rows, cols, M, T, seed, n=3000, out_dtype=torch.float32):
+def sampled_check(rows, cols, M, T, seed, n=3000, out_dtype=torch.float32, tc=False):
     W = synth.weights(rows, cols, seed=seed, kind="outlier")
     XT = synth.activations_t(cols, T, seed=seed + 1)
     Wd, Xd = to_dev_bf16(W), to_dev_bf16(XT)
-    P, mask_d = vnm.prune_compress(Wd, 64, M, want_mask=True)
+    P, mask_d = vnm.prune_compress(Wd, 64, M, want_mask=True, tc=tc)
     Y = vnm.spmm(Xd, P, T=T, out_dtype=out_dtype)
     torch.cuda.synchronize()
     mask = mask_d.cpu().numpy().view(np.uint32)
@@ -125,10 +125,11 @@ def sampled_check(rows, cols, M, T, seed, n=3000, out_dtype=torch.float32):
     assert torch.isfinite(Y).all()
 
 
+@pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("rows,cols", [(4096, 4096), (11008, 4096), (4096, 11008)])
-def test_llama_prefill_sampled(rows, cols):
-    """BJ config 4a at full size (T = 2048, 64:2:5), in the launch configuration bench.py times."""
-    sampled_check(rows, cols, 5, 2048, seed=rows + cols, out_dtype=torch.bfloat16)
+def test_llama_prefill_sampled(rows, cols, tc):
+    """BJ config 4a at full size (T = 2048, 64:2:5), both plans (bench.py times the window plan, tc=True)."""
+    sampled_check(rows, cols, 5, 2048, seed=rows + cols, out_dtype=torch.bfloat16, tc=tc)
 
 
 @pytest.mark.parametrize("T", [1, 2, 4, 8, 16])
@@ -142,10 +143,40 @@ def test_llama_decode_full(T):
     assert_within(gpu_y(W, XT, 64, 5, T), Yref, Aref)
 
 
+@pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("rows,cols,M", [(1152, 384, 5), (384, 1536, 5), (3072, 768, 8), (768, 3072, 8)])
-def test_deit_sampled(rows, cols, M):
-    """BJ configs 2/3: DeiT-S @64:2:5 and DeiT-B @64:2:8 with T = 197 * 256 tokens."""
-    sampled_check(rows, cols, M, 197 * 256, seed=rows * 3 + cols, out_dtype=torch.bfloat16)
+def test_deit_sampled(rows, cols, M, tc):
+    """BJ configs 2/3: DeiT-S @64:2:5 and DeiT-B @64:2:8 with T = 197 * 256 tokens (both plans)."""
+    sampled_check(rows, cols, M, 197 * 256, seed=rows * 3 + cols, out_dtype=torch.bfloat16, tc=tc)
+
+
+@pytest.mark.parametrize("M", [4, 5, 6, 7, 8])
+@pytest.mark.parametrize("rows,cols,T", [(128, 512, 192), (70, 23, 65), (200, 333, 193), (384, 1000, 500),
+                                         (64, 40, 100), (1000, 257, 384)])
+def test_window_plan(rows, cols, T, M):
+    """The tensor-core window form (values_tc / meta_tc, T > 64): ragged rows / cols / tokens, every M <= 8."""
+    W, XT, Wm = make(rows, cols, 64, M, T, seed=rows + 7 * cols + M)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, M, T, tc=True), Yref, Aref)
+
+
+def test_window_plan_exact_integers():
+    """Integer W and X: the window plan (extra zero-valued positions included) is exact."""
+    W, XT, Wm = make(256, 640, 64, 5, 256, seed=9, wkind="int", xkind="int")
+    Yref, _ = oracle.gemm_ref(XT, Wm)
+    assert np.array_equal(gpu_y(W, XT, 64, 5, 256, tc=True), Yref)
+
+
+def test_window_plan_bf16_out_and_identity():
+    rows, cols, M = 192, 200, 6
+    W = synth.weights(rows, cols, seed=13)
+    XT = synth.f32_to_bf16_bits(np.eye(cols, dtype=np.float32))
+    mask = oracle.prune(W, 64, M)
+    Wm = synth.bf16_bits_to_f32(oracle.apply_mask(W, mask, 64, M)).astype(np.float64)
+    assert np.array_equal(gpu_y(W, XT, 64, M, cols, tc=True), Wm)
+    W2, X2, Wm2 = make(300, 700, 64, 7, 333, seed=14)
+    Yref, Aref = oracle.gemm_ref(X2, Wm2)
+    assert_within(gpu_y(W2, X2, 64, 7, 333, out_dtype=torch.bfloat16, tc=True), Yref, Aref, bf16=True)
 
 
 def test_determinism():
