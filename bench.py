@@ -165,24 +165,29 @@ def run_gpu(args):
     import ctypes
 
     use_tc = T > 64 and M <= 8 and V == 64
-    if use_tc:
+    if use_tc:  # window-form buffers, written by vnm_prune_compress in the same pass (include/vnm.h)
         for l in layers:
-            vnm.pack_tc(l["P"])  # allocates the window-form buffers once; refilled inside every step
+            nv, nm = vnm.tc_bytes(l["P"].g)
+            l["P"].values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=dev)
+            l["P"].meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=dev)
 
     def prune_compress(l):
         cp = l["P"].c()
         st = L.vnm_prune_compress(ctypes.c_void_p(l["W"].data_ptr()), l["W"].stride(0), None, 0,
                                   ctypes.byref(l["P"].g), ctypes.byref(cp), None, ctypes.c_void_p(stream.cuda_stream))
         assert st == 0, vnm.status_string(st)
-        if use_tc:
-            st = L.vnm_pack_tc(ctypes.byref(cp), ctypes.c_void_p(stream.cuda_stream))
-            assert st == 0, vnm.status_string(st)
+
+    for l in layers:  # split-K scratch (small T), allocated once outside the timed region
+        nws = vnm.spmm_workspace_bytes(l["P"].g, T)
+        l["ws"] = torch.empty(max(nws, 16) // 4, dtype=torch.float32, device=dev) if nws else None
 
     def spmm(l):
         cp = l["P"].c()
+        ws = l["ws"]
         st = L.vnm_spmm(ctypes.c_void_p(l["X"].data_ptr()), l["X"].stride(0), T, ctypes.byref(cp),
-                        ctypes.c_void_p(l["Y"].data_ptr()), l["Y"].stride(0), vnm.VNM_BF16, None, 0,
-                        ctypes.c_void_p(stream.cuda_stream))
+                        ctypes.c_void_p(l["Y"].data_ptr()), l["Y"].stride(0), vnm.VNM_BF16,
+                        ctypes.c_void_p(ws.data_ptr()) if ws is not None else None,
+                        ws.numel() * 4 if ws is not None else 0, ctypes.c_void_p(stream.cuda_stream))
         assert st == 0, vnm.status_string(st)
 
     def step(ev=None):

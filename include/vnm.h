@@ -109,7 +109,9 @@ vnm_status vnm_prune(const uint16_t* W, int64_t ldw, const float* score, int64_t
 vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, const vnm_geom* g,
                         vnm_packed* out, int32_t* d_status, vnm_stream_t stream);
 
-/* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.      */
+/* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.
+ * If out->values_tc / out->meta_tc are set (V = 64, M <= 8) the window form is written in the same pass
+ * (identical to vnm_pack_tc of the result).                                                             */
 vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
                               const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
 

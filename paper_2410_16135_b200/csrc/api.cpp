@@ -154,6 +154,13 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
     if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
     if (!W) return VNM_ERR_ARG;
     vnm::PruneLaunch L{g, W, ldw, score, lds, nullptr, mask, out->values, out->col_idx, out->meta, nullptr};
+    if (out->values_tc || out->meta_tc) {  // fused window form (include/vnm.h), V = 64 and M <= 8 only
+        if (g->V != 64 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+        if (!out->values_tc || !out->meta_tc) return VNM_ERR_ARG;
+        if (!aligned16(out->values_tc) || !aligned16(out->meta_tc)) return VNM_ERR_ALIGN;
+        L.values_tc = out->values_tc;
+        L.meta_tc = out->meta_tc;
+    }
     return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "tc_form.cuh"
 #include "vnm_internal.h"
 
 namespace vnm {
@@ -23,30 +24,6 @@ struct PackTcArgs {
     int32_t M, rows_p, rows_w, nb_pad, ld_val, ld_meta, n_mma, n_stage, ld_tc;
 };
 
-// one 2:4 group: positions (pa < pb) and the stored-value slot of each of the row's two nonzeros
-struct Group {
-    uint32_t nib;
-    int slot0, slot1;  // slot (0/1) taken by nonzero 0 / 1, or -1 if not in this group
-};
-
-__device__ __forceinline__ Group encode_group(int c0, int c1, int base) {
-    const bool in0 = c0 >= base && c0 < base + 4, in1 = c1 >= base && c1 < base + 4;
-    Group g{0x4u, -1, -1};
-    if (in0 && in1) {
-        g.nib = static_cast<uint32_t>(c0 - base) | (static_cast<uint32_t>(c1 - base) << 2);
-        g.slot0 = 0;
-        g.slot1 = 1;
-    } else if (in0 || in1) {
-        const int p = (in0 ? c0 : c1) - base;
-        const int f = p == 0 ? 1 : 0;  // lowest free position
-        const int lo = p < f ? p : f, hi = p < f ? f : p;
-        g.nib = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 2);
-        const int slot = p < f ? 0 : 1;
-        if (in0) g.slot0 = slot; else g.slot1 = slot;
-    }
-    return g;
-}
-
 // the 8-nibble metadata word of MMA `mi` for row r (rows >= rows_p: zero weights, nibble 0x4)
 __device__ uint32_t mma_word(const PackTcArgs& a, int r, int mi) {
     if (r >= a.rows_p || mi >= a.n_mma) return 0x44444444u;
@@ -59,8 +36,7 @@ __device__ uint32_t mma_word(const PackTcArgs& a, int r, int mi) {
         const uint32_t nib = (a.meta[static_cast<int64_t>(r) * a.ld_meta + b / 8] >> (4 * (b % 8))) & 0xFu;
         const uint8_t* ci = ci_row + b * 4;
         const int c0 = ci[nib & 3u], c1 = ci[nib >> 2];
-        w |= encode_group(c0, c1, 0).nib << (8 * i);
-        w |= encode_group(c0, c1, 4).nib << (8 * i + 4);
+        w |= tc_encode_block(c0, c1, 0, 0).nibs << (8 * i);
     }
     return w;
 }
@@ -84,12 +60,9 @@ __global__ void pack_tc_values_kernel(const PackTcArgs a) {
         const int c0 = ci[nib & 3u], c1 = ci[nib >> 2];
         const uint16_t v0 = a.values[static_cast<int64_t>(r) * a.ld_val + 2 * b];
         const uint16_t v1 = a.values[static_cast<int64_t>(r) * a.ld_val + 2 * b + 1];
+        const TcBlock t = tc_encode_block(c0, c1, v0, v1);
 #pragma unroll
-        for (int gi = 0; gi < 2; ++gi) {
-            const Group g = encode_group(c0, c1, 4 * gi);
-            if (g.slot0 >= 0) out[2 * gi + g.slot0] = v0;
-            if (g.slot1 >= 0) out[2 * gi + g.slot1] = v1;
-        }
+        for (int q = 0; q < 4; ++q) out[q] = t.val[q];
     }
     uint2 pk;
     pk.x = static_cast<uint32_t>(out[0]) | (static_cast<uint32_t>(out[1]) << 16);

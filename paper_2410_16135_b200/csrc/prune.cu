@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
+#include "tc_form.cuh"
 #include "vnm_internal.h"
 
 namespace vnm {
@@ -40,6 +41,9 @@ struct PruneArgs {
     uint8_t* col_idx;
     uint32_t* meta;
     int32_t* status;  // FROM_MASK, may be null
+    uint16_t* values_tc;  // optional window form (V = 64, M <= 8, CB = 32), see tc_form.cuh
+    uint32_t* meta_tc;
+    int32_t ld_tc, n_stage_tc;
     int32_t rows, cols, M, rows_p, cols_p, nb, nb_pad, ld_val, ld_meta, ld_mask;
     int32_t CB;  // column blocks per CTA (32, 16 or 8)
 };
@@ -69,12 +73,14 @@ __device__ __forceinline__ uint32_t butterfly_or(uint32_t v) {
     return v;
 }
 
-template <int V, bool FROM_MASK, bool HAS_SCORE>
+// MT: compile-time M (0 = runtime a.M).  With M known the tile pitch and every block offset fold into
+// immediate shared-memory offsets (address arithmetic was a third of the instructions with runtime M).
+template <int V, int MT, bool FROM_MASK, bool HAS_SCORE>
 __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a) {
     using S = Shape<V>;
     constexpr int RT = S::RT, Lb = S::Lb, RPL = S::RPL, IPW = S::IPW;
     extern __shared__ __align__(16) uint8_t smem[];
-    const int CB = a.CB, M = a.M;
+    const int CB = MT ? 32 : a.CB, M = MT ? MT : a.M;
     const int tile_cols = CB * M;
     const int pitch_w = tile_cols + 8;  // bf16 elements; +16 B breaks row-to-row bank aliasing
     const int pitch_s = tile_cols + 4;  // fp32
@@ -98,6 +104,12 @@ __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a)
     uint32_t* sCi = reinterpret_cast<uint32_t*>(p);
     p += static_cast<size_t>(RT / V) * CB * 4;
     uint8_t* sNib = p;
+    p += static_cast<size_t>(RT) * CB;
+    // window form staging (only when a.values_tc): 4 values and a nibble pair per row-block
+    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    uint16_t* sTcv = reinterpret_cast<uint16_t*>(p);
+    p += static_cast<size_t>(RT) * 4 * CB * 2;
+    uint8_t* sTcn = p;
 
     // ---- load the tile (zero-filled outside rows x cols)
     {
@@ -274,6 +286,20 @@ __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a)
                 sVal[r * 2 * CB + 2 * bl + 0] = v0;
                 sVal[r * 2 * CB + 2 * bl + 1] = v1;
                 sNib[r * CB + bl] = static_cast<uint8_t>(nib);
+                if (a.values_tc) {
+                    const int cl = rb ? __ffs(rb) - 1 : 0, ch = rb ? 31 - __clz(rb) : 1;
+                    const TcBlock t = tc_encode_block(cl, ch, v0, v1);
+                    if (M == 4) {
+                        sTcv[r * 4 * CB + 2 * bl] = v0;
+                        sTcv[r * 4 * CB + 2 * bl + 1] = v1;
+                    } else {
+                        uint2 pk;
+                        pk.x = static_cast<uint32_t>(t.val[0]) | (static_cast<uint32_t>(t.val[1]) << 16);
+                        pk.y = static_cast<uint32_t>(t.val[2]) | (static_cast<uint32_t>(t.val[3]) << 16);
+                        *reinterpret_cast<uint2*>(sTcv + r * 4 * CB + 4 * bl) = pk;
+                    }
+                    sTcn[r * CB + bl] = static_cast<uint8_t>(t.nibs);
+                }
                 sBits[r * CB + bl] = rb;
             }
         }
@@ -314,6 +340,47 @@ __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a)
             reinterpret_cast<uint32_t*>(a.col_idx)[static_cast<int64_t>(vbg) * a.nb_pad + b0 + bl] = sCi[v * CB + bl];
         }
     }
+    if (a.values_tc && cbv > 0) {
+        // window form (include/vnm.h values_tc / meta_tc): this CTA = one V-block (64 rows) x 32 blocks
+        const int bpm = M == 4 ? 8 : 4;
+        const int vpb = M == 4 ? 2 : 4;  // window-form values per block
+        const int tch = cbv * vpb / 8;   // 16-byte chunks per row
+        for (int i = threadIdx.x; i < rows_here * tch; i += kThreads) {
+            const int r = i / tch, c = i % tch;
+            const uint4 v = *reinterpret_cast<const uint4*>(sTcv + r * 4 * CB + 8 * c);
+            *reinterpret_cast<uint4*>(a.values_tc + static_cast<int64_t>(r0 + r) * a.ld_tc + vpb * b0 + 8 * c) = v;
+        }
+        // meta_tc words of this V-block's 64 lanes (lanes 64h..64h+63 of the 128-row tile)
+        const int tile = r0 / 128, half = (r0 / 64) & 1;
+        const int mi0 = b0 / bpm, n_mi = cbv / bpm;
+        for (int i = threadIdx.x; i < n_mi * 64; i += kThreads) {
+            const int L = 64 * half + (i % 64), mi = mi0 + i / 64;
+            const int h = (L / 8) & 1;
+            const int ra = (L % 8) + 16 * (L / 16) - 64 * half, rb_ = ra + 8;
+            uint32_t wa = 0, wb = 0;
+            if (M == 4) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int bl = 8 * (mi - mi0) + 4 * h + q;
+                    wa |= static_cast<uint32_t>(sNib[ra * CB + bl]) << (4 * q);
+                    wb |= static_cast<uint32_t>(sNib[rb_ * CB + bl]) << (4 * q);
+                }
+            } else {
+                const int bl = 4 * (mi - mi0) + 2 * h;
+                wa = static_cast<uint32_t>(sTcn[ra * CB + bl]) | (static_cast<uint32_t>(sTcn[ra * CB + bl + 1]) << 8);
+                wb = static_cast<uint32_t>(sTcn[rb_ * CB + bl]) | (static_cast<uint32_t>(sTcn[rb_ * CB + bl + 1]) << 8);
+            }
+            a.meta_tc[((static_cast<int64_t>(tile) * a.n_stage_tc + mi / 4) * 128 + L) * 4 + (mi % 4)] = wa | (wb << 16);
+        }
+        // MMA slots past the last real MMA of the last stage: filler metadata (as vnm_pack_tc writes)
+        const int n_mma = a.ld_tc / 16;
+        if (b0 + CB >= a.nb_pad) {
+            for (int i = threadIdx.x; i < (4 * a.n_stage_tc - n_mma) * 64; i += kThreads) {
+                const int L = 64 * half + (i % 64), mi = n_mma + i / 64;
+                a.meta_tc[((static_cast<int64_t>(tile) * a.n_stage_tc + mi / 4) * 128 + L) * 4 + (mi % 4)] = 0x44444444u;
+            }
+        }
+    }
     if (a.mask_out) {
         const int w0 = c0 / 32;
         const int nw = min(mwords, a.ld_mask - w0);
@@ -336,7 +403,7 @@ __global__ void status_fini_kernel(int32_t* s) {
     if (*s == 0x7fffffff) *s = 0;
 }
 
-size_t smem_bytes(int V, int M, int CB, bool from_mask, bool has_score) {
+size_t smem_bytes(int V, int M, int CB, bool from_mask, bool has_score, bool tc) {
     const int RT = V < 32 ? 32 : V;
     const int tile_cols = CB * M;
     size_t b = static_cast<size_t>(RT) * (tile_cols + 8) * 2;
@@ -344,12 +411,13 @@ size_t smem_bytes(int V, int M, int CB, bool from_mask, bool has_score) {
     if (from_mask) b += static_cast<size_t>(RT) * (tile_cols / 32) * 4;
     b += static_cast<size_t>(RT) * 2 * CB * 2 + static_cast<size_t>(RT) * CB * 4 +
          static_cast<size_t>(RT / V) * CB * 4 + static_cast<size_t>(RT) * CB;
+    if (tc) b += 16 + static_cast<size_t>(RT) * 4 * CB * 2 + static_cast<size_t>(RT) * CB;
     return b;
 }
 
-template <int V, bool FROM_MASK, bool HAS_SCORE>
+template <int V, int MT, bool FROM_MASK, bool HAS_SCORE>
 cudaError_t launch_t(const PruneArgs& a, size_t smem, cudaStream_t st) {
-    auto k = prune_pack_kernel<V, FROM_MASK, HAS_SCORE>;
+    auto k = prune_pack_kernel<V, MT, FROM_MASK, HAS_SCORE>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     constexpr int RT = Shape<V>::RT;
@@ -359,18 +427,34 @@ cudaError_t launch_t(const PruneArgs& a, size_t smem, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// V = 64 with M in 4..8 and CB = 32 (the paper's configurations) get compile-time M
+template <bool FROM_MASK, bool HAS_SCORE>
+cudaError_t launch_m64(const PruneArgs& a, size_t smem, cudaStream_t st) {
+    if (a.CB == 32) {
+        switch (a.M) {
+            case 4: return launch_t<64, 4, FROM_MASK, HAS_SCORE>(a, smem, st);
+            case 5: return launch_t<64, 5, FROM_MASK, HAS_SCORE>(a, smem, st);
+            case 6: return launch_t<64, 6, FROM_MASK, HAS_SCORE>(a, smem, st);
+            case 7: return launch_t<64, 7, FROM_MASK, HAS_SCORE>(a, smem, st);
+            case 8: return launch_t<64, 8, FROM_MASK, HAS_SCORE>(a, smem, st);
+            default: break;
+        }
+    }
+    return launch_t<64, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+}
+
 template <bool FROM_MASK, bool HAS_SCORE>
 cudaError_t launch_v(int V, const PruneArgs& a, size_t smem, cudaStream_t st) {
     switch (V) {
-        case 1: return launch_t<1, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 2: return launch_t<2, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 4: return launch_t<4, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 8: return launch_t<8, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 16: return launch_t<16, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 32: return launch_t<32, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 64: return launch_t<64, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 128: return launch_t<128, FROM_MASK, HAS_SCORE>(a, smem, st);
-        case 256: return launch_t<256, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 1: return launch_t<1, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 2: return launch_t<2, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 4: return launch_t<4, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 8: return launch_t<8, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 16: return launch_t<16, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 32: return launch_t<32, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 64: return launch_m64<FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 128: return launch_t<128, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
+        case 256: return launch_t<256, 0, FROM_MASK, HAS_SCORE>(a, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -385,7 +469,7 @@ int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
     int CB = 0;
     for (int cb : {32, 16, 8}) {
         if ((cb * g.M) % 32 != 0) continue;  // whole mask words per tile
-        if (smem_bytes(g.V, g.M, cb, from_mask, has_score) > kMaxSmem) continue;
+        if (smem_bytes(g.V, g.M, cb, from_mask, has_score, L.values_tc != nullptr) > kMaxSmem) continue;
         CB = cb;
         break;
     }
@@ -397,7 +481,25 @@ int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
     a.rows = g.rows; a.cols = g.cols; a.M = g.M; a.rows_p = g.rows_p; a.cols_p = g.cols_p;
     a.nb = g.nb; a.nb_pad = g.nb_pad; a.ld_val = g.ld_val; a.ld_meta = g.ld_meta; a.ld_mask = g.ld_mask;
     a.CB = CB;
-    const size_t smem = smem_bytes(g.V, g.M, CB, from_mask, has_score);
+    a.values_tc = L.values_tc;
+    a.meta_tc = L.meta_tc;
+    a.ld_tc = 0;
+    a.n_stage_tc = 0;
+    if (a.values_tc) {
+        if (g.V != 64 || g.M > 8 || CB != 32 || !a.meta_tc) return kLaunchUnsupported;
+        const int n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+        a.ld_tc = 16 * n_mma;
+        a.n_stage_tc = (n_mma + 3) / 4;
+        // rows of the last 128-row tile beyond rows_p: zero values, nibble 0x4 metadata
+        const int rows_w = (g.rows_p + 127) / 128 * 128;
+        if (rows_w > g.rows_p) {
+            cudaMemsetAsync(a.values_tc + static_cast<int64_t>(g.rows_p) * a.ld_tc, 0,
+                            static_cast<size_t>(rows_w - g.rows_p) * a.ld_tc * 2, stream);
+            cudaMemset2DAsync(a.meta_tc + (static_cast<int64_t>(rows_w / 128 - 1) * a.n_stage_tc * 128 + 64) * 4, 2048,
+                              0x44, 1024, a.n_stage_tc, stream);
+        }
+    }
+    const size_t smem = smem_bytes(g.V, g.M, CB, from_mask, has_score, a.values_tc != nullptr);
     cudaError_t e;
     if (from_mask && a.status) {
         status_init_kernel<<<1, 1, 0, stream>>>(a.status);

@@ -55,6 +55,10 @@ struct SpmmArgs {
     int32_t T;
     int32_t y_bf16;
     int32_t rows, M, nb_pad, ld_meta, nvb, ntt, ntiles;
+    // split-K (small T): unit u = (tile u / ks_n, K-slice u % ks_n of sps stages); partial sums go to
+    // ws[k][row][t] (fp32) and a second kernel adds the ks_n slices in order (deterministic)
+    int32_t ks_n, sps, nunits;
+    float* ws;
 };
 
 template <int NT>
@@ -119,17 +123,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sub = lane / CPR, ch = lane % CPR;
         const uint32_t dst_chunk = (ch / 8) * (kKRowsPerStage * 128);
         int q = 0;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        for (int u = blockIdx.x; u < a.nunits; u += gridDim.x) {
+            const int tile = u / a.ks_n, k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
             const int vb = tile % a.nvb, n0 = (tile / a.nvb) * NT;
             const uint32_t* ci_vb = reinterpret_cast<const uint32_t*>(a.col_idx) + static_cast<int64_t>(vb) * a.nb_pad;
             int tok_bytes = (a.T - (n0 + 8 * ch)) * 2;
             tok_bytes = tok_bytes < 0 ? 0 : (tok_bytes > 16 ? 16 : tok_bytes);
             const uint16_t* xt_tok = a.XT + n0 + 8 * ch;
-            for (int ks = 0; ks < n_stage; ++ks, ++q) {
+            // A_i1 words of this warp's 4 blocks, loaded two stages ahead (the load latency is not exposed)
+            auto load_ci = [&](int ks) -> uint32_t {
+                const int blk_l = ks * kBlocksPerStage + 4 * pw + (lane & 3);
+                return (ks < k1 && blk_l < a.nb_pad) ? __ldg(ci_vb + blk_l) : 0xFFFFFFFFu;
+            };
+            uint32_t ci_n1 = load_ci(k0), ci_n2 = load_ci(k0 + 1);
+            for (int ks = k0; ks < k1; ++ks, ++q) {
                 const int s = q % S;
                 const uint32_t ph = (q / S) & 1;
-                const int blk_l = ks * kBlocksPerStage + 4 * pw + (lane & 3);
-                const uint32_t ci = (blk_l < a.nb_pad) ? __ldg(ci_vb + blk_l) : 0xFFFFFFFFu;
+                const uint32_t ci = ci_n1;
+                ci_n1 = ci_n2;
+                ci_n2 = load_ci(ks + 2);
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* bst = sB + s * C::kBBytes + dst_chunk;
 #pragma unroll
@@ -152,9 +164,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ TMA producer (A_n)
         if (lane == 0) {
             int q = 0;
-            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+            for (int u = blockIdx.x; u < a.nunits; u += gridDim.x) {
+                const int tile = u / a.ks_n, k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
                 const int vb = tile % a.nvb;
-                for (int ks = 0; ks < n_stage; ++ks, ++q) {
+                for (int ks = k0; ks < k1; ++ks, ++q) {
                     const int s = q % S;
                     const uint32_t ph = (q / S) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
@@ -169,13 +182,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int q = 0, tl = 0;
             const uint32_t idesc0 = idesc_bf16(64, NT, true, 0, true);
             const uint32_t idesc1 = idesc_bf16(64, NT, true, 1, true);
-            for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tl) {
+            for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++tl) {
+                const int k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
                 const int acc = tl & 1;
                 const uint32_t aph = (tl >> 1) & 1;
                 mbar_wait(&tmem_empty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + ((16u * acc) << 16);
-                for (int ks = 0; ks < n_stage; ++ks, ++q) {
+                for (int ks = k0; ks < k1; ++ks, ++q) {
                     const int s = q % S;
                     const uint32_t ph = (q / S) & 1;
                     mbar_wait(&full[s], ph);
@@ -190,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint64_t ad = sdesc(a_base + 32 * k, 16, 1024, kLayoutSW128);
                             const uint64_t bd = sdesc(b_base + 4096 * k, kKRowsPerStage * 128, 1024, kLayoutSW128);
                             const uint32_t e = d_tmem + kMetaCol + 4 * s + (k & ~1);
-                            mma_sp_bf16(d_tmem, ad, bd, e, (k & 1) ? idesc1 : idesc0, mi > 0 ? 1u : 0u);
+                            mma_sp_bf16(d_tmem, ad, bd, e, (k & 1) ? idesc1 : idesc0, mi > k0 * kMmaPerStage ? 1u : 0u);
                         }
                     }
                     mma_commit(&empty[s]);
@@ -205,27 +219,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qd = warp - kMetaWarp0;  // TMEM sub-partition (== warp % 4)
         const int ml = lane % 16, mh = ml / 8;
         int q = 0, tl = 0;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tl) {
+        for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++tl) {
+            const int tile = u / a.ks_n, k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
             const int vb = tile % a.nvb;
             const int acc = tl & 1;
             const int row_a = vb * kV + 16 * qd + (ml % 8);
             const uint32_t* ma = a.meta + static_cast<int64_t>(row_a) * a.ld_meta;
             const uint32_t* mb = ma + 8 * static_cast<int64_t>(a.ld_meta);
             const bool mine = (lane / 16) == acc;  // lanes 16*acc .. +15 carry this tile's metadata
-            for (int ks = 0; ks < n_stage; ++ks, ++q) {
-                const int s = q % S;
-                const uint32_t ph = (q / S) & 1;
-                uint32_t w[kMmaPerStage];
+            // the A_i2 words of a stage, loaded two stages ahead (the load latency is not exposed)
+            struct Words {
+                uint32_t a[kMmaPerStage], b[kMmaPerStage];
+            };
+            auto load_words = [&](int ks) -> Words {
+                Words r;
 #pragma unroll
                 for (int k = 0; k < kMmaPerStage; ++k) {
                     const int mi = ks * kMmaPerStage + k;
-                    uint32_t wa = 0x44444444u, wb = 0x44444444u;
-                    if (mine && mi < n_mma) {
-                        wa = __ldg(ma + mi);
-                        wb = __ldg(mb + mi);
-                    }
-                    w[k] = ((wa >> (16 * mh)) & 0xFFFFu) | (((wb >> (16 * mh)) & 0xFFFFu) << 16);
+                    const bool ok = mine && ks < k1 && mi < n_mma;
+                    r.a[k] = ok ? __ldg(ma + mi) : 0x44444444u;
+                    r.b[k] = ok ? __ldg(mb + mi) : 0x44444444u;
                 }
+                return r;
+            };
+            Words n1 = load_words(k0), n2 = load_words(k0 + 1);
+            for (int ks = k0; ks < k1; ++ks, ++q) {
+                const int s = q % S;
+                const uint32_t ph = (q / S) & 1;
+                const Words cur = n1;
+                n1 = n2;
+                n2 = load_words(ks + 2);
+                uint32_t w[kMmaPerStage];
+#pragma unroll
+                for (int k = 0; k < kMmaPerStage; ++k)
+                    w[k] = ((cur.a[k] >> (16 * mh)) & 0xFFFFu) | (((cur.b[k] >> (16 * mh)) & 0xFFFFu) << 16);
                 mbar_wait(&empty[s], ph ^ 1);
                 tmem_st_32x32b_x4(tmem + ((32 * qd) << 16) + kMetaCol + 4 * s, w[0], w[1], w[2], w[3]);
                 tmem_wait_st();
@@ -238,7 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ epilogue
         const int qd = warp - kEpiWarp0;
         int tl = 0;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++tl) {
+        for (int u = blockIdx.x; u < a.nunits; u += gridDim.x, ++tl) {
+            const int tile = u / a.ks_n, kspl = u % a.ks_n;
             const int vb = tile % a.nvb, n0 = (tile / a.nvb) * NT;
             const int acc = tl & 1;
             const uint32_t aph = (tl >> 1) & 1;
@@ -254,7 +282,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait_ld();
                 const int tcol = n0 + c;
                 if (row_ok && tcol < a.T) {
-                    if (!a.y_bf16) {
+                    if (a.ks_n > 1) {  // fp32 partial of K-slice kspl
+                        float* y = a.ws + (static_cast<int64_t>(kspl) * a.rows + row) * a.T + tcol;
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            if (tcol + k < a.T) y[k] = __uint_as_float(v[k]);
+                    } else if (!a.y_bf16) {
                         float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
                         if (tcol + 16 <= a.T) {
 #pragma unroll
@@ -294,6 +327,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == kMmaWarp) tmem_dealloc(tmem, 512);
+}
+
+// Y^T[row][t] = sum over the ks K-slices, in slice order (deterministic), then fp32 or bf16 (RNE)
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int ks, int rows, int T, void* YT, int64_t ldy,
+                                     int y_bf16) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<int64_t>(rows) * T) return;
+    const int row = static_cast<int>(idx / T), t = static_cast<int>(idx % T);
+    float acc = ws[idx];
+    for (int k = 1; k < ks; ++k) acc += ws[static_cast<int64_t>(k) * rows * T + idx];
+    if (y_bf16) {
+        reinterpret_cast<__nv_bfloat16*>(YT)[static_cast<int64_t>(row) * ldy + t] = __float2bfloat16_rn(acc);
+    } else {
+        reinterpret_cast<float*>(YT)[static_cast<int64_t>(row) * ldy + t] = acc;
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -336,6 +384,24 @@ bool encode_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Split K when the tiles cannot fill the GPU: minimise (waves of units) x (stages per unit + 1 for the
+// per-unit epilogue / pipeline refill), K-slices of at least 2 stages.
+int choose_ksplit(int ntiles, int n_stage) {
+    const int G = num_sms();
+    if (ntiles >= 2 * G) return 1;
+    int best = 1;
+    long best_cost = static_cast<long>((ntiles + G - 1) / G) * (n_stage + 1);
+    for (int ks = 2; ks <= 16 && 2 * ks <= n_stage; ++ks) {
+        const int sps = (n_stage + ks - 1) / ks;
+        const long cost = static_cast<long>((ntiles * ks + G - 1) / G) * (sps + 1);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = ks;
+        }
+    }
+    return best;
+}
+
 template <int NT>
 int launch_nt(const SpmmLaunch& L, const CUtensorMap& ta, SpmmArgs a, cudaStream_t st) {
     auto k = vnm_spmm_kernel<NT>;
@@ -343,15 +409,38 @@ int launch_nt(const SpmmLaunch& L, const CUtensorMap& ta, SpmmArgs a, cudaStream
         return kLaunchCudaError;
     a.ntt = (L.T + NT - 1) / NT;
     a.ntiles = a.nvb * a.ntt;
-    const int grid = a.ntiles < num_sms() ? a.ntiles : num_sms();
+    const int n_stage = (a.ld_meta + kMmaPerStage - 1) / kMmaPerStage;
+    a.ks_n = 1;
+    if (L.workspace) {
+        const int ks = choose_ksplit(a.ntiles, n_stage);
+        if (ks > 1 && L.workspace_bytes >= static_cast<size_t>(ks) * a.rows * L.T * 4) {
+            a.ks_n = ks;
+            a.ws = static_cast<float*>(L.workspace);
+        }
+    }
+    a.sps = (n_stage + a.ks_n - 1) / a.ks_n;
+    a.ks_n = (n_stage + a.sps - 1) / a.sps;  // no empty slices
+    a.nunits = a.ntiles * a.ks_n;
+    const int grid = a.nunits < num_sms() ? a.nunits : num_sms();
     k<<<grid, kThreads, Cfg<NT>::kSmem, st>>>(ta, a);
     count_launch();
+    if (a.ks_n > 1) {
+        const int64_t n = static_cast<int64_t>(a.rows) * L.T;
+        splitk_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(a.ws, a.ks_n, a.rows, L.T, a.YT, a.ldy,
+                                                                                    a.y_bf16);
+        count_launch();
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
 
 }  // namespace
 
-size_t spmm_workspace_bytes(const vnm_geom&, int32_t) { return 0; }
+size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T) {
+    if (g.V != kV || T <= 0 || T > 64 || g.nb_pad == 0) return 0;  // split-K serves the small-T (gather) plan
+    const int n_stage = (g.ld_meta + kMmaPerStage - 1) / kMmaPerStage;
+    const int ks = choose_ksplit(g.rows_p / kV, n_stage);
+    return ks > 1 ? static_cast<size_t>(ks) * g.rows * T * 4 : 0;
+}
 
 int launch_spmm(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;

@@ -6,17 +6,20 @@
 // the gather path (TMA gather4 7-15 B/clk/SM, cp.async ~27 B/clk/SM: MB3b) rather than by the MMA.  Here
 // every V x M block is an 8-channel window of the DENSE X^T tile — the sparse MMA's K-group stride is set
 // to M rows (UMMA SBO = M * 128 B; measured exact, probes2.cu "window") — so one X^T tile loaded by plain
-// 2D TMA serves all output rows: M = 128 MMAs (two V-blocks), the tile multicast across a CTA cluster.
+// 2D TMA serves all output rows: M = 128 MMAs (two V-blocks), and RT = 2 row tiles per CTA share each
+// X^T tile in shared memory (a 2-CTA multicast of the tile was measured no faster: at cluster size <= 4
+// multicast costs about the same L2 traffic as unicast).
 // Cost in tensor-core work: 8 logical K per block instead of 4, i.e. the same MMA time as the M = 64 gather
 // plan (2x K at 2x rate) for 5 <= M <= 8, with no gather at all.
 //
-// Tile = 128 output rows x NT = 192 tokens; stage = 4 MMAs (16 blocks, or 32 for M = 4).  Per CTA:
-//   warp 0     TMA: A (values_tc 128 x 64 bf16) and the stage's metadata chunk (2 KB bulk copy), plus this
-//              CTA's slice of the dense X^T tile, multicast to every CTA of the cluster;
-//   warp 1     MMA: tcgen05.cp (metadata smem -> TMEM) then 4 x tcgen05.mma.sp M=128 N=192; commits free
-//              the stage in every CTA of the cluster (multicast arrive);
-//   warps 4-7  epilogue: TMEM -> fp32 / bf16 -> Y^T (double-buffered accumulators in TMEM).
+// Tile = RT x 128 output rows x NT tokens; stage = 4 MMAs per row tile (16 blocks, or 32 for M = 4):
+//   warp 0     TMA: A (values_tc 128 x 64 bf16) and the metadata chunk (2 KB bulk copy) of each row tile,
+//              and the dense X^T tile (NT/64 boxes of 64 tokens x rows);
+//   warp 1     MMA: tcgen05.cp (metadata smem -> TMEM) then 4 x RT tcgen05.mma.sp M=128 N=NT;
+//   warps 4-7  epilogue: TMEM -> fp32 / bf16 -> Y^T (accumulators double-buffered when TMEM allows).
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -27,10 +30,7 @@
 namespace vnm {
 namespace {
 
-constexpr int kNT = 192;                 // tokens per tile (3 x 64-token TMA chunks)
-constexpr int kChunks = kNT / 64;
 constexpr int kThreads = 256;
-constexpr uint32_t kMetaCol = 2 * kNT;   // TMEM: acc0 [0,192), acc1 [192,384), metadata from 384
 constexpr uint32_t kABytes = 128 * 128;  // 128 rows x 64 bf16
 constexpr uint32_t kEBytes = 128 * 16;   // 128 lanes x 4 words
 
@@ -40,28 +40,13 @@ struct TcArgs {
     int64_t ldy;
     int32_t T, y_bf16, rows, M;
     int32_t n_mma, n_stage, n_rt, n_tt, n_rg, work;
+    int32_t row_major;   // tile order: row-tile-major (A reused across token tiles) or token-tile-major
     int32_t rows_stage;  // dense X^T rows advanced per stage
-    int32_t rb;          // B rows per stage per chunk (multiple of 8 * CS)
+    int32_t rb;          // B rows per stage per chunk (multiple of 8)
     int32_t stages;      // pipeline depth
     uint32_t b_stage_bytes, stage_bytes;
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* tmap, int32_t x, int32_t y, uint64_t* bar,
-                                               uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, "
-        "{%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
-        : "memory");
-}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -71,37 +56,64 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t d) {
     asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
 }
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"(mask)
-        : "memory");
+
+// 16 consecutive outputs of one Y^T row (fp32 or bf16 RNE), masked at T
+__device__ __forceinline__ void store_row16(const TcArgs& a, int row, int tcol, const uint32_t (&v)[16]) {
+    if (!a.y_bf16) {
+        float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
+        if (tcol + 16 <= a.T) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                reinterpret_cast<uint4*>(y)[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (tcol + k < a.T) y[k] = __uint_as_float(v[k]);
+        }
+    } else {
+        uint16_t* y = reinterpret_cast<uint16_t*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
+        uint32_t pk[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+            pk[k] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        if (tcol + 16 <= a.T) {
+            reinterpret_cast<uint4*>(y)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            reinterpret_cast<uint4*>(y)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (tcol + k < a.T) y[k] = static_cast<uint16_t>((pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+        }
+    }
 }
 
-template <int CS>
+// NT tokens per tile (NT/64 TMA chunks); RT row tiles of 128 rows per CTA share every B tile; NACC
+// accumulator sets (double buffering when they fit in TMEM next to the metadata slots).
+template <int NT, int RT>
 __global__ void __launch_bounds__(kThreads, 1)
     vnm_spmm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        const TcArgs a) {
+    constexpr int kChunks = NT / 64;
+    constexpr int NACC = 2 * RT * NT + 16 * RT <= 512 ? 2 : 1;
+    constexpr uint32_t kMetaCol = NACC * RT * NT;  // TMEM: accumulators, then 4 metadata columns per stage & tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = a.stages;
-    // per stage: [A 16 KB][B chunks][E 2 KB]
+    // per stage: [A x RT][B chunks][E x RT]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * a.stage_bytes);
     uint64_t* empty = full + S;
     uint64_t* tmem_full = empty + S;
     uint64_t* tmem_empty = tmem_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    const uint32_t b_off = RT * kABytes, e_off = RT * kABytes + a.b_stage_bytes;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = CS > 1 ? cluster_rank() : 0u;
-    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
-    const uint16_t all = static_cast<uint16_t>((1u << CS) - 1u);
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CS);
+            mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
@@ -115,119 +127,98 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmap_b);
     }
     tc_fence_before();
-    if (CS > 1) cluster_sync_all(); else __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int rb_rank = a.rb / CS;
 
     if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             int q = 0;
-            for (int w = cid; w < a.work; w += ncl) {
-                const int tt = w / a.n_rg, rt = (w % a.n_rg) * CS + static_cast<int>(rank);
-                const int n0 = tt * kNT;
+            for (int w = blockIdx.x; w < a.work; w += gridDim.x) {
+                const int rg = a.row_major ? w / a.n_tt : w % a.n_rg, tt = a.row_major ? w % a.n_tt : w / a.n_rg;
+                const int n0 = tt * NT;
                 for (int st = 0; st < a.n_stage; ++st, ++q) {
                     const int s = q % S;
-                    const uint32_t ph = (q / S) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
                     uint8_t* base = smem + s * a.stage_bytes;
-                    mbar_arrive_expect_tx(&full[s], kABytes + kEBytes + a.b_stage_bytes);
-                    tma_load_2d(base, &tmap_a, st * 64, rt * 128, &full[s]);
-                    const uint32_t* esrc = a.meta_tc + (static_cast<int64_t>(rt < a.n_rt ? rt : 0) * a.n_stage + st) * 512;
-                    bulk_load(base + kABytes + a.b_stage_bytes, esrc, kEBytes, &full[s]);
-                    const int y = st * a.rows_stage + static_cast<int>(rank) * rb_rank;
+                    mbar_arrive_expect_tx(&full[s], RT * (kABytes + kEBytes) + a.b_stage_bytes);
 #pragma unroll
-                    for (int c = 0; c < kChunks; ++c) {
-                        uint8_t* dst = base + kABytes + c * (a.rb * 128) + rank * (rb_rank * 128);
-                        if (CS > 1) tma_load_2d_mc(dst, &tmap_b, n0 + 64 * c, y, &full[s], all);
-                        else tma_load_2d(dst, &tmap_b, n0 + 64 * c, y, &full[s]);
+                    for (int j = 0; j < RT; ++j) {
+                        const int rt = rg * RT + j;  // row tiles past n_rt read as zeros (TMA OOB)
+                        tma_load_2d(base + j * kABytes, &tmap_a, st * 64, rt * 128, &full[s]);
+                        const int rte = rt < a.n_rt ? rt : 0;
+                        bulk_load(base + e_off + j * kEBytes, a.meta_tc + (static_cast<int64_t>(rte) * a.n_stage + st) * 512,
+                                  kEBytes, &full[s]);
                     }
+#pragma unroll
+                    for (int c = 0; c < kChunks; ++c)
+                        tma_load_2d(base + b_off + c * (a.rb * 128), &tmap_b, n0 + 64 * c, st * a.rows_stage, &full[s]);
                 }
             }
         }
     } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             int q = 0, tl = 0;
-            const uint32_t idesc0 = idesc_bf16(128, kNT, true, 0, true);
-            const uint32_t idesc1 = idesc_bf16(128, kNT, true, 1, true);
+            const uint32_t idesc0 = idesc_bf16(128, NT, true, 0, true);
+            const uint32_t idesc1 = idesc_bf16(128, NT, true, 1, true);
             const uint32_t k_bytes = (a.M == 4 ? 32u : 4u * a.M) * 128u;  // B advance per MMA
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;          // K-group (window) stride
-            for (int w = cid; w < a.work; w += ncl, ++tl) {
-                const int acc = tl & 1;
-                mbar_wait(&tmem_empty[acc], ((tl >> 1) & 1) ^ 1);
+            for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++tl) {
+                const int acc = NACC == 2 ? (tl & 1) : 0;
+                mbar_wait(&tmem_empty[acc], ((NACC == 2 ? (tl >> 1) : tl) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + acc * kNT;
                 for (int st = 0; st < a.n_stage; ++st, ++q) {
                     const int s = q % S;
                     mbar_wait(&full[s], (q / S) & 1);
                     tc_fence_after();
                     uint8_t* base = smem + s * a.stage_bytes;
-                    tmem_cp_128x128b(tmem + kMetaCol + 4 * s, sdesc(smem_u32(base + kABytes + a.b_stage_bytes), 16, 128, 0));
-                    const uint32_t a0 = smem_u32(base), b0 = smem_u32(base + kABytes);
+                    const uint32_t meta_s = tmem + kMetaCol + 4 * RT * s;
+#pragma unroll
+                    for (int j = 0; j < RT; ++j)
+                        tmem_cp_128x128b(meta_s + 4 * j, sdesc(smem_u32(base + e_off + j * kEBytes), 16, 128, 0));
+                    const uint32_t b0 = smem_u32(base + b_off);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int mi = st * 4 + k;
                         if (mi < a.n_mma) {
-                            const uint64_t ad = sdesc(a0 + 32 * k, 16, 1024, kLayoutSW128);
                             const uint64_t bd = sdesc(b0 + k * k_bytes, a.rb * 128, sbo, kLayoutSW128);
-                            mma_sp_bf16(d, ad, bd, tmem + kMetaCol + 4 * s + (k & ~1), (k & 1) ? idesc1 : idesc0,
-                                        mi > 0 ? 1u : 0u);
+#pragma unroll
+                            for (int j = 0; j < RT; ++j) {
+                                const uint64_t ad = sdesc(smem_u32(base + j * kABytes) + 32 * k, 16, 1024, kLayoutSW128);
+                                mma_sp_bf16(tmem + (acc * RT + j) * NT, ad, bd, meta_s + 4 * j + (k & ~1),
+                                            (k & 1) ? idesc1 : idesc0, mi > 0 ? 1u : 0u);
+                            }
                         }
                     }
-                    if (CS > 1) mma_commit_mc(&empty[s], all); else mma_commit(&empty[s]);
+                    mma_commit(&empty[s]);
                 }
                 mma_commit(&tmem_full[acc]);
             }
         }
     } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
         const int qd = warp - 4;
         int tl = 0;
-        for (int w = cid; w < a.work; w += ncl, ++tl) {
-            const int tt = w / a.n_rg, rt = (w % a.n_rg) * CS + static_cast<int>(rank);
-            const int n0 = tt * kNT;
-            const int acc = tl & 1;
-            mbar_wait(&tmem_full[acc], (tl >> 1) & 1);
+        for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++tl) {
+            const int rg = a.row_major ? w / a.n_tt : w % a.n_rg, tt = a.row_major ? w % a.n_tt : w / a.n_rg;
+            const int n0 = tt * NT;
+            const int acc = NACC == 2 ? (tl & 1) : 0;
+            mbar_wait(&tmem_full[acc], (NACC == 2 ? (tl >> 1) : tl) & 1);
             tc_fence_after();
-            const int row = rt * 128 + 32 * qd + lane;
-            const bool row_ok = rt < a.n_rt && row < a.rows;
 #pragma unroll 1
-            for (int c = 0; c < kNT; c += 16) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + acc * kNT + c, v);
-                tmem_wait_ld();
-                const int tcol = n0 + c;
-                if (row_ok && tcol < a.T) {
-                    if (!a.y_bf16) {
-                        float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
-                        if (tcol + 16 <= a.T) {
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                reinterpret_cast<uint4*>(y)[k] =
-                                    make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < 16; ++k)
-                                if (tcol + k < a.T) y[k] = __uint_as_float(v[k]);
-                        }
-                    } else {
-                        uint16_t* y = reinterpret_cast<uint16_t*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
-                        uint32_t pk[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            __nv_bfloat162 h =
-                                __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-                            pk[k] = *reinterpret_cast<uint32_t*>(&h);
-                        }
-                        if (tcol + 16 <= a.T) {
-                            reinterpret_cast<uint4*>(y)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                            reinterpret_cast<uint4*>(y)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < 16; ++k)
-                                if (tcol + k < a.T)
-                                    y[k] = static_cast<uint16_t>((pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
-                        }
-                    }
+            for (int j = 0; j < RT; ++j) {
+                const int rt = rg * RT + j;
+                const int row = rt * 128 + 32 * qd + lane;
+                const bool row_ok = rt < a.n_rt && row < a.rows;
+#pragma unroll 1
+                for (int c = 0; c < NT; c += 16) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + (acc * RT + j) * NT + c, v);
+                    tmem_wait_ld();
+                    const int tcol = n0 + c;
+                    if (row_ok && tcol < a.T) store_row16(a, row, tcol, v);
                 }
             }
             tc_fence_before();
@@ -236,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     tc_fence_before();
-    if (CS > 1) cluster_sync_all(); else __syncthreads();
+    __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -279,21 +270,21 @@ int sm_count() {
     return n;
 }
 
-template <int CS>
-int launch_cs(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
+template <int NT, int RT>
+int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
+    constexpr int kChunks = NT / 64;
     const vnm_geom& g = L.P->g;
-    const int rows_stage = g.M == 4 ? 128 : 16 * g.M;
+    a.n_tt = (L.T + NT - 1) / NT;
+    a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
     const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // rows one stage's windows touch
-    a.rows_stage = rows_stage;
-    a.rb = (need + 8 * CS - 1) / (8 * CS) * (8 * CS);
+    a.rb = (need + 7) / 8 * 8;
     a.b_stage_bytes = static_cast<uint32_t>(kChunks * a.rb * 128);
-    a.stage_bytes = kABytes + a.b_stage_bytes + kEBytes;
+    a.stage_bytes = RT * (kABytes + kEBytes) + a.b_stage_bytes;
     a.stage_bytes = (a.stage_bytes + 1023) / 1024 * 1024;
-    const uint32_t budget = 224 * 1024;
-    a.stages = static_cast<int>(budget / a.stage_bytes);
+    a.stages = static_cast<int>((224u * 1024u) / a.stage_bytes);
     if (a.stages > 4) a.stages = 4;
     if (a.stages < 2) return kLaunchUnsupported;
-    a.n_rg = (a.n_rt + CS - 1) / CS;
+    a.n_rg = (a.n_rt + RT - 1) / RT;
     a.work = a.n_rg * a.n_tt;
     CUtensorMap ta, tb;
     const int ld_tc = 16 * a.n_mma;
@@ -302,27 +293,14 @@ int launch_cs(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
                 static_cast<uint64_t>(ld_tc) * 2, 64, 128))
         return kLaunchCudaError;
     if (!encode(&tb, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
-                64, static_cast<uint32_t>(a.rb / CS)))
+                64, static_cast<uint32_t>(a.rb)))
         return kLaunchCudaError;
     const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + 1024 + 256;
-    auto k = vnm_spmm_tc_kernel<CS>;
+    auto k = vnm_spmm_tc_kernel<NT, RT>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
-    int clusters = sm_count() / CS;
-    if (clusters > a.work) clusters = a.work;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * CS);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k, ta, tb, a) != cudaSuccess) return kLaunchCudaError;
+    const int grid = a.work < sm_count() ? a.work : sm_count();
+    k<<<grid, kThreads, smem, stream>>>(ta, tb, a);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
@@ -343,8 +321,20 @@ int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream) {
     a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
     a.n_stage = (a.n_mma + 3) / 4;
     a.n_rt = (g.rows_p + 127) / 128;
-    a.n_tt = (L.T + kNT - 1) / kNT;
-    return launch_cs<2>(L, a, stream);
+    // Plan (measured, profiles/r01_*): long K (many stages per tile) -> NT = 256, one accumulator (the
+    // epilogue is amortised over the K loop); short K -> NT = 192 with double-buffered accumulators so the
+    // epilogue overlaps the next tile.  RT = 2 (two row tiles sharing each X^T tile) measured no faster.
+    // VNM_TC_CFG="NT,RT" overrides (tuning experiments).
+    // Tile order: the larger operand is the one to keep hot in L2 across the tiles resident at a time —
+    // row-tile-major when the window-form weights outweigh X^T (Llama), token-tile-major otherwise (DeiT).
+    a.row_major = static_cast<int64_t>(a.n_rt) * 128 * 16 * a.n_mma > static_cast<int64_t>(g.cols) * L.T ? 1 : 0;
+    int nt = a.n_stage >= 12 ? 256 : 192, rt = 1;
+    if (const char* e = getenv("VNM_TC_CFG")) sscanf(e, "%d,%d", &nt, &rt);
+    if (nt == 256 && rt == 1) return launch_cfg<256, 1>(L, a, stream);
+    if (nt == 128 && rt == 1) return launch_cfg<128, 1>(L, a, stream);
+    if (nt == 128 && rt == 2) return launch_cfg<128, 2>(L, a, stream);
+    if (nt == 192 && rt == 2) return launch_cfg<192, 2>(L, a, stream);
+    return launch_cfg<192, 1>(L, a, stream);
 }
 
 }  // namespace vnm

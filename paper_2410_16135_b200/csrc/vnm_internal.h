@@ -26,6 +26,8 @@ struct PruneLaunch {
     uint8_t* col_idx;
     uint32_t* meta;
     int32_t* status;         // compress only, may be null
+    uint16_t* values_tc = nullptr;  // optional fused window form (prune_compress)
+    uint32_t* meta_tc = nullptr;
 };
 int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream);
 

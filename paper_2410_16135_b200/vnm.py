@@ -206,13 +206,15 @@ def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None =
     _require_cuda(W, score)
     g = geometry(W.shape[0], W.shape[1], V, M)
     P = Packed.empty(g, W.device)
+    if tc and V == 64 and M <= 8:
+        nv, nm = tc_bytes(g)
+        P.values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=W.device)
+        P.meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=W.device)
     mask = torch.empty((g.rows_p, g.ld_mask), dtype=torch.int32, device=W.device) if want_mask else None
     cp = P.c()
     _check(lib().vnm_prune_compress(_ptr(W), _ld(W), _ptr(score), _ld(score) if score is not None else 0,
                                     ctypes.byref(g), ctypes.byref(cp), _ptr(mask), _stream(W.device)),
            "vnm_prune_compress")
-    if tc and V == 64 and M <= 8:
-        pack_tc(P)
     return (P, mask) if want_mask else P
 
 
@@ -234,6 +236,10 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
     if out.dtype not in (torch.bfloat16, torch.float32):
         raise TypeError("Y^T must be fp32 or bf16")
     cp = P.c()
+    if workspace is None:  # split-K scratch for the small-T plan (the library allocates no device memory)
+        nws = spmm_workspace_bytes(g, T)
+        if nws:
+            workspace = torch.empty(nws // 4, dtype=torch.float32, device=XT.device)
     ws_ptr, ws_bytes = (_ptr(workspace), workspace.numel() * workspace.element_size()) if workspace is not None \
         else (None, 0)
     _check(lib().vnm_spmm(_ptr(XT), XT.stride(0), T, ctypes.byref(cp), _ptr(out), out.stride(0), ydt, ws_ptr,

@@ -122,3 +122,18 @@ def test_strided_input():
     assert Wd.stride(0) == 136
     mask = u32(vnm.prune(Wd, 64, 5))
     assert np.array_equal(mask, oracle.prune(W, 64, 5))
+
+
+@pytest.mark.parametrize("rows,cols,M", [(128, 512, 5), (192, 333, 8), (70, 90, 4), (300, 1000, 6), (64, 257, 7),
+                                         (4096, 4096, 5)])
+def test_window_form_fused_equals_standalone(rows, cols, M):
+    """vnm_prune_compress writing values_tc / meta_tc in the same pass == vnm_pack_tc of its canonical output."""
+    W = synth.weights(rows, cols, seed=rows + cols + M)
+    Wd = to_dev_bf16(W)
+    P = vnm.prune_compress(Wd, 64, M, tc=True)
+    Q = vnm.prune_compress(Wd, 64, M)
+    vnm.pack_tc(Q)
+    torch.cuda.synchronize()
+    assert torch.equal(P.values.view(torch.int16), Q.values.view(torch.int16))
+    assert torch.equal(P.values_tc.view(torch.int16), Q.values_tc.view(torch.int16))
+    assert torch.equal(P.meta_tc, Q.meta_tc)
