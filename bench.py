@@ -81,7 +81,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.index), "-lms", "200"], stdout=subprocess.PIPE,
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -221,10 +221,16 @@ def run_gpu(args):
         step()
     barrier()
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
-    n_launch0 = vnm.launch_count()
     step_ms, pc_ms, sp_ms = [], [[] for _ in layers], [[] for _ in layers]
     with ClockSampler(local) as clk:
+        # keep the GPU under this same load for >= 0.6 s right before the timed steps so nvidia-smi (200 ms
+        # period) sees the clocks of this workload; these steps are not timed
+        t_load = time.perf_counter() + 0.6
+        while time.perf_counter() < t_load:
+            step()
+            torch.cuda.synchronize(dev)
         barrier()
+        n_launch0 = vnm.launch_count()
         for _ in range(args.steps):
             flush.zero_()
             ev = [(E(), E(), E()) for _ in layers]
@@ -237,8 +243,8 @@ def run_gpu(args):
             for i in range(len(layers)):
                 pc_ms[i].append(ev[i][0].elapsed_time(ev[i][1]))
                 sp_ms[i].append(ev[i][1].elapsed_time(ev[i][2]))
+        launches = vnm.launch_count() - n_launch0
         barrier()
-    launches = vnm.launch_count() - n_launch0
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)

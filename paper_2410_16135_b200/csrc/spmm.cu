@@ -12,7 +12,8 @@
 //              on the stage barrier asynchronously (cp.async.mbarrier.arrive.noinc).  TMA tile::gather4 was
 //              measured at only 7-15 B/clk/SM (csrc/probes2.cu MB3b) and is not used;
 //   warp 16    TMA: the stage's A_n tile (64 x 64 bf16, 128B swizzle, K-major);
-//   warps 4-7  metadata: A_i2 words -> TMEM in the M=64 sparse-metadata layout (tcgen05.st);
+//   warps 4-7  metadata: A_i2 words (staged in smem by the gather threads) -> TMEM in the M=64
+//              sparse-metadata layout (tcgen05.st);
 //   warp 17    one thread issues tcgen05.mma.sp.cta_group::1.kind::f16 M=64 N=NT into TMEM;
 //   warps 0-3  epilogue: tcgen05.ld -> fp32 / bf16 -> Y^T.
 // Two accumulators share TMEM columns: accumulator a (a = tile parity) and its metadata live in lanes
@@ -24,6 +25,8 @@
 //              16a + (m % 8) + 8*(g/4) + 32*(m/16), column e_col + id2 (e_col even).
 //   D and E must carry the same lane offset (0 or 16).
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -59,12 +62,18 @@ struct SpmmArgs {
     // ws[k][row][t] (fp32) and a second kernel adds the ks_n slices in order (deterministic)
     int32_t ks_n, sps, nunits;
     float* ws;
+    int32_t trace;  // VNM_SPMM_TRACE: record per-stage clock64 stamps of CTA 0 (g_trace)
 };
+
+// debug trace (VNM_SPMM_TRACE=1): clock64 stamps of CTA 0 per pipeline stage q:
+// [0] A TMA issued, [1] MMA saw full, [2] MMA saw meta_ready, [3] gather warp 0 issued, [4] MMA committed
+__device__ unsigned long long g_trace[5][512];
 
 template <int NT>
 struct Cfg {
     static constexpr int kBBytes = kKRowsPerStage * NT * 2;
-    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kMetaBytes = kV * kMmaPerStage * 4;  // A_i2 words of the stage: [64 rows][4]
+    static constexpr int kStageBytes = kABytes + kBBytes + kMetaBytes;
     static constexpr int kStages = NT == 256 ? 3 : (NT == 128 ? 5 : 8);
     static constexpr int kSmem = kStages * kStageBytes + 1024 + 512;
 };
@@ -83,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * kABytes;
+    uint32_t* sMeta = reinterpret_cast<uint32_t*>(sB + S * C::kBBytes);  // [S][64][4]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
     uint64_t* empty = full + S;
     uint64_t* meta_ready = empty + S;
@@ -115,49 +125,74 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp >= kGatherWarp0 && warp < kGatherWarp0 + kGatherWarps) {
         // ------------------------------------------------------------ gather producers (B = kept X^T rows)
-        // Warp pw owns blocks 4pw..4pw+3 of every stage (gathered rows 16pw..16pw+15); each lane moves 16 B
-        // (8 tokens) per cp.async, zero-filled past T (tokens) and past cols (padded channels).
-        constexpr int CPR = NT / 8;       // 16-byte chunks per gathered row
-        constexpr int RPI = 32 / CPR;     // rows per warp instruction
+        // Warp pw owns blocks 4pw..4pw+3 of every stage (gathered rows 16pw..16pw+15); each cp.async moves 16 B
+        // (8 tokens), zero-filled past cols (padded channels) and past T inside the last chunk.
         const int pw = warp - kGatherWarp0;
-        const int sub = lane / CPR, ch = lane % CPR;
-        const uint32_t dst_chunk = (ch / 8) * (kKRowsPerStage * 128);
         int q = 0;
         for (int u = blockIdx.x; u < a.nunits; u += gridDim.x) {
             const int tile = u / a.ks_n, k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
             const int vb = tile % a.nvb, n0 = (tile / a.nvb) * NT;
             const uint32_t* ci_vb = reinterpret_cast<const uint32_t*>(a.col_idx) + static_cast<int64_t>(vb) * a.nb_pad;
-            int tok_bytes = (a.T - (n0 + 8 * ch)) * 2;
-            tok_bytes = tok_bytes < 0 ? 0 : (tok_bytes > 16 ? 16 : tok_bytes);
-            const uint16_t* xt_tok = a.XT + n0 + 8 * ch;
-            // A_i1 words of this warp's 4 blocks, loaded two stages ahead (the load latency is not exposed)
+            // only the 16-byte chunks holding tokens < T are copied: lanes form groups of gsz (power of two
+            // >= chunks per row), one row per group, so a decode stage (T <= 16) is one instruction per warp.
+            // Everything that does not depend on the stage is computed here, once per unit.
+            const int tt_tok = min(a.T - n0, NT);
+            const int cu = (tt_tok + 7) / 8;  // 16-byte chunks per row holding tokens < T
+            const int lg = cu <= 1 ? 0 : 32 - __clz(cu - 1);  // log2(gsz)
+            const int chn = lane & ((1 << lg) - 1), rsub = lane >> lg;
+            const int rows_it = 32 >> lg;                       // rows per instruction
+            const int n_it = rows_it >= 16 ? 1 : 16 / rows_it;
+            const bool lane_ok = chn < cu && rsub < 16;
+            int tokb = (tt_tok - 8 * chn) * 2;
+            tokb = tokb > 16 ? 16 : (tokb < 0 ? 0 : tokb);
+            const uint16_t* xt_lane = a.XT + n0 + 8 * chn;
+            const uint32_t dst_lane = (chn >> 3) * (kKRowsPerStage * 128);
+            const int M_ = a.M, cols_ = a.cols;
+            const int64_t ldx_ = a.ldx;
+            // this lane's A_i2 word copy: word (t % 4) of row t / 4 of the V-block, t = 32 pw + lane
+            const int mrow = (32 * pw + lane) >> 2, mk = lane & 3;
+            const uint32_t* meta_lane = a.meta + static_cast<int64_t>(vb * kV + mrow) * a.ld_meta + mk;
+            // A_i1 words of this warp's 4 blocks are loaded 4 stages ahead into 4 rotating registers that are
+            // consumed in place (copying a register whose load is still in flight would wait for the load)
             auto load_ci = [&](int ks) -> uint32_t {
                 const int blk_l = ks * kBlocksPerStage + 4 * pw + (lane & 3);
                 return (ks < k1 && blk_l < a.nb_pad) ? __ldg(ci_vb + blk_l) : 0xFFFFFFFFu;
             };
-            uint32_t ci_n1 = load_ci(k0), ci_n2 = load_ci(k0 + 1);
-            for (int ks = k0; ks < k1; ++ks, ++q) {
+            auto do_stage = [&](int ks, uint32_t ci) {
                 const int s = q % S;
                 const uint32_t ph = (q / S) & 1;
-                const uint32_t ci = ci_n1;
-                ci_n1 = ci_n2;
-                ci_n2 = load_ci(ks + 2);
                 mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* bst = sB + s * C::kBBytes + dst_chunk;
-#pragma unroll
-                for (int it = 0; it < 16 / RPI; ++it) {
-                    const int rl = it * RPI + sub;             // 0..15 within the warp's rows
-                    const int r = 16 * pw + rl;                // gathered row of the stage (0..127)
-                    const uint32_t cw = __shfl_sync(0xffffffffu, ci, rl >> 2);
-                    const int blk = ks * kBlocksPerStage + (r >> 2);
-                    const int krow = blk * a.M + static_cast<int>((cw >> (8 * (r & 3))) & 0xFFu);
-                    const bool ok = cw != 0xFFFFFFFFu && krow < a.cols;
-                    const int bytes = ok ? tok_bytes : 0;
-                    const uint16_t* src = bytes ? xt_tok + static_cast<int64_t>(krow) * a.ldx : a.XT;
-                    cp_async_16(bst + (r >> 3) * 1024 + sw128_offset(r & 7, (ch & 7) * 16), src,
-                                static_cast<uint32_t>(bytes));
+                const uint32_t bst = smem_u32(sB + s * C::kBBytes) + dst_lane;
+                const int blk0 = ks * kBlocksPerStage + 4 * pw;
+#pragma unroll 1
+                for (int it = 0; it < n_it; ++it) {
+                    const int rl = it * rows_it + rsub;  // row of this warp's 16 (0..15)
+                    const uint32_t cw = __shfl_sync(0xffffffffu, ci, (rl >> 2) & 3);
+                    const int krow = (blk0 + (rl >> 2)) * M_ + static_cast<int>((cw >> (8 * (rl & 3))) & 0xFFu);
+                    const int bytes = (cw == 0xFFFFFFFFu || krow >= cols_) ? 0 : tokb;  // padded channel: zero fill
+                    const int r = 16 * pw + rl;  // gathered row of the stage (0..127)
+                    if (lane_ok && tokb > 0)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                                         bst + (r >> 3) * 1024 + (r & 7) * 128 + (((r ^ chn) & 7) << 4)),
+                                     "l"(bytes ? xt_lane + krow * ldx_ : a.XT), "r"(bytes)
+                                     : "memory");
+                }
+                {   // this stage's A_i2 words
+                    const int mi = ks * kMmaPerStage + mk;
+                    cp_async_4(sMeta + (s * kV + mrow) * kMmaPerStage + mk, mi < n_mma ? meta_lane + ks * kMmaPerStage : a.meta,
+                               mi < n_mma ? 4u : 0u);
                 }
                 cp_async_arrive_noinc(&full[s]);
+                if (a.trace && blockIdx.x == 0 && pw == 0 && lane == 0 && q < 512) g_trace[3][q] = clock64();
+                ++q;
+            };
+            uint32_t c0 = load_ci(k0), c1 = load_ci(k0 + 1), c2 = load_ci(k0 + 2), c3 = load_ci(k0 + 3);
+            for (int ks = k0; ks < k1; ks += 4) {
+                do_stage(ks, c0);
+                c0 = load_ci(ks + 4);
+                if (ks + 1 < k1) { do_stage(ks + 1, c1); c1 = load_ci(ks + 5); }
+                if (ks + 2 < k1) { do_stage(ks + 2, c2); c2 = load_ci(ks + 6); }
+                if (ks + 3 < k1) { do_stage(ks + 3, c3); c3 = load_ci(ks + 7); }
             }
         }
     } else if (warp == kProdWarp) {
@@ -173,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], kABytes);
                     tma_load_2d(sA + s * kABytes, &tmap_a, ks * (2 * kBlocksPerStage), vb * kV, &full[s]);
+                    if (a.trace && blockIdx.x == 0 && q < 512) g_trace[0][q] = clock64();
                 }
             }
         }
@@ -193,7 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = q % S;
                     const uint32_t ph = (q / S) & 1;
                     mbar_wait(&full[s], ph);
+                    if (a.trace && blockIdx.x == 0 && q < 512) g_trace[1][q] = clock64();
                     mbar_wait(&meta_ready[s], ph);
+                    if (a.trace && blockIdx.x == 0 && q < 512) g_trace[2][q] = clock64();
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sA + s * kABytes);
                     const uint32_t b_base = smem_u32(sB + s * C::kBBytes);
@@ -208,14 +246,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     mma_commit(&empty[s]);
+                    if (a.trace && blockIdx.x == 0 && q < 512) g_trace[4][q] = clock64();
                 }
                 mma_commit(&tmem_full[acc]);
             }
         }
     } else if (warp >= kMetaWarp0 && warp < kMetaWarp0 + 4) {
         // ------------------------------------------------------------ metadata -> TMEM
-        // The slot of stage s is reused only after the MMAs that read it completed (empty[s]); lanes of the
-        // other accumulator's half are written with a don't-care pattern (no in-flight MMA reads slot s).
+        // A_i2 words arrive in shared memory with the stage (gather threads, cp.async); these warps repack
+        // them into the M = 64 TMEM metadata layout.  Lanes of the other accumulator's half are written with
+        // a don't-care pattern (no in-flight MMA reads slot s).
         const int qd = warp - kMetaWarp0;  // TMEM sub-partition (== warp % 4)
         const int ml = lane % 16, mh = ml / 8;
         int q = 0, tl = 0;
@@ -223,37 +263,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tile = u / a.ks_n, k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
             const int vb = tile % a.nvb;
             const int acc = tl & 1;
-            const int row_a = vb * kV + 16 * qd + (ml % 8);
-            const uint32_t* ma = a.meta + static_cast<int64_t>(row_a) * a.ld_meta;
-            const uint32_t* mb = ma + 8 * static_cast<int64_t>(a.ld_meta);
+            const int ra = 16 * qd + (ml % 8), rb = ra + 8;  // rows of the V-block this lane combines
             const bool mine = (lane / 16) == acc;  // lanes 16*acc .. +15 carry this tile's metadata
-            // the A_i2 words of a stage, loaded two stages ahead (the load latency is not exposed)
-            struct Words {
-                uint32_t a[kMmaPerStage], b[kMmaPerStage];
-            };
-            auto load_words = [&](int ks) -> Words {
-                Words r;
-#pragma unroll
-                for (int k = 0; k < kMmaPerStage; ++k) {
-                    const int mi = ks * kMmaPerStage + k;
-                    const bool ok = mine && ks < k1 && mi < n_mma;
-                    r.a[k] = ok ? __ldg(ma + mi) : 0x44444444u;
-                    r.b[k] = ok ? __ldg(mb + mi) : 0x44444444u;
-                }
-                return r;
-            };
-            Words n1 = load_words(k0), n2 = load_words(k0 + 1);
+            (void)vb;
             for (int ks = k0; ks < k1; ++ks, ++q) {
                 const int s = q % S;
                 const uint32_t ph = (q / S) & 1;
-                const Words cur = n1;
-                n1 = n2;
-                n2 = load_words(ks + 2);
+                // the words landed with the stage's gathers (full[s]); full[s] also implies the MMAs that read
+                // this TMEM slot in the previous round have completed
+                mbar_wait(&full[s], ph);
+                const uint4 wa4 = *reinterpret_cast<const uint4*>(sMeta + (s * kV + ra) * kMmaPerStage);
+                const uint4 wb4 = *reinterpret_cast<const uint4*>(sMeta + (s * kV + rb) * kMmaPerStage);
+                const uint32_t wa[4] = {wa4.x, wa4.y, wa4.z, wa4.w}, wb[4] = {wb4.x, wb4.y, wb4.z, wb4.w};
                 uint32_t w[kMmaPerStage];
 #pragma unroll
                 for (int k = 0; k < kMmaPerStage; ++k)
-                    w[k] = ((cur.a[k] >> (16 * mh)) & 0xFFFFu) | (((cur.b[k] >> (16 * mh)) & 0xFFFFu) << 16);
-                mbar_wait(&empty[s], ph ^ 1);
+                    w[k] = mine ? (((wa[k] >> (16 * mh)) & 0xFFFFu) | (((wb[k] >> (16 * mh)) & 0xFFFFu) << 16))
+                                : 0x44444444u;
                 tmem_st_32x32b_x4(tmem + ((32 * qd) << 16) + kMetaCol + 4 * s, w[0], w[1], w[2], w[3]);
                 tmem_wait_st();
                 tc_fence_before();
@@ -410,6 +436,7 @@ int launch_nt(const SpmmLaunch& L, const CUtensorMap& ta, SpmmArgs a, cudaStream
     a.ntt = (L.T + NT - 1) / NT;
     a.ntiles = a.nvb * a.ntt;
     const int n_stage = (a.ld_meta + kMmaPerStage - 1) / kMmaPerStage;
+    a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
     a.ks_n = 1;
     if (L.workspace) {
         const int ks = choose_ksplit(a.ntiles, n_stage);
@@ -424,6 +451,17 @@ int launch_nt(const SpmmLaunch& L, const CUtensorMap& ta, SpmmArgs a, cudaStream
     const int grid = a.nunits < num_sms() ? a.nunits : num_sms();
     k<<<grid, kThreads, Cfg<NT>::kSmem, st>>>(ta, a);
     count_launch();
+    if (getenv("VNM_SPMM_TRACE")) {
+        static unsigned long long h[5][512];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+        const unsigned long long t0 = h[0][0];
+        for (int qq = 0; qq < 64; ++qq)
+            fprintf(stderr, "trace q=%d tma=%lld gather=%lld full=%lld meta=%lld commit=%lld\n", qq,
+                    (long long)(h[0][qq] - t0),
+                    (long long)(h[3][qq] - t0), (long long)(h[1][qq] - t0), (long long)(h[2][qq] - t0),
+                    (long long)(h[4][qq] - t0));
+    }
     if (a.ks_n > 1) {
         const int64_t n = static_cast<int64_t>(a.rows) * L.T;
         splitk_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(a.ws, a.ks_n, a.rows, L.T, a.YT, a.ldy,
