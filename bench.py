@@ -174,7 +174,8 @@ def run_gpu(args):
     def prune_compress(l):
         cp = l["P"].c()
         st = L.vnm_prune_compress(ctypes.c_void_p(l["W"].data_ptr()), l["W"].stride(0), None, 0,
-                                  ctypes.byref(l["P"].g), ctypes.byref(cp), None, ctypes.c_void_p(stream.cuda_stream))
+                                  ctypes.byref(l["P"].g), ctypes.byref(cp), None,
+                                  ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
         assert st == 0, vnm.status_string(st)
 
     for l in layers:  # split-K scratch (small T), allocated once outside the timed region
@@ -187,19 +188,20 @@ def run_gpu(args):
         st = L.vnm_spmm(ctypes.c_void_p(l["X"].data_ptr()), l["X"].stride(0), T, ctypes.byref(cp),
                         ctypes.c_void_p(l["Y"].data_ptr()), l["Y"].stride(0), vnm.VNM_BF16,
                         ctypes.c_void_p(ws.data_ptr()) if ws is not None else None,
-                        ws.numel() * 4 if ws is not None else 0, ctypes.c_void_p(stream.cuda_stream))
+                        ws.numel() * 4 if ws is not None else 0,
+                        ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
         assert st == 0, vnm.status_string(st)
 
     def step(ev=None):
         for i, l in enumerate(layers):
             if ev is not None:
-                ev[i][0].record(stream)
+                ev[i][0].record()
             prune_compress(l)
             if ev is not None:
-                ev[i][1].record(stream)
+                ev[i][1].record()
             spmm(l)
             if ev is not None:
-                ev[i][2].record(stream)
+                ev[i][2].record()
 
     def step_e2e():
         for l in layers:
@@ -216,9 +218,21 @@ def run_gpu(args):
         torch.cuda.synchronize(dev)
 
     E = lambda: torch.cuda.Event(enable_timing=True)
+    # ---- the step is captured once into a CUDA graph (every launch of the step, through the C ABI, replayed
+    # each timed step); per-launch timing events are graph nodes (external events)
+    for _ in range(2):
+        step()  # module loading / first-touch outside the capture
+    torch.cuda.synchronize(dev)
+    EX = lambda: torch.cuda.Event(enable_timing=True, external=True)
+    ev = [(EX(), EX(), EX()) for _ in layers]
+    graph = torch.cuda.CUDAGraph()
+    n_launch0 = vnm.launch_count()
+    with torch.cuda.graph(graph):
+        step(ev)
+    launches_per_step = vnm.launch_count() - n_launch0
     # ---- warm-up
     for _ in range(args.warmup):
-        step()
+        graph.replay()
     barrier()
     # ---- timed region: K steps, L2 flushed between steps (outside the events)
     step_ms, pc_ms, sp_ms = [], [[] for _ in layers], [[] for _ in layers]
@@ -227,23 +241,21 @@ def run_gpu(args):
         # period) sees the clocks of this workload; these steps are not timed
         t_load = time.perf_counter() + 0.6
         while time.perf_counter() < t_load:
-            step()
+            graph.replay()
             torch.cuda.synchronize(dev)
         barrier()
-        n_launch0 = vnm.launch_count()
         for _ in range(args.steps):
             flush.zero_()
-            ev = [(E(), E(), E()) for _ in layers]
             s0, s1 = E(), E()
             s0.record(stream)
-            step(ev)
+            graph.replay()
             s1.record(stream)
             torch.cuda.synchronize(dev)
             step_ms.append(s0.elapsed_time(s1))
             for i in range(len(layers)):
                 pc_ms[i].append(ev[i][0].elapsed_time(ev[i][1]))
                 sp_ms[i].append(ev[i][1].elapsed_time(ev[i][2]))
-        launches = vnm.launch_count() - n_launch0
+        launches = launches_per_step * args.steps
         barrier()
     total_ms = sum(step_ms)
     if world > 1:
@@ -332,7 +344,8 @@ def run_gpu(args):
                "config": {"workload": f"{args.workload} V:N:M {V}:2:{M}", "tokens_per_gpu": T,
                           "layers": [f"{n} {c}->{r}" for n, r, c in wl["layers"]],
                           "parallelism": f"token-sharded x{world}" if world > 1 else "single GPU",
-                          "l2": "flushed between timed steps (256 MB write)"},
+                          "l2": "flushed between timed steps (256 MB write)",
+                          "launch": "timed steps replay one CUDA graph of the step; e2e launches eagerly"},
                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roofline,
                "cpu_baseline": cpu, "detail": detail}
         print(json.dumps(out), flush=True)

@@ -49,7 +49,8 @@ typedef enum { VNM_F32 = 0, VNM_BF16 = 1 } vnm_dtype;
 /* Padded geometry.  N (=2) is implicit ("N≡2").
  *   rows_p = ceil(rows/V)*V      cols_p = ceil(cols/M)*M      nb = cols_p/M (column blocks per row)
  *   nb_pad = ceil(nb/8)*8        (one u32 of metadata = 8 blocks = one 32-wide sparse MMA K step)
- *   ld_val = 2*nb_pad (bf16)     ld_meta = nb_pad/8 (u32)     ld_mask = ceil(cols_p/32) (u32)     */
+ *   ld_val = 2*nb_pad (bf16)     ld_meta = ceil(nb_pad/8 / 4)*4 (u32, rows of 16 B multiples)
+ *   ld_mask = ceil(cols_p/32) (u32)                                                                  */
 typedef struct {
     int32_t rows, cols, V, M;
     int32_t rows_p, cols_p, nb, nb_pad;
@@ -60,7 +61,8 @@ typedef struct {
  *   values  (A_n)  bf16 [rows_p][ld_val]       the 2 kept values of each block of each row, left to right
  *   col_idx (A_i1) u8   [rows_p/V][nb_pad][4]  the block's 4 column indices (0..M-1), strictly ascending
  *   meta    (A_i2) u32  [rows_p][ld_meta]      nibble (b%8) of word b/8 = pos_lo | pos_hi<<2, pos in 0..3
- *                                              indexes col_idx, pos_lo < pos_hi
+ *                                              indexes col_idx, pos_lo < pos_hi; words nb_pad/8 ..
+ *                                              ld_meta-1 of a row hold 0x44444444 (reading Q20)
  * A_i1 lists the columns that carry the block's nonzeros; when fewer than 4 do (always possible,
  * e.g. V = 1) it is completed with the lowest-index remaining columns (reading Q19), so the
  * packed form is a function of the mask alone.                                                        */

@@ -64,7 +64,7 @@ int vnmo_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnmo_geom* g
     g->nb = g->cols_p / M;
     g->nb_pad = ceil_to(g->nb, 8);
     g->ld_val = 2 * g->nb_pad;
-    g->ld_meta = g->nb_pad / 8;
+    g->ld_meta = ceil_to(g->nb_pad / 8, 4);  /* DESIGN.md reading Q20: rows padded to 16 B */
     g->ld_mask = (g->cols_p + 31) / 32;
     return VNMO_OK;
 }
@@ -235,6 +235,9 @@ int vnmo_pack(const uint16_t* W, int64_t ldw, const uint32_t* mask,
             }
         }
     }
+    /* words past the nb_pad/8 block words of a row (Q20): eight pad blocks, nibble 0x4 each */
+    for (int32_t r = 0; r < g.rows_p; ++r)
+        for (int32_t w = g.nb_pad / 8; w < g.ld_meta; ++w) meta[(int64_t)r * g.ld_meta + w] = 0x44444444u;
     if (first_bad >= 0) return (int)(1 + first_bad);
     /* bits beyond cols_p (checked after the blocks: the status is the lowest error index) */
     for (int32_t r = 0; r < g.rows_p; ++r)

@@ -17,7 +17,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
          "-Xptxas", "-warn-spills"]
 
 LIBS = {
-    "libvnm.so": ["api.cpp", "prune.cu", "spmm.cu", "pack_tc.cu", "spmm_tc.cu"],
+    "libvnm.so": ["api.cpp", "prune.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu", "spmm_tc.cu"],
     "libvnm_probe.so": ["probes.cu", "probes2.cu"],
 }
 

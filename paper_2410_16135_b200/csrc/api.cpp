@@ -84,7 +84,7 @@ vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_ge
     g.nb = g.cols_p / M;
     g.nb_pad = ceil_to(g.nb, 8);
     g.ld_val = 2 * g.nb_pad;
-    g.ld_meta = g.nb_pad / 8;
+    g.ld_meta = (g.nb_pad / 8 + 3) / 4 * 4;  // rows padded to 16 B (TMA-loadable), pad words 0x44444444
     g.ld_mask = (g.cols_p + 31) / 32;
     *out = g;
     return VNM_OK;
@@ -196,12 +196,13 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     const bool tc = P->values_tc && P->meta_tc && g->M <= 8 && g->nb_pad > 0 && T > kTcMinTokens;
     if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
     if (tc) return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
+    if (vnm::spmm_pair_applies(*g, T)) return from_launch(vnm::launch_spmm_pair(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T) {
     if (check_geom(g) != VNM_OK || T < 0) return 0;
-    return vnm::spmm_workspace_bytes(*g, T);
+    return vnm::spmm_pair_applies(*g, T) ? vnm::spmm_pair_workspace_bytes(*g, T) : vnm::spmm_workspace_bytes(*g, T);
 }
 
 const char* vnm_status_string(vnm_status s) {

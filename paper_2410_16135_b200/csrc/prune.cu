@@ -332,6 +332,11 @@ __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a)
             for (int q = 0; q < 8; ++q) word |= static_cast<uint32_t>(sNib[r * CB + 8 * w + q]) << (4 * q);
             a.meta[static_cast<int64_t>(r0 + r) * a.ld_meta + b0 / 8 + w] = word;
         }
+        if (b0 + cbv == a.nb_pad) {  // last column tile: the row's pad words past nb_pad / 8 (8 pad blocks each)
+            const int pw0 = a.nb_pad / 8, npw = a.ld_meta - pw0;
+            for (int i = threadIdx.x; i < rows_here * npw; i += kThreads)
+                a.meta[static_cast<int64_t>(r0 + i / npw) * a.ld_meta + pw0 + i % npw] = 0x44444444u;
+        }
         // col_idx: [vb][b][4]
         const int nvb_here = rows_here / V;
         for (int i = threadIdx.x; i < nvb_here * cbv; i += kThreads) {

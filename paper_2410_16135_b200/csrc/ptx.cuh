@@ -56,6 +56,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int32_t
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+// 1-D bulk copy global -> shared (size and both addresses multiples of 16 B), completes on `bar` (tx bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
@@ -129,10 +136,47 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint6
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// shared [128 rows][16 B] (descriptor: no swizzle, SBO 128 B) -> TMEM lanes 0..127, 4 consecutive columns
+// (measured identity placement, csrc/probes2.cu); ordered with later tcgen05.mma of the same thread
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t d) {
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
 // arrive on an mbarrier when all previously issued tcgen05 ops of this thread have completed
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+
+// the 4 sparse MMAs of one stage (K-groups of 8 blocks: A +32 B, B +4096 B, metadata column pair
+// e, e+2 with id2 = k & 1), issued by one elected lane of a converged warp
+__device__ __forceinline__ void mma_sp_x4(uint32_t d, uint64_t ad, uint64_t bd, uint32_t e, uint32_t idesc0,
+                                              uint32_t idesc1, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b32 e2;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "setp.ne.b32 acc, %6, 0;\n\t"
+        "setp.eq.b32 one, 0, 0;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 256;\n\tadd.s64 b2, %2, 512;\n\tadd.s64 b3, %2, 768;\n\t"
+        "add.u32 e2, %3, 2;\n\t"
+        "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, acc;\n\t"
+        "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a1, b1, [%3], %5, one;\n\t"
+        "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a2, b2, [e2], %4, one;\n\t"
+        "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a3, b3, [e2], %5, one;\n\t"
+        "}" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(p));
+    return p != 0;
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
 }
 
 // ---------------------------------------------------------------- descriptors

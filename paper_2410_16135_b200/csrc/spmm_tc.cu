@@ -47,15 +47,6 @@ struct TcArgs {
     uint32_t b_stage_bytes, stage_bytes;
 };
 
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t d) {
-    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
-}
 
 // 16 consecutive outputs of one Y^T row (fp32 or bf16 RNE), masked at T
 __device__ __forceinline__ void store_row16(const TcArgs& a, int row, int tcol, const uint32_t (&v)[16]) {

@@ -46,5 +46,9 @@ int launch_spmm(const SpmmLaunch& L, cudaStream_t stream);
 int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream);  // window form (values_tc / meta_tc)
 int launch_pack_tc(const vnm_packed& P, cudaStream_t stream);
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
+// small-T plan (spmm_pair.cu): T <= 32, V = 64, M <= 8
+bool spmm_pair_applies(const vnm_geom& g, int32_t T);
+size_t spmm_pair_workspace_bytes(const vnm_geom& g, int32_t T);
+int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t stream);
 
 }  // namespace vnm

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
 C3="python bench.py --workload llama_decode --steps 2 --warmup 3 --no-baselines --no-cpu-baseline"
-timeout 300 $C3 > gpurun_out/p_plain3.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"vnm_spmm_kernel" -s 10 -c 1 -o gpurun_out/prof_dec_up2 $C3 > gpurun_out/p_ncu3.log 2>&1; echo "ncu3 $?"
+timeout 300 $C3 > gpurun_out/p_plain3.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"vnm_spmm_kernel" -s 10 -c 1 -o gpurun_out/prof_dec_up3 $C3 > gpurun_out/p_ncu3.log 2>&1; echo "ncu3 $?"

@@ -143,6 +143,31 @@ def test_llama_decode_full(T):
     assert_within(gpu_y(W, XT, 64, 5, T), Yref, Aref)
 
 
+@pytest.mark.parametrize("rows,cols,T,M", [(70, 23, 3, 5), (200, 333, 17, 7), (128, 1000, 32, 8), (64, 4, 1, 4),
+                                           (130, 2048, 24, 6), (4096, 11008, 9, 5), (11008, 4096, 31, 4)])
+def test_slab_plan(rows, cols, T, M):
+    """The small-T plan (T <= 32, M <= 8): dense X^T slab per stage by TMA, gather in shared memory;
+    ragged rows / channels / tokens, split-K on the Llama shapes, every output compared."""
+    W, XT, Wm = make(rows, cols, 64, M, T, seed=rows + cols + T)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, 64, M, T), Yref, Aref)
+    assert_within(gpu_y(W, XT, 64, M, T, out_dtype=torch.bfloat16), Yref, Aref, bf16=True)
+
+
+@pytest.mark.parametrize("T,ld", [(17, 32), (5, 16), (32, 40)])
+def test_slab_plan_strided_x(T, ld):
+    """X^T with a leading dimension past T rounded to 8: the slab comes from a 2-D TMA instead of one bulk copy."""
+    rows, cols, M = 192, 700, 6
+    W, XT, Wm = make(rows, cols, 64, M, T, seed=T + ld)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    P = vnm.prune_compress(to_dev_bf16(W), 64, M)
+    Xd = to_dev_bf16(XT, ld=ld)
+    assert Xd.stride(0) == ld
+    Y = vnm.spmm(Xd, P, T=T)
+    torch.cuda.synchronize()
+    assert_within(Y.cpu().numpy().astype(np.float64), Yref, Aref)
+
+
 @pytest.mark.parametrize("tc", [False, True])
 @pytest.mark.parametrize("rows,cols,M", [(1152, 384, 5), (384, 1536, 5), (3072, 768, 8), (768, 3072, 8)])
 def test_deit_sampled(rows, cols, M, tc):
