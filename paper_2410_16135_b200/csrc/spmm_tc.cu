@@ -16,7 +16,8 @@
 //   warp 0     TMA: A (values_tc 128 x 64 bf16) and the metadata chunk (2 KB bulk copy) of each row tile,
 //              and the dense X^T tile (NT/64 boxes of 64 tokens x rows);
 //   warp 1     MMA: tcgen05.cp (metadata smem -> TMEM) then 4 x RT tcgen05.mma.sp M=128 N=NT;
-//   warps 4-7  epilogue: TMEM -> fp32 / bf16 -> Y^T (accumulators double-buffered when TMEM allows).
+//   warps 4-7  epilogue: TMEM -> fp32 / bf16 -> shared staging -> TMA tensor store of Y^T (accumulators
+//              double-buffered when TMEM allows).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
+#include "tmap.h"
 #include "vnm_internal.h"
 
 namespace vnm {
@@ -33,6 +35,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr uint32_t kABytes = 128 * 128;  // 128 rows x 64 bf16
 constexpr uint32_t kEBytes = 128 * 16;   // 128 lanes x 4 words
+constexpr uint32_t kYBytes = 32 * 128;   // epilogue staging per warp: 32 rows x 128 B (SW128), one TMA store
 
 struct TcArgs {
     const uint32_t* meta_tc;
@@ -48,52 +51,21 @@ struct TcArgs {
 };
 
 
-// 16 consecutive outputs of one Y^T row (fp32 or bf16 RNE), masked at T
-__device__ __forceinline__ void store_row16(const TcArgs& a, int row, int tcol, const uint32_t (&v)[16]) {
-    if (!a.y_bf16) {
-        float* y = reinterpret_cast<float*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
-        if (tcol + 16 <= a.T) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                reinterpret_cast<uint4*>(y)[k] = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (tcol + k < a.T) y[k] = __uint_as_float(v[k]);
-        }
-    } else {
-        uint16_t* y = reinterpret_cast<uint16_t*>(a.YT) + static_cast<int64_t>(row) * a.ldy + tcol;
-        uint32_t pk[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-            pk[k] = *reinterpret_cast<uint32_t*>(&h);
-        }
-        if (tcol + 16 <= a.T) {
-            reinterpret_cast<uint4*>(y)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            reinterpret_cast<uint4*>(y)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (tcol + k < a.T) y[k] = static_cast<uint16_t>((pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
-        }
-    }
-}
-
 // NT tokens per tile (NT/64 TMA chunks); RT row tiles of 128 rows per CTA share every B tile; NACC
 // accumulator sets (double buffering when they fit in TMEM next to the metadata slots).
 template <int NT, int RT>
 __global__ void __launch_bounds__(kThreads, 1)
     vnm_spmm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                       const TcArgs a) {
+                       const __grid_constant__ CUtensorMap tmap_y, const TcArgs a) {
     constexpr int kChunks = NT / 64;
     constexpr int NACC = 2 * RT * NT + 16 * RT <= 512 ? 2 : 1;
     constexpr uint32_t kMetaCol = NACC * RT * NT;  // TMEM: accumulators, then 4 metadata columns per stage & tile
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = a.stages;
-    // per stage: [A x RT][B chunks][E x RT]
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * a.stage_bytes);
+    // per stage: [A x RT][B chunks][E x RT]; then 4 epilogue staging buffers, then the barriers
+    uint8_t* sY = smem + S * a.stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sY + 4 * kYBytes);
     uint64_t* empty = full + S;
     uint64_t* tmem_full = empty + S;
     uint64_t* tmem_empty = tmem_full + 2;
@@ -116,6 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmap_a);
         tma_prefetch_desc(&tmap_b);
+        tma_prefetch_desc(&tmap_y);
     }
     tc_fence_before();
     __syncthreads();
@@ -190,7 +163,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
+        // TMEM -> registers -> bf16 / fp32 -> the warp's 32 x 128 B staging buffer (SW128: 16-byte chunk c of
+        // row r at c ^ (r % 8), conflict-free) -> one TMA tensor store per chunk of 128 B per row; the store
+        // clips rows >= rows and tokens >= T.
         const int qd = warp - 4;
+        uint8_t* buf = sY + qd * kYBytes;
+        const uint32_t buf_row = smem_u32(buf) + lane * 128;
+        const int cw = a.y_bf16 ? 64 : 32;  // tokens per 128-byte chunk
         int tl = 0;
         for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++tl) {
             const int rg = a.row_major ? w / a.n_tt : w % a.n_rg, tt = a.row_major ? w % a.n_tt : w / a.n_rg;
@@ -201,64 +180,63 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int j = 0; j < RT; ++j) {
                 const int rt = rg * RT + j;
-                const int row = rt * 128 + 32 * qd + lane;
-                const bool row_ok = rt < a.n_rt && row < a.rows;
+                if (rt >= a.n_rt) break;
 #pragma unroll 1
-                for (int c = 0; c < NT; c += 16) {
-                    uint32_t v[16];
-                    tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + (acc * RT + j) * NT + c, v);
-                    tmem_wait_ld();
-                    const int tcol = n0 + c;
-                    if (row_ok && tcol < a.T) store_row16(a, row, tcol, v);
+                for (int c = 0; c < NT && n0 + c < a.T; c += cw) {
+                    uint32_t pk[32];
+                    if (a.y_bf16) {
+#pragma unroll
+                        for (int hh = 0; hh < 4; ++hh) {
+                            uint32_t v[16];
+                            tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + (acc * RT + j) * NT + c + 16 * hh, v);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                __nv_bfloat162 b2 =
+                                    __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                                pk[8 * hh + k] = *reinterpret_cast<uint32_t*>(&b2);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            uint32_t v[16];
+                            tmem_ld_32x32b_x16(tmem + ((32 * qd) << 16) + (acc * RT + j) * NT + c + 16 * hh, v);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) pk[16 * hh + k] = v[k];
+                        }
+                    }
+                    if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         buf_row + (((k ^ lane) & 7) << 4)),
+                                     "r"(pk[4 * k]), "r"(pk[4 * k + 1]), "r"(pk[4 * k + 2]), "r"(pk[4 * k + 3])
+                                     : "memory");
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmap_y, n0 + c, rt * 128 + 32 * qd, buf);
+                        bulk_commit();
+                    }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tmem_empty[acc]);
         }
+        if (lane == 0) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encoder() {
-    static EncodeTiledFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return static_cast<EncodeTiledFn>(nullptr);
-        return reinterpret_cast<EncodeTiledFn>(p);
-    }();
-    return fn;
-}
-
 bool encode(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t bi,
             uint32_t bo) {
-    EncodeTiledFn enc = encoder();
-    if (!enc) return false;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {row_bytes};
-    cuuint32_t box[2] = {bi, bo};
-    cuuint32_t es[2] = {1, 1};
-    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int sm_count() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
+    return encode_2d(tm, base, inner, outer, row_bytes, bi, bo);
 }
 
 template <int NT, int RT>
@@ -272,7 +250,7 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
     a.b_stage_bytes = static_cast<uint32_t>(kChunks * a.rb * 128);
     a.stage_bytes = RT * (kABytes + kEBytes) + a.b_stage_bytes;
     a.stage_bytes = (a.stage_bytes + 1023) / 1024 * 1024;
-    a.stages = static_cast<int>((224u * 1024u) / a.stage_bytes);
+    a.stages = static_cast<int>((224u * 1024u - 4 * kYBytes) / a.stage_bytes);
     if (a.stages > 4) a.stages = 4;
     if (a.stages < 2) return kLaunchUnsupported;
     a.n_rg = (a.n_rt + RT - 1) / RT;
@@ -286,12 +264,19 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
     if (!encode(&tb, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
                 64, static_cast<uint32_t>(a.rb)))
         return kLaunchCudaError;
-    const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + 1024 + 256;
+    // Y^T [rows][ldy]: box 128 B of tokens x 32 rows, 128B swizzle (the epilogue staging layout)
+    CUtensorMap ty;
+    const bool bf = L.y_dtype == VNM_BF16;
+    if (!encode_2d(&ty, L.YT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.rows),
+                   static_cast<uint64_t>(L.ldy) * (bf ? 2 : 4), bf ? 64 : 32, 32,
+                   bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32))
+        return kLaunchCudaError;
+    const size_t smem = static_cast<size_t>(a.stages) * a.stage_bytes + 4 * kYBytes + 1024 + 256;
     auto k = vnm_spmm_tc_kernel<NT, RT>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
-    const int grid = a.work < sm_count() ? a.work : sm_count();
-    k<<<grid, kThreads, smem, stream>>>(ta, tb, a);
+    const int grid = a.work < num_sms() ? a.work : num_sms();
+    k<<<grid, kThreads, smem, stream>>>(ta, tb, ty, a);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
