@@ -76,7 +76,8 @@ typedef struct {
      * 8-row window of X^T (the block's M channels followed by 8-M channels of the next block) holding two
      * 2:4 groups (channels 0-3 and 4-7); the row's two nonzeros sit in their own channels, the other
      * positions carry zero values.  This lets M = 128 sparse MMAs share one dense, TMA-loaded X^T tile
-     * instead of gathering per V-block.  Layouts (rows_w = ceil(rows_p/128)*128, bpm = M == 4 ? 8 : 4
+     * instead of gathering per V-block.  Any 32 <= V <= 128: each row's metadata selects within the window, so rows
+ * of different V-blocks share the tile.  Layouts (rows_w = ceil(rows_p/128)*128, bpm = M == 4 ? 8 : 4
      * blocks per MMA, n_mma_w = nb_pad/bpm, n_stage_w = ceil(n_mma_w/4)):
      *   values_tc bf16 [rows_w][16*n_mma_w]       4 values per block (M >= 5: lo pair, hi pair); = A_n for M = 4
      *   meta_tc   u32  [rows_w/128][n_stage_w][128][4]   2:4 metadata of MMA (stage*4 + k) in the M = 128
@@ -90,7 +91,7 @@ typedef struct {
 vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_geom* out);
 
 /* Bytes of one buffer for geometry g: which = 0 values, 1 col_idx, 2 meta, 3 mask, 4 values_tc, 5 meta_tc
- * (4 and 5 are 0 when the tensor-core form does not apply: V != 64 or M > 8).  0 on bad input.         */
+ * (4 and 5 are 0 when the tensor-core form does not apply: V < 32, V > 128 or M > 8).  0 on bad input.          */
 size_t vnm_bytes(const vnm_geom* g, int which);
 
 /* S_{V:N:M} (§3) -> mask bits.
@@ -112,13 +113,13 @@ vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, co
                         vnm_packed* out, int32_t* d_status, vnm_stream_t stream);
 
 /* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.
- * If out->values_tc / out->meta_tc are set (V = 64, M <= 8) the window form is written in the same pass
+ * If out->values_tc / out->meta_tc are set (32 <= V <= 128, M <= 8) the window form is written in the same pass
  * (identical to vnm_pack_tc of the result).                                                             */
 vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
                               const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
 
 /* Fill P->values_tc / P->meta_tc (caller-allocated, vnm_bytes 4 / 5) from the canonical A_n / A_i1 / A_i2
- * of P.  VNM_ERR_UNSUPPORTED unless V == 64 and 4 <= M <= 8; VNM_ERR_ARG if a tc pointer is NULL.       */
+ * of P.  VNM_ERR_UNSUPPORTED unless 32 <= V <= 128 and 4 <= M <= 8; VNM_ERR_ARG if a tc pointer is NULL.       */
 vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
 
 /* The V:N:M SpMM (App. A):  Y^T[o][t] = sum_k W'[o][k] * X^T[k][t],  W' = unpack(P).
@@ -127,10 +128,12 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
  *   YT  [P->g.rows][ldy]  fp32 (y_dtype VNM_F32) or bf16 (VNM_BF16, round-to-nearest-even), 16-B aligned,
  *       ldy % 8 == 0, ldy >= T; only rows < g.rows and columns < T are written.
  * bf16 x bf16 products, fp32 accumulation on the sparse tensor cores (tcgen05.mma.sp).
- * Supported: V == 64 (VNM_ERR_UNSUPPORTED otherwise; V = 128 is the next step).
- * Plans: T > 64 with P->values_tc / meta_tc set (4 <= M <= 8) -> window-form kernel (dense X^T tiles by
- * TMA, multicast across a CTA cluster, M = 128 sparse MMAs); otherwise the gather kernel (M = 64 sparse
- * MMAs on the 4 kept X^T rows of each block, 16-byte cp.async gathers).
+ * Supported: V == 64 (any M), and any 32 <= V <= 128 (e.g. the paper's 128:2:M) when the
+ * window form is present (4 <= M <= 8); VNM_ERR_UNSUPPORTED otherwise.
+ * Plans: window form present and T > 64 (or V != 64) -> window-form kernel on CTA pairs (dense X^T tiles by
+ * TMA, tcgen05.mma.sp.cta_group::2 with M = 256); V = 64, T <= 32, M <= 8 -> small-T kernel (two V-blocks per
+ * M = 128 sparse MMA, split-K); otherwise the gather kernel (M = 64 sparse MMAs on the 4 kept X^T rows of each
+ * block, 16-byte cp.async gathers).
  * workspace: optional device scratch (16-B aligned) used by the small-T split-K plan; pass NULL/0 to
  * let the library choose a plan without it (vnm_spmm_workspace_bytes gives the size it can use).     */
 vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,

@@ -1,6 +1,6 @@
 """Build the in-tree CUDA libraries with nvcc for sm_100a (no JIT, no torch extension machinery).
 
-  libvnm.so        the product: C ABI of include/vnm.h (api.cpp + prune.cu + spmm.cu)
+  libvnm.so        the product: C ABI of include/vnm.h (api.cpp + the kernels)
   libvnm_probe.so  test-only hardware probes / microbenchmarks (probes.cu)
 """
 from __future__ import annotations
@@ -17,8 +17,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
          "-Xptxas", "-warn-spills"]
 
 LIBS = {
-    "libvnm.so": ["api.cpp", "prune.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu", "spmm_tc.cu"],
-    "libvnm_probe.so": ["probes.cu", "probes2.cu"],
+    "libvnm.so": ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu", "spmm_tc.cu", "spmm_tc2.cu"],
+    "libvnm_probe.so": ["probes.cu", "probes2.cu", "probes3.cu"],
 }
 
 
@@ -32,13 +32,31 @@ def _stale(out: str, srcs: list[str]) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> None:
+    """Each source is compiled to an object in build/ (in parallel, only when stale), then linked."""
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
     for lib, files in LIBS.items():
         srcs = [os.path.join(CSRC, f) for f in files]
         out = os.path.join(HERE, lib)
         if not force and not _stale(out, srcs):
             continue
+        objs = [os.path.join(objdir, f + ".o") for f in files]
+
+        def compile_one(i):
+            if not force and not _stale(objs[i], [srcs[i]]):
+                return
+            tmp = objs[i] + f".tmp{os.getpid()}"
+            cmd = [NVCC, *ARCH, *FLAGS, "-c", "-o", tmp, srcs[i]]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.check_call(cmd)
+            os.replace(tmp, objs[i])
+
+        with ThreadPoolExecutor(max_workers=min(8, len(files))) as ex:
+            list(ex.map(compile_one, range(len(files))))
         tmp = out + f".tmp{os.getpid()}"
-        cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", tmp, *srcs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

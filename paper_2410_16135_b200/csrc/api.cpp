@@ -3,6 +3,7 @@
 // device memory.
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "vnm_internal.h"
@@ -100,7 +101,7 @@ size_t vnm_bytes(const vnm_geom* g, int which) {
         case 3: return rp * static_cast<size_t>(g->ld_mask) * 4;
         case 4:
         case 5: {
-            if (g->V != 64 || g->M > 8) return 0;
+            if (g->V < 32 || g->V > 128 || g->M > 8) return 0;
             const size_t rows_w = (rp + 127) / 128 * 128;
             const size_t bpm = g->M == 4 ? 8 : 4;
             const size_t n_mma = static_cast<size_t>(g->nb_pad) / bpm;
@@ -154,8 +155,8 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
     if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
     if (!W) return VNM_ERR_ARG;
     vnm::PruneLaunch L{g, W, ldw, score, lds, nullptr, mask, out->values, out->col_idx, out->meta, nullptr};
-    if (out->values_tc || out->meta_tc) {  // fused window form (include/vnm.h), V = 64 and M <= 8 only
-        if (g->V != 64 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (out->values_tc || out->meta_tc) {  // fused window form (include/vnm.h), V >= 32 and M <= 8 only
+        if (g->V < 32 || g->V > 128 || g->M > 8) return VNM_ERR_UNSUPPORTED;
         if (!out->values_tc || !out->meta_tc) return VNM_ERR_ARG;
         if (!aligned16(out->values_tc) || !aligned16(out->meta_tc)) return VNM_ERR_ALIGN;
         L.values_tc = out->values_tc;
@@ -170,7 +171,7 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream) {
     vnm_status s = check_geom(g);
     if (s) return s;
     if ((s = check_packed(P, g))) return s;
-    if (g->V != 64 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (g->V < 32 || g->V > 128 || g->M > 8) return VNM_ERR_UNSUPPORTED;
     if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
     if (!P->values_tc || !P->meta_tc) return VNM_ERR_ARG;
     if (!aligned16(P->values_tc) || !aligned16(P->meta_tc)) return VNM_ERR_ALIGN;
@@ -186,16 +187,23 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     if ((s = check_packed(P, g))) return s;
     if (y_dtype != VNM_F32 && y_dtype != VNM_BF16) return VNM_ERR_ARG;
     if (T < 0 || ldx < T || ldy < T) return VNM_ERR_SHAPE;
-    if (g->V != 64) return VNM_ERR_UNSUPPORTED;
+    // window form: 32 <= V <= 128 with M <= 8 (rows are independent in it); gather / small-T plans: V = 64
+    const bool tc_form = P->values_tc && P->meta_tc && g->V >= 32 && g->V <= 128 && g->M <= 8;
+    if (g->V != 64 && !tc_form) return VNM_ERR_UNSUPPORTED;
     if (T == 0 || g->rows == 0) return VNM_OK;
     if (!YT) return VNM_ERR_ARG;
     if (g->cols > 0 && !XT) return VNM_ERR_ARG;
     if ((XT && !aligned16(XT)) || !aligned16(YT) || (ldx % 8) != 0 || (ldy % 8) != 0) return VNM_ERR_ALIGN;
     if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
     vnm::SpmmLaunch L{P, XT, ldx, T, YT, ldy, y_dtype, workspace, workspace ? workspace_bytes : 0};
-    const bool tc = P->values_tc && P->meta_tc && g->M <= 8 && g->nb_pad > 0 && T > kTcMinTokens;
+    const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || g->V != 64);
     if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
-    if (tc) return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
+    if (tc) {
+        // CTA-pair kernel by default; VNM_TC_PLAN=1 selects the single-CTA window kernel (comparisons)
+        static const bool single = [] { const char* e = getenv("VNM_TC_PLAN"); return e && e[0] == '1'; }();
+        if (!single) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
+        return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
+    }
     if (vnm::spmm_pair_applies(*g, T)) return from_launch(vnm::launch_spmm_pair(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }

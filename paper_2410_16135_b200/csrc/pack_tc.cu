@@ -1,7 +1,7 @@
 // pack_tc.cu — canonical A_n / A_i1 / A_i2 (App. A) -> the tensor-core "window" form used by
 // spmm_tc.cu (include/vnm.h).  Pure data movement + integer logic, HBM-bound.
 //
-// Window form, V = 64, 4 <= M <= 8: block b of a row becomes the 8 consecutive X^T channels
+// Window form, V >= 32, 4 <= M <= 8: block b of a row becomes the 8 consecutive X^T channels
 // [b*M, b*M + 8) split into two 2:4 groups (channels 0-3 "lo", 4-7 "hi").  The row's two kept values
 // (block columns c0 < c1) sit at their own positions; each group is completed to exactly two entries with
 // zero values at the lowest free positions.  For M = 4 two blocks form one 8-channel window and the form is
@@ -21,7 +21,7 @@ struct PackTcArgs {
     const uint32_t* meta;
     uint16_t* values_tc;
     uint32_t* meta_tc;
-    int32_t M, rows_p, rows_w, nb_pad, ld_val, ld_meta, n_mma, n_stage, ld_tc;
+    int32_t V, M, rows_p, rows_w, nb_pad, ld_val, ld_meta, n_mma, n_stage, ld_tc;
 };
 
 // the 8-nibble metadata word of MMA `mi` for row r (rows >= rows_p: zero weights, nibble 0x4)
@@ -29,7 +29,7 @@ __device__ uint32_t mma_word(const PackTcArgs& a, int r, int mi) {
     if (r >= a.rows_p || mi >= a.n_mma) return 0x44444444u;
     if (a.M == 4) return a.meta[static_cast<int64_t>(r) * a.ld_meta + mi];
     uint32_t w = 0;
-    const uint8_t* ci_row = a.col_idx + static_cast<int64_t>(r / 64) * a.nb_pad * 4;
+    const uint8_t* ci_row = a.col_idx + static_cast<int64_t>(r / a.V) * a.nb_pad * 4;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int b = 4 * mi + i;
@@ -56,7 +56,7 @@ __global__ void pack_tc_values_kernel(const PackTcArgs a) {
     uint16_t out[4] = {0, 0, 0, 0};
     if (r < a.rows_p) {
         const uint32_t nib = (a.meta[static_cast<int64_t>(r) * a.ld_meta + b / 8] >> (4 * (b % 8))) & 0xFu;
-        const uint8_t* ci = a.col_idx + (static_cast<int64_t>(r / 64) * a.nb_pad + b) * 4;
+        const uint8_t* ci = a.col_idx + (static_cast<int64_t>(r / a.V) * a.nb_pad + b) * 4;
         const int c0 = ci[nib & 3u], c1 = ci[nib >> 2];
         const uint16_t v0 = a.values[static_cast<int64_t>(r) * a.ld_val + 2 * b];
         const uint16_t v1 = a.values[static_cast<int64_t>(r) * a.ld_val + 2 * b + 1];
@@ -98,6 +98,7 @@ int launch_pack_tc(const vnm_packed& P, cudaStream_t stream) {
     a.meta = P.meta;
     a.values_tc = P.values_tc;
     a.meta_tc = P.meta_tc;
+    a.V = g.V;
     a.M = g.M;
     a.rows_p = g.rows_p;
     a.rows_w = (g.rows_p + 127) / 128 * 128;

@@ -1,0 +1,99 @@
+// probes3.cu — test-only microbenchmark (round 1b): back-to-back tcgen05.mma(.sp) on CTA PAIRS
+// (cta_group::2, M = 256) from resident shared memory, optionally with a concurrent TMA stream into the
+// same shared memory (the window SpMM's load traffic), to find the MMA ceiling of spmm_tc2.cu.
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "tmap.h"
+
+namespace vnm {
+namespace {
+
+// smem: A 16 KB | B 4 chunks x 4 KB x ... (48 KB window region) | TMA sink 96 KB
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    bench_mma_pair_kernel(const __grid_constant__ CUtensorMap tm, uint32_t n_mma, uint32_t sparse, uint32_t sbo,
+                          uint32_t iters, uint32_t tma_kb_per_mma, unsigned long long* cycles) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t bar, tbar[2];
+    __shared__ uint32_t tmem_base;
+    const uint32_t tid = threadIdx.x, warp = tid / 32;
+    const uint32_t rank = cluster_ctarank();
+    for (uint32_t i = tid; i < 65536 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    fence_proxy_async_smem();
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_init(&tbar[0], 1);
+        mbar_init(&tbar[1], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_pair(&tmem_base, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tbase = tmem_base;
+    tmem_st_32x32b_x4(tbase + ((warp * 32) << 16) + 256, 0x44444444u, 0x44444444u, 0x44444444u, 0x44444444u);
+    tmem_wait_st();
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    if (tid == 0 && rank == 0) {
+        const uint64_t ad = sdesc(smem_u32(smem), 16, 1024, kLayoutSW128);
+        const uint64_t bd = sdesc(smem_u32(smem + 16384), 8192, sbo, kLayoutSW128);
+        const uint32_t idesc = idesc_bf16(256, n_mma, sparse != 0, 0, true);
+        unsigned long long t0 = clock64();
+        for (uint32_t i = 0; i < iters; ++i) {
+            if (sparse)
+                mma_sp_bf16_pair(tbase, ad, bd, tbase + 256, idesc, i > 0);
+            else
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tbase),
+                    "l"(ad), "l"(bd), "r"(idesc), "r"(i > 0 ? 1u : 0u)
+                    : "memory");
+        }
+        mma_commit_pair(&bar, 0x3);
+        mbar_wait(&bar, 0);
+        unsigned long long t1 = clock64();
+        cycles[blockIdx.x / 2] = t1 - t0;
+    } else if (tid == 32 && tma_kb_per_mma) {
+        // concurrent TMA stream: tma_kb_per_mma KB per MMA-equivalent, 16 KB boxes (64 x 128 rows) into a
+        // 96 KB sink, two in flight
+        const uint32_t nbox = (iters * tma_kb_per_mma) / 48;  // groups of 3 boxes
+        for (uint32_t i = 0; i < nbox; ++i) {
+            const int s = i & 1;
+            if (i >= 2) mbar_wait(&tbar[s], ((i / 2) - 1) & 1);
+            mbar_arrive_expect_tx(&tbar[s], 16384 * 3);
+            for (int j = 0; j < 3; ++j)
+                tma_load_2d(smem + 65536 + (s * 3 + j) * 16384, &tm, 0, ((blockIdx.x * 7 + i * 3 + j) * 128) % 8192, &tbar[s]);
+        }
+        if (nbox >= 1) mbar_wait(&tbar[(nbox - 1) & 1], ((nbox - 1) / 2) & 1);
+        if (nbox >= 2) mbar_wait(&tbar[(nbox - 2) & 1], ((nbox - 2) / 2) & 1);
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_pair(tbase, 512);
+    }
+}
+
+}  // namespace
+}  // namespace vnm
+
+// X: bf16 [8192][64] (1 MB, L2-resident) feeds the concurrent TMA stream.  cycles: one per pair.
+extern "C" int vnm_probe_bench_mma_pair(const uint16_t* X, uint32_t n_mma, uint32_t sparse, uint32_t sbo,
+                                        uint32_t iters, uint32_t tma_kb_per_mma, int pairs, unsigned long long* cycles) {
+    using namespace vnm;
+    CUtensorMap tm;
+    if (!encode_2d(&tm, X, 64, 8192, 128, 64, 128)) return 2;
+    const size_t smem = 65536 + 96 * 1024 + 1024;
+    if (cudaFuncSetAttribute(bench_mma_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return 3;
+    bench_mma_pair_kernel<<<2 * pairs, 128, smem>>>(tm, n_mma, sparse, sbo, iters, tma_kb_per_mma, cycles);
+    if (cudaGetLastError() != cudaSuccess) return 4;
+    return cudaDeviceSynchronize() == cudaSuccess ? 0 : 5;
+}

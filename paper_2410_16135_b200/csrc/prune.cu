@@ -18,6 +18,7 @@
 // The pass is HBM-bound: algorithmic bytes per weight element = 2 (W) [+4 score] + (4 + 0.5)/M
 // (values + meta) + 4/(V M) (col_idx) + 1/8 (mask).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
@@ -469,6 +470,12 @@ cudaError_t launch_v(int V, const PruneArgs& a, size_t smem, cudaStream_t st) {
 // Host entry used by api.cpp.  Picks CB so that the tile fits in shared memory.
 int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = *L.g;
+    // V >= 32: the instruction-lean kernel (prune2.cu); VNM_PRUNE_V1=1 keeps this one (comparisons)
+    static const bool v1 = [] { const char* e = getenv("VNM_PRUNE_V1"); return e && e[0] == '1'; }();
+    if (!v1 && !L.mask_in) {
+        const int rc = launch_prune2(L, stream);
+        if (rc != kLaunchUnsupported) return rc;
+    }
     const bool from_mask = L.mask_in != nullptr;
     const bool has_score = L.score != nullptr;
     int CB = 0;

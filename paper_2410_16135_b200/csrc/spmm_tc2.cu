@@ -1,0 +1,400 @@
+// spmm_tc2.cu — the window-form V:N:M SpMM (include/vnm.h values_tc / meta_tc) on CTA
+// PAIRS: tcgen05.mma.sp.cta_group::2 with M = 256, N = 256.
+//
+// Why pairs.  A 1-CTA M = 128, N = 256 sparse MMA reads A (4 KB) and the whole B tile (16 KB) from one SM's
+// shared memory per 128 x 256 x 16 effectual MACs; the measured back-to-back cost (~165 cycles,
+// profiles/r01_probes.md MB2) is the shared-memory read rate (~124 B/clk), so any TMA or epilogue traffic
+// in the same shared memory slows the MMAs down.  In a pair each CTA holds its own 128 rows of A and only
+// HALF of the B tile (128 tokens), and the two SMs' tensor cores execute the M = 256 product together:
+// 12 KB of shared memory per CTA per MMA instead of 20 KB, and every X^T tile is fetched from L2 once per
+// 256 output rows.  Rows are independent in the window form (each row carries its own 2:4 metadata over
+// the block's 8-channel window), so any V works as long as the window form was built for it.
+//
+// Tile = 256 output rows (row tiles 2p, 2p+1; CTA rank r owns 2p+r) x 256 tokens (rank r loads B for
+// tokens 128r..128r+127).  Stage = 4 MMAs (16 blocks; 32 for M = 4).
+//   warp 0       TMA (both CTAs): own A (values_tc 128 x 64), own metadata chunk, own half of the X^T
+//                window rows; completion counted on the leader's full barrier (cta_group::2 TMA);
+//   warp 1       TMEM allocation (both CTAs) and, in the leader only, the MMA thread: tcgen05.cp of both
+//                CTAs' metadata -> their TMEM, 4 x tcgen05.mma.sp.cta_group::2, commits multicast to both;
+//   warps 4-11   epilogue (both CTAs): warp 4 + q + 4h drains TMEM lanes 32q.. x columns 128h.. into
+//                registers, releases the accumulator (leader's tmem_empty, 16 arrivals), then converts and
+//                writes Y^T through swizzled shared staging with TMA tensor stores — so the store of tile i
+//                overlaps the main loop of tile i + 1 although the accumulator is single-buffered
+//                (256 fp32 columns + the metadata ring fill the 512 TMEM columns).
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "tmap.h"
+#include "vnm_internal.h"
+
+namespace vnm {
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kNT = 256;                    // tokens per pair tile
+constexpr int kNH = kNT / 2;                // tokens per CTA of B
+constexpr uint32_t kABytes = 128 * 128;     // 128 rows x 64 bf16 (SW128)
+constexpr uint32_t kEBytes = 128 * 16;      // 128 lanes x 4 words
+constexpr uint32_t kYSlot = 32 * 128;       // one 32 row x 128 B staging slot (SW128)
+constexpr uint32_t kMetaCol = 256;          // TMEM: accumulator columns 0..255, metadata ring from 256
+
+struct Tc2Args {
+    int32_t T, rows, M;
+    int32_t n_mma, n_stage, n_rt, n_rp, n_tt, work;
+    int32_t row_major;   // tile order: pair-row-major (A reused across token tiles) or token-tile-major
+    int32_t rows_stage;  // X^T rows advanced per stage
+    int32_t rb;          // X^T rows loaded per stage (windows of the stage's blocks), multiple of 8
+    int32_t stages;
+    int32_t a_res;       // 1: A (values_tc) and metadata of the pair's rows stay resident in shared memory
+                         //    (short K): the ring carries X^T only; each pair keeps one row pair
+    int32_t y_slots;     // epilogue staging slots per warp (1 or 2)
+    uint32_t b_bytes, stage_bytes, res_bytes;
+    int32_t trace;       // VNM_SPMM_TRACE: per-CTA wait / busy cycle counters into g_tc2_t
+};
+
+// VNM_SPMM_TRACE counters per CTA: MMA wait full, MMA wait tmem_empty, MMA loop total, producer wait empty,
+// epilogue (warp 4) wait tmem_full, drain, store, tiles
+__device__ unsigned long long g_tc2_t[8][160];
+
+// i-th tile (row pair rp, token tile tt) of cluster cid; false past the end
+__device__ __forceinline__ bool tile_of(const Tc2Args& a, int cid, int ncl, int i, int& rp, int& tt) {
+    if (a.a_res) {  // pairs in groups of n_rp (one per row pair); group g walks token tiles g, g + ng, ...
+        const int ng = ncl / a.n_rp, g = cid / a.n_rp;
+        rp = cid % a.n_rp;
+        tt = g + i * ng;
+        return g < ng && tt < a.n_tt;
+    }
+    const int w = cid + i * ncl;
+    if (w >= a.work) return false;
+    rp = a.row_major ? w / a.n_tt : w % a.n_rp;
+    tt = a.row_major ? w % a.n_tt : w / a.n_rp;
+    return true;
+}
+
+// the warp's TMEM reads are complete: one arrival per warp on the leader's tmem_empty
+__device__ __forceinline__ void release(uint64_t* tmem_empty, int lane, bool leader) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        if (leader) mbar_arrive(tmem_empty);
+        else mbar_arrive_cluster(tmem_empty, 0);
+    }
+}
+
+// 32 rows x 128 B (32 words per lane = one row) -> staging slot (c % nslot) of the warp, SW128 (16-byte chunk k
+// of row r at k ^ (r % 8): conflict-free), then one TMA tensor store; the store clips rows / tokens
+__device__ __forceinline__ void stage_store(uint8_t* buf, int nslot, int c, int lane, const uint32_t* w,
+                                            const CUtensorMap* tm, int x, int y) {
+    uint8_t* slot = buf + (nslot == 2 ? (c & 1) * kYSlot : 0);
+    if (lane == 0) {  // the store that last used this slot has read it
+        if (nslot == 2) bulk_wait_read<1>();
+        else bulk_wait_read<0>();
+    }
+    __syncwarp();
+    const uint32_t row = smem_u32(slot) + lane * 128;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((k ^ lane) & 7) << 4)), "r"(w[4 * k]),
+                     "r"(w[4 * k + 1]), "r"(w[4 * k + 2]), "r"(w[4 * k + 3])
+                     : "memory");
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(tm, x, y, slot);
+        bulk_commit();
+    }
+}
+
+template <bool kBf16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    vnm_spmm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                        const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_y,
+                        const Tc2Args a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = a.stages;
+    // [resident A (n_stage x 16 KB) | resident E (n_stage x 2 KB)] (a_res only), ring, Y staging, barriers
+    uint8_t* ring = smem + a.res_bytes;
+    uint8_t* sY = ring + S * a.stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sY + 8 * a.y_slots * kYSlot);
+    uint64_t* empty = full + S;
+    uint64_t* tmem_full = empty + S;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint64_t* res_full = tmem_empty + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 1);
+    const uint32_t b_off = a.a_res ? 0u : kABytes, e_off = kABytes + a.b_bytes;
+    uint8_t* resE = smem + a.n_stage * kABytes;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cid = static_cast<int>(cluster_id_x()), ncl = static_cast<int>(nclusters_x());
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 16);
+        mbar_init(res_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmap_a);
+        tma_prefetch_desc(&tmap_b);
+        tma_prefetch_desc(&tmap_e);
+        tma_prefetch_desc(&tmap_y);
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer (both CTAs)
+        if (lane == 0) {
+            int q = 0, rp, tt;
+            unsigned long long c_emp = 0, c0;
+            for (int i = 0; tile_of(a, cid, ncl, i, rp, tt); ++i) {
+                const int rt = 2 * rp + static_cast<int>(rank);  // row tiles past n_rt read as zeros (TMA OOB)
+                const int rte = rt < a.n_rt ? rt : 0;             // ... with valid metadata
+                const int n0 = tt * kNT + kNH * static_cast<int>(rank);
+                if (a.a_res && i == 0) {  // the pair's A and metadata, once
+                    if (leader) mbar_arrive_expect_tx(res_full, 2 * a.n_stage * (kABytes + kEBytes));
+                    for (int st = 0; st < a.n_stage; ++st) {
+                        tma_load_2d_pair(smem + st * kABytes, &tmap_a, st * 64, rt * 128, res_full);
+                        tma_load_2d_pair(resE + st * kEBytes, &tmap_e, 0, (rte * a.n_stage + st) * 128, res_full);
+                    }
+                }
+                for (int st = 0; st < a.n_stage; ++st, ++q) {
+                    const int s = q % S;
+                    c0 = clock64();
+                    mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
+                    c_emp += clock64() - c0;
+                    uint8_t* base = ring + s * a.stage_bytes;
+                    if (a.a_res) {
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * a.b_bytes);
+                    } else {
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * (kABytes + kEBytes + a.b_bytes));
+                        tma_load_2d_pair(base, &tmap_a, st * 64, rt * 128, &full[s]);
+                        tma_load_2d_pair(base + e_off, &tmap_e, 0, (rte * a.n_stage + st) * 128, &full[s]);
+                    }
+                    tma_load_2d_pair(base + b_off, &tmap_b, n0, st * a.rows_stage, &full[s]);
+                    tma_load_2d_pair(base + b_off + a.rb * 128, &tmap_b, n0 + 64, st * a.rows_stage, &full[s]);
+                }
+            }
+            if (a.trace) g_tc2_t[3][blockIdx.x] = c_emp;
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer (leader CTA)
+        if (leader && lane == 0) {
+            int q = 0, tl = 0, rp, tt;
+            const uint32_t idesc0 = idesc_bf16(256, kNT, true, 0, true);
+            const uint32_t idesc1 = idesc_bf16(256, kNT, true, 1, true);
+            const uint32_t k_bytes = (a.M == 4 ? 32u : 4u * a.M) * 128u;  // B advance per MMA
+            const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;          // K-group (window) stride
+            unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
+            for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
+                if (a.a_res && tl == 0) mbar_wait(res_full, 0);
+                c0 = clock64();
+                mbar_wait(tmem_empty, (tl & 1) ^ 1);
+                c_emp += clock64() - c0;
+                tc_fence_after();
+                for (int st = 0; st < a.n_stage; ++st, ++q) {
+                    const int s = q % S;
+                    c0 = clock64();
+                    mbar_wait(&full[s], (q / S) & 1);
+                    c_full += clock64() - c0;
+                    tc_fence_after();
+                    uint8_t* base = ring + s * a.stage_bytes;
+                    const uint32_t meta_s = tmem + kMetaCol + 4 * s;
+                    const uint32_t e_s = a.a_res ? smem_u32(resE + st * kEBytes) : smem_u32(base + e_off);
+                    tmem_cp_128x128b_pair(meta_s, sdesc(e_s, 16, 128, 0));
+                    const uint32_t b0 = smem_u32(base + b_off);
+                    const uint32_t a0 = a.a_res ? smem_u32(smem + st * kABytes) : smem_u32(base);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int mi = st * 4 + k;
+                        if (mi < a.n_mma) {
+                            const uint64_t bd = sdesc(b0 + k * k_bytes, a.rb * 128, sbo, kLayoutSW128);
+                            const uint64_t ad = sdesc(a0 + 32 * k, 16, 1024, kLayoutSW128);
+                            mma_sp_bf16_pair(tmem, ad, bd, meta_s + (k & ~1), (k & 1) ? idesc1 : idesc0,
+                                             mi > 0 ? 1u : 0u);
+                        }
+                    }
+                    mma_commit_pair(&empty[s], 0x3);
+                }
+                mma_commit_pair(tmem_full, 0x3);
+            }
+            if (a.trace) {
+                g_tc2_t[0][blockIdx.x] = c_full;
+                g_tc2_t[1][blockIdx.x] = c_emp;
+                g_tc2_t[2][blockIdx.x] = clock64() - c_all;
+                g_tc2_t[7][blockIdx.x] = tl;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue (both CTAs)
+        const int ew = warp - 4, qd = ew % 4, hf = ew / 4;
+        uint8_t* buf = sY + ew * a.y_slots * kYSlot;
+        constexpr int kCw = kBf16 ? 64 : 32;             // tokens per 128-byte chunk
+        constexpr int kChunks = kNH / kCw;               // chunks per warp per tile (2 bf16, 4 fp32)
+        int tl = 0, rp, tt;
+        unsigned long long c_wait = 0, c_drain = 0, c_store = 0, c0, c1;
+        for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
+            const int rt = 2 * rp + static_cast<int>(rank);
+            const int t0 = tt * kNT + kNH * hf;  // first token of this warp's columns
+            c0 = clock64();
+            mbar_wait(tmem_full, tl & 1);
+            c1 = clock64();
+            c_wait += c1 - c0;
+            tc_fence_after();
+            const uint32_t taddr = tmem + ((32 * qd) << 16) + kNH * hf;
+            const bool store = rt < a.n_rt && t0 < a.T;
+            if constexpr (kBf16) {
+                // drain the warp's 32 x 128 accumulator block into 64 packed registers, release TMEM, store
+                uint32_t pk[kNH / 2];
+#pragma unroll
+                for (int c = 0; c < kNH; c += 32) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(taddr + c, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        __nv_bfloat162 b2 =
+                            __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                        pk[c / 2 + k] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                }
+                release(tmem_empty, lane, leader);
+                c0 = clock64();
+                c_drain += c0 - c1;
+                if (store) {
+#pragma unroll
+                    for (int c = 0; c < kChunks; ++c)
+                        if (t0 + c * kCw < a.T) stage_store(buf, a.y_slots, c, lane, &pk[32 * c], &tmap_y, t0 + c * kCw, rt * 128 + 32 * qd);
+                }
+                c_store += clock64() - c0;
+            } else {
+                // fp32 (parity path): 32 columns at a time straight from TMEM; release at the end
+#pragma unroll 1
+                for (int c = 0; c < kChunks; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(taddr + 32 * c, v);
+                    tmem_wait_ld();
+                    if (store && t0 + c * kCw < a.T) stage_store(buf, a.y_slots, c, lane, v, &tmap_y, t0 + c * kCw, rt * 128 + 32 * qd);
+                }
+                release(tmem_empty, lane, leader);
+            }
+        }
+        if (lane == 0) bulk_wait0();
+        if (a.trace && warp == 4 && lane == 0) {
+            g_tc2_t[4][blockIdx.x] = c_wait;
+            g_tc2_t[5][blockIdx.x] = c_drain;
+            g_tc2_t[6][blockIdx.x] = c_store;
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // the peer's remote arrivals / the leader's reads of peer shared memory are done
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem, 512);
+    }
+}
+
+}  // namespace
+
+// T > 64, 4 <= M <= 8 (window form).  Returns kLaunchUnsupported when the configuration does not fit.
+int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
+    const vnm_geom& g = L.P->g;
+    if (g.M > 8) return kLaunchUnsupported;
+    Tc2Args a;
+    a.T = L.T;
+    a.rows = g.rows;
+    a.M = g.M;
+    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+    a.n_stage = (a.n_mma + 3) / 4;
+    a.n_rt = (g.rows_p + 127) / 128;
+    a.n_rp = (a.n_rt + 1) / 2;
+    a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
+    const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // X^T rows one stage's windows touch
+    a.rb = (need + 7) / 8 * 8;
+    a.b_bytes = static_cast<uint32_t>(2 * a.rb * 128);
+    // resident A when the pair's whole A + metadata fit next to >= 3 X^T stages (short K: DeiT layers)
+    a.y_slots = 2;
+    a.res_bytes = static_cast<uint32_t>(a.n_stage) * (kABytes + kEBytes);
+    const uint32_t b_stage = (a.b_bytes + 1023) / 1024 * 1024;
+    const uint32_t fixed = 1024 + 256;
+    a.a_res = a.res_bytes + 3 * b_stage + 8 * kYSlot + fixed <= kMaxSmem ? 1 : 0;
+    if (const char* e = getenv("VNM_TC2_ARES")) a.a_res = a.a_res && atoi(e) != 0;
+    a.n_tt = (L.T + kNT - 1) / kNT;
+    a.work = a.n_rp * a.n_tt;
+    if (a.a_res && num_sms() / 2 < a.n_rp) a.a_res = 0;  // every row pair needs a CTA pair of its own
+    if (a.a_res) {
+        a.y_slots = a.res_bytes + 3 * b_stage + 16 * kYSlot + fixed <= kMaxSmem ? 2 : 1;
+        a.stage_bytes = b_stage;
+    } else {
+        a.res_bytes = 0;
+        a.stage_bytes = (kABytes + kEBytes + a.b_bytes + 1023) / 1024 * 1024;
+    }
+    const uint32_t avail = static_cast<uint32_t>(kMaxSmem) - a.res_bytes - 8 * a.y_slots * kYSlot - fixed;
+    a.stages = static_cast<int>(avail / a.stage_bytes);
+    if (a.stages > 8) a.stages = 8;
+    if (a.stages < 2) return kLaunchUnsupported;
+    // the larger operand stays hot in L2 across the tiles resident at a time (see spmm_tc.cu)
+    const int64_t w_bytes = static_cast<int64_t>(a.n_rt) * 128 * 16 * a.n_mma;
+    a.row_major = w_bytes > static_cast<int64_t>(g.cols) * L.T ? 1 : 0;
+    if (const char* e = getenv("VNM_TC2_ORDER")) a.row_major = atoi(e);
+
+    CUtensorMap ta, tb, te, ty;
+    const int ld_tc = 16 * a.n_mma;
+    if (!encode_2d(&ta, L.P->values_tc, static_cast<uint64_t>(ld_tc), static_cast<uint64_t>(a.n_rt) * 128,
+                   static_cast<uint64_t>(ld_tc) * 2, 64, 128))
+        return kLaunchCudaError;
+    if (!encode_2d(&tb, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols),
+                   static_cast<uint64_t>(L.ldx) * 2, 64, static_cast<uint32_t>(a.rb)))
+        return kLaunchCudaError;
+    if (!encode_2d(&te, L.P->meta_tc, 4, static_cast<uint64_t>(a.n_rt) * a.n_stage * 128, 16, 4, 128,
+                   CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return kLaunchCudaError;
+    const bool bf = L.y_dtype == VNM_BF16;
+    if (!encode_2d(&ty, L.YT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.rows),
+                   static_cast<uint64_t>(L.ldy) * (bf ? 2 : 4), bf ? 64 : 32, 32,
+                   bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32))
+        return kLaunchCudaError;
+    const size_t smem = a.res_bytes + static_cast<size_t>(a.stages) * a.stage_bytes + 8 * a.y_slots * kYSlot + 1024 + 256;
+    auto k = bf ? vnm_spmm_tc2_kernel<true> : vnm_spmm_tc2_kernel<false>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return kLaunchCudaError;
+    int pairs = num_sms() / 2;
+    if (a.a_res) {
+        const int ng = pairs / a.n_rp;  // groups of n_rp pairs, at most one group per token tile
+        pairs = (ng < a.n_tt ? ng : a.n_tt) * a.n_rp;
+    } else if (a.work < pairs) {
+        pairs = a.work;
+    }
+    a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
+    k<<<2 * pairs, kThreads, smem, stream>>>(ta, tb, te, ty, a);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && a.trace) {
+        static unsigned long long h[8][160];
+        cudaStreamSynchronize(stream);
+        cudaMemcpyFromSymbol(h, g_tc2_t, sizeof(h));
+        fprintf(stderr, "tc2: grid %d stages %d a_res %d y_slots %d n_stage %d work %d row_major %d\n", 2 * pairs,
+                a.stages, a.a_res, a.y_slots, a.n_stage, a.work, a.row_major);
+        for (int i = 0; i < 2 * pairs; i += 9)
+            fprintf(stderr, "  cta %3d tiles %llu | mma: wait_full %7llu wait_empty %7llu total %8llu | prod wait %8llu | "
+                            "epi wait %8llu drain %6llu store %7llu\n", i, h[7][i], h[0][i], h[1][i], h[2][i], h[3][i],
+                    h[4][i], h[5][i], h[6][i]);
+    }
+    return e == cudaSuccess ? 0 : kLaunchCudaError;
+}
+
+}  // namespace vnm

@@ -30,6 +30,7 @@ struct PruneLaunch {
     uint32_t* meta_tc = nullptr;
 };
 int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream);
+int launch_prune2(const PruneLaunch& L, cudaStream_t stream);  // V >= 32 (prune2.cu)
 
 struct SpmmLaunch {
     const vnm_packed* P;
@@ -43,7 +44,8 @@ struct SpmmLaunch {
     size_t workspace_bytes;
 };
 int launch_spmm(const SpmmLaunch& L, cudaStream_t stream);
-int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream);  // window form (values_tc / meta_tc)
+int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream);   // window form (values_tc / meta_tc), 1 CTA
+int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream);  // window form on CTA pairs (M = 256)
 int launch_pack_tc(const vnm_packed& P, cudaStream_t stream);
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 // small-T plan (spmm_pair.cu): T <= 32, V = 64, M <= 8

@@ -160,7 +160,7 @@ def tc_bytes(g: Geom) -> tuple[int, int]:
 
 
 def pack_tc(P: Packed) -> Packed:
-    """Fill the tensor-core window form of P (allocating it on P's device); V = 64, 4 <= M <= 8 only."""
+    """Fill the tensor-core window form of P (allocating it on P's device); 32 <= V <= 128, 4 <= M <= 8 only."""
     _require_cuda(P.values)
     nv, nm = tc_bytes(P.g)
     if nv == 0:
@@ -201,12 +201,12 @@ def compress(W: torch.Tensor, mask: torch.Tensor, V: int, M: int, status: torch.
 def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None, want_mask: bool = False,
                    tc: bool = False):
     """Fused S_{V:N:M} + compression in one pass over W.  Returns Packed (and the mask if asked); with tc=True
-    the tensor-core window form is also filled (vnm_pack_tc) when it applies (V = 64, M <= 8)."""
+    the tensor-core window form is also filled in the same pass when it applies (32 <= V <= 128, M <= 8)."""
     W = _as_bits16(W)
     _require_cuda(W, score)
     g = geometry(W.shape[0], W.shape[1], V, M)
     P = Packed.empty(g, W.device)
-    if tc and V == 64 and M <= 8:
+    if tc and 32 <= V <= 128 and M <= 8:
         nv, nm = tc_bytes(g)
         P.values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=W.device)
         P.meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=W.device)

@@ -137,3 +137,28 @@ def test_window_form_fused_equals_standalone(rows, cols, M):
     assert torch.equal(P.values.view(torch.int16), Q.values.view(torch.int16))
     assert torch.equal(P.values_tc.view(torch.int16), Q.values_tc.view(torch.int16))
     assert torch.equal(P.meta_tc, Q.meta_tc)
+
+
+@pytest.mark.parametrize("V", [32, 128])
+@pytest.mark.parametrize("rows,cols,M", [(256, 640, 5), (300, 333, 8), (128, 100, 4), (512, 1000, 7)])
+def test_window_form_fused_any_v(V, rows, cols, M):
+    """Window form written by the fused pass for V != 64 == vnm_pack_tc of the canonical output."""
+    W = synth.weights(rows, cols, seed=rows + cols + M + V)
+    Wd = to_dev_bf16(W)
+    P = vnm.prune_compress(Wd, V, M, tc=True)
+    Q = vnm.prune_compress(Wd, V, M)
+    vnm.pack_tc(Q)
+    torch.cuda.synchronize()
+    assert torch.equal(P.values_tc.view(torch.int16), Q.values_tc.view(torch.int16))
+    assert torch.equal(P.meta_tc, Q.meta_tc)
+    mask_ref, v_ref, c_ref, m_ref = oracle.prune_pack(W, V, M)
+    v, c, m = packed_np(P)
+    assert np.array_equal(v, v_ref) and np.array_equal(c, c_ref) and np.array_equal(m, m_ref)
+
+
+@pytest.mark.parametrize("V,M,kind", [(64, 5, "normal"), (128, 6, "int"), (32, 9, "wide"), (256, 4, "outlier"),
+                                      (64, 16, "int"), (128, 32, "normal")])
+def test_llama_scale_bitexact(V, M, kind):
+    """Full-width weight (4096 x 4096-ish, ragged) through the V >= 32 kernel, every byte vs the oracle."""
+    W = synth.weights(4160 if V <= 64 else 4096, 4100, seed=V * 31 + M, kind=kind)
+    check(W, V, M)

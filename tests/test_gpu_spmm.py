@@ -207,3 +207,21 @@ def test_window_plan_bf16_out_and_identity():
 def test_determinism():
     W, XT, _ = make(256, 1000, 64, 5, 300, seed=77)
     assert np.array_equal(gpu_y(W, XT, 64, 5, 300), gpu_y(W, XT, 64, 5, 300))
+
+
+@pytest.mark.parametrize("V", [32, 128])
+@pytest.mark.parametrize("rows,cols,T,M", [(256, 640, 300, 5), (384, 1000, 65, 8), (128, 333, 8, 6),
+                                           (512, 4096, 256, 5), (640, 770, 1, 4)])
+def test_window_plan_any_v(V, rows, cols, T, M):
+    """NEXT-1: V != 64 (e.g. the paper's 128:2:M) runs in the window form at any T."""
+    W, XT, Wm = make(rows, cols, V, M, T, seed=V + rows + cols + M)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, V, M, T, tc=True), Yref, Aref)
+
+
+def test_v128_without_window_form_is_unsupported():
+    W = synth.weights(256, 256, seed=3)
+    P = vnm.prune_compress(to_dev_bf16(W), 128, 5)
+    with pytest.raises(RuntimeError):
+        vnm.spmm(to_dev_bf16(synth.activations_t(256, 128, seed=4)), P, T=128)
+
