@@ -285,15 +285,25 @@ def run_gpu(args):
         achieved, peak, unit = sp_bytes / sp_t / 1e9, pk["hbm_gbs"], "GB/s"
     else:
         achieved, peak, unit = useful / sp_t / 1e12, pk["bf16_tflops"], "TFLOP/s"
-    traffic = None
+    traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.workload)
+            t = json.load(open(tf)).get(args.workload)
+            if t:
+                # dram read + write bytes of one captured launch (ncu --set full); its algorithmic bytes beside it
+                li = next((i for i, l in enumerate(layers) if t["launch"].startswith(l["name"] + " ")), None)
+                traffic = t["bytes_per_launch"]
+                if li is not None:
+                    n = layers[li]["n"]
+                    traffic_note = (f"{t['launch']}: {traffic / 1e6:.1f} MB DRAM vs "
+                                    f"{(n['packed_bytes'] + n['xt_bytes'] + n['yt_bytes']) / 1e6:.1f} MB algorithmic "
+                                    f"({t['source']})")
         except Exception:
             traffic = None
     roofline = {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
-                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "vnm_spmm_kernel",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_note": traffic_note,
+                "kernel": "vnm_spmm (tcgen05.mma.sp window-form / small-T kernels, per-layer launches)",
                 "peak_source": "MEASURED_PEAKS.json" if not pk.get("fallback") else "fallback",
                 "spmm_share_of_step": round(sp_t / (ms_per_step * 1e-3), 4)}
 

@@ -141,6 +141,23 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T);
 
+/* ---- RIA importance: the score pre-pass for vnm_prune / vnm_prune_compress.
+ * Eq. (1), §3 P:86-90:
+ *     RIA_ij = ( |W_ij| / sum_r |W_rj| + |W_ij| / sum_c |W_ic| ) * ( ||X_j||_2 )^a
+ * Readings (Q16, Q21): ||X_j|| is the L2 norm over tokens of INPUT channel j (the column of W,
+ * SPEC S:165); a zero row / column sum makes its fraction 0; fp32 arithmetic.
+ *
+ * vnm_act_norms: norms[j] = ||X^T[j][0..T)||_2 for j < cols.  XT bf16 [cols][ldx] (16-B aligned), norms fp32
+ *   [cols] (4-B aligned, caller-owned).
+ * vnm_ria_score: score fp32 [rows][lds] (16-B aligned, lds % 4 == 0) from W bf16 [rows][ldw] (16-B aligned,
+ *   ldw % 8 == 0); act_norms fp32 [cols] or NULL (all ones: the activation factor is 1); a >= 0
+ *   (0.5 in the cited RIA work).  workspace: caller-owned device scratch of at least
+ *   vnm_ria_workspace_bytes(rows, cols) bytes, 16-B aligned.  Deterministic (fixed summation order).  */
+vnm_status vnm_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, float* norms, vnm_stream_t stream);
+size_t vnm_ria_workspace_bytes(int32_t rows, int32_t cols);
+vnm_status vnm_ria_score(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const float* act_norms, float a,
+                         float* score, int64_t lds, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
+
 /* Human-readable text of a status (static storage).                                                   */
 const char* vnm_status_string(vnm_status s);
 

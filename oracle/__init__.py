@@ -66,6 +66,8 @@ def lib():
             L.vnmo_apply_mask.argtypes = [P, i64, P, i32, i32, i32, i32, P]
             L.vnmo_retained_score.argtypes = [P, i64, P, i32, i32, i32, i32]
             L.vnmo_retained_score.restype = ctypes.c_double
+            L.vnmo_act_norms.argtypes = [P, i64, i32, i32, P]
+            L.vnmo_ria.argtypes = [P, i64, i32, i32, P, ctypes.c_double, P, i64, P]
             _lib = L
     return _lib
 
@@ -207,3 +209,30 @@ def tolerance(YT_ref: np.ndarray, AT_ref: np.ndarray, y_is_bf16: bool = False) -
     if y_is_bf16:
         tol = tol + np.abs(YT_ref) * 2.0 ** -8
     return tol
+
+
+def act_norms(XT: np.ndarray, T: int | None = None) -> np.ndarray:
+    """||X_j||_2 over the tokens of every input channel j (Eq. 1; channel reading S:165), fp64.
+    XT: bf16 bits [cols][ldx] (feature-major)."""
+    XT = np.ascontiguousarray(XT, dtype=np.uint16)
+    cols, ldx = XT.shape
+    T = ldx if T is None else T
+    out = np.zeros(cols, np.float64)
+    st = lib().vnmo_act_norms(_p(XT), ldx, cols, T, _p(out))
+    if st:
+        raise ValueError(f"vnmo_act_norms status {st}")
+    return out
+
+
+def ria(W: np.ndarray, act: np.ndarray | None = None, a: float = 0.5, want_f64: bool = False):
+    """RIA importance, Eq. (1): (|W_ij| / sum_r |W_rj| + |W_ij| / sum_c |W_ic|) * act_j^a, fp64 rounded
+    to fp32 once; zero sums give a zero fraction; act None = all ones."""
+    W = np.ascontiguousarray(W, dtype=np.uint16)
+    rows, cols = W.shape
+    out = np.zeros((rows, cols), np.float32)
+    s64 = np.zeros((rows, cols), np.float64) if want_f64 else None
+    actv = None if act is None else np.ascontiguousarray(act, dtype=np.float64)
+    st = lib().vnmo_ria(_p(W), cols, rows, cols, _p(actv), float(a), _p(out), cols, _p(s64))
+    if st:
+        raise ValueError(f"vnmo_ria status {st}")
+    return (out, s64) if want_f64 else out

@@ -362,3 +362,52 @@ double vnmo_retained_score(const float* score, int64_t lds, const uint32_t* mask
             if (mask_bit(mask, &g, r, c)) s += fabs((double)score[(int64_t)r * lds + c]);
     return s;
 }
+
+/* ---------------------------------------------------------------------------------------------------
+ * RIA importance, the step before the path for TS1/TS3 masks:
+ *   Eq. (1):  RIA_ij = ( |W_ij| / sum_r |W_rj| + |W_ij| / sum_c |W_ic| ) * ( ||X_j||_2 )^a
+ * with the SPEC reading of the activation index (input channel j = column of W) and of
+ * zero sums (a fraction with a zero denominator is 0).  Computed in fp64 and rounded to fp32 once
+ * (the precision is not fixed by the paper; reading Q21).
+ *   vnmo_act_norms:  norms[j] = sqrt( sum_t x[j][t]^2 ), X^T bf16 [cols][ldx] (feature-major)
+ *   vnmo_ria:        score fp32 [rows][lds]; act == NULL means ||X_j|| = 1 for every j (S:166 default)
+ * ------------------------------------------------------------------------------------------------- */
+int vnmo_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, double* norms) {
+    if (!XT || !norms || cols < 0 || T < 0 || ldx < T) return VNMO_ERR_ARG;
+    for (int32_t j = 0; j < cols; ++j) {
+        double s = 0.0;
+        for (int32_t t = 0; t < T; ++t) {
+            const double x = (double)bf16_bits_to_float(XT[(int64_t)j * ldx + t]);
+            s += x * x;
+        }
+        norms[j] = sqrt(s);
+    }
+    return VNMO_OK;
+}
+
+int vnmo_ria(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const double* act, double a,
+             float* score, int64_t lds, double* score64 /* nullable: the fp64 values before rounding */) {
+    if (!W || !score || rows < 0 || cols < 0 || ldw < cols || lds < cols) return VNMO_ERR_ARG;
+    double* colsum = (double*)calloc((size_t)cols + 1, sizeof(double));
+    double* rowsum = (double*)calloc((size_t)rows + 1, sizeof(double));
+    if (!colsum || !rowsum) { free(colsum); free(rowsum); return VNMO_ERR_ARG; }
+    for (int32_t i = 0; i < rows; ++i)
+        for (int32_t j = 0; j < cols; ++j) {
+            const double w = fabs((double)bf16_bits_to_float(W[(int64_t)i * ldw + j]));
+            rowsum[i] += w;   /* sum_c |W_ic|: output channel i */
+            colsum[j] += w;   /* sum_r |W_rj|: input channel j  */
+        }
+    for (int32_t i = 0; i < rows; ++i)
+        for (int32_t j = 0; j < cols; ++j) {
+            const double w = fabs((double)bf16_bits_to_float(W[(int64_t)i * ldw + j]));
+            const double f1 = colsum[j] > 0.0 ? w / colsum[j] : 0.0;
+            const double f2 = rowsum[i] > 0.0 ? w / rowsum[i] : 0.0;
+            const double act_j = act ? act[j] : 1.0;
+            const double s = (f1 + f2) * pow(act_j, a);
+            score[(int64_t)i * lds + j] = (float)s;
+            if (score64) score64[(int64_t)i * cols + j] = s;
+        }
+    free(colsum);
+    free(rowsum);
+    return VNMO_OK;
+}

@@ -199,10 +199,22 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || g->V != 64);
     if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
     if (tc) {
-        // CTA-pair kernel by default; VNM_TC_PLAN=1 selects the single-CTA window kernel (comparisons)
-        static const bool single = [] { const char* e = getenv("VNM_TC_PLAN"); return e && e[0] == '1'; }();
-        if (!single) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
+        // Measured (profiles/r01b_*): the CTA-pair kernel wins for long K with an even number of 128-row tiles
+        // (Llama layers, DeiT-B fc2) — tensor-bound; the single-CTA kernel wins for short K / HBM-bound shapes
+        // (DeiT qkv / proj / fc1), where its deeper X^T prefetch and finer tiles matter more.
+        // VNM_TC_PLAN=1 / 2 forces the single-CTA / pair kernel (comparisons).
+        static const int force = [] { const char* e = getenv("VNM_TC_PLAN"); return e ? atoi(e) : 0; }();
+        const int n_stage = (g->nb_pad / (g->M == 4 ? 8 : 4) + 3) / 4, n_rt = (g->rows_p + 127) / 128;
+        const bool pair = force ? force == 2 : (n_stage >= 12 && n_rt % 2 == 0);
+        if (pair) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
         return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
+    }
+    // the register-direct mma.sp decode kernel (spmm_dec.cu) measured slower than the small-T TMA plan
+    // (32-byte row segments per k-step: poor DRAM locality, profiles/r01b_decode.md); opt-in VNM_DEC=1
+    static const bool use_dec = [] { const char* e = getenv("VNM_DEC"); return e && e[0] == '1'; }();
+    if (use_dec && vnm::spmm_dec_applies(*g, T)) {
+        const int rc = vnm::launch_spmm_dec(L, reinterpret_cast<cudaStream_t>(stream));
+        if (rc != vnm::kLaunchUnsupported) return from_launch(rc);  // else: no workspace -> other plans
     }
     if (vnm::spmm_pair_applies(*g, T)) return from_launch(vnm::launch_spmm_pair(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
@@ -210,7 +222,35 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T) {
     if (check_geom(g) != VNM_OK || T < 0) return 0;
-    return vnm::spmm_pair_applies(*g, T) ? vnm::spmm_pair_workspace_bytes(*g, T) : vnm::spmm_workspace_bytes(*g, T);
+    size_t dec = vnm::spmm_dec_applies(*g, T) ? vnm::spmm_dec_workspace_bytes(*g, T) : 0;
+    size_t other = vnm::spmm_pair_applies(*g, T) ? vnm::spmm_pair_workspace_bytes(*g, T) : vnm::spmm_workspace_bytes(*g, T);
+    return dec > other ? dec : other;
+}
+
+vnm_status vnm_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, float* norms, vnm_stream_t stream) {
+    if (cols < 0 || T < 0 || ldx < T) return VNM_ERR_SHAPE;
+    if (cols == 0) return VNM_OK;
+    if (!norms || (T > 0 && !XT)) return VNM_ERR_ARG;
+    if ((XT && !aligned16(XT)) || (reinterpret_cast<uintptr_t>(norms) & 3u)) return VNM_ERR_ALIGN;
+    return from_launch(vnm::launch_act_norms(XT, ldx, cols, T, norms, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t vnm_ria_workspace_bytes(int32_t rows, int32_t cols) {
+    if (rows < 0 || cols < 0) return 0;
+    return vnm::ria_workspace_bytes(rows, cols);
+}
+
+vnm_status vnm_ria_score(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const float* act_norms, float a,
+                         float* score, int64_t lds, void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
+    if (rows < 0 || cols < 0 || ldw < cols || lds < cols || !(a >= 0.f)) return VNM_ERR_SHAPE;
+    if (rows == 0 || cols == 0) return VNM_OK;
+    if (!W || !score || !workspace) return VNM_ERR_ARG;
+    if (workspace_bytes < vnm::ria_workspace_bytes(rows, cols)) return VNM_ERR_SHAPE;
+    if (!aligned16(W) || (ldw % 8) != 0 || !aligned16(score) || (lds % 4) != 0 || !aligned16(workspace) ||
+        (act_norms && (reinterpret_cast<uintptr_t>(act_norms) & 3u)))
+        return VNM_ERR_ALIGN;
+    return from_launch(vnm::launch_ria(W, ldw, rows, cols, act_norms, a, score, lds, workspace,
+                                       reinterpret_cast<cudaStream_t>(stream)));
 }
 
 const char* vnm_status_string(vnm_status s) {

@@ -97,3 +97,59 @@ extern "C" int vnm_probe_bench_mma_pair(const uint16_t* X, uint32_t n_mma, uint3
     if (cudaGetLastError() != cudaSuccess) return 4;
     return cudaDeviceSynchronize() == cudaSuccess ? 0 : 5;
 }
+
+// ---- DRAM access pattern probe: stream a [rows][ld] bf16 matrix with TMA boxes of box_h rows x box_w
+// values; CTA c takes row groups c, c + grid, ... and walks each group's K tiles in order (the decode
+// kernels' pattern), `stages` boxes in flight.  Returns elapsed ns (globaltimer) of the whole grid.
+namespace vnm {
+namespace {
+__device__ unsigned long long g_p3_t[2];
+__global__ void __launch_bounds__(32, 1) stream_boxes_kernel(const __grid_constant__ CUtensorMap tm, int32_t rows,
+                                                              int32_t cols, int32_t box_h, int32_t box_w, int32_t stages,
+                                                              uint32_t box_bytes) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    __shared__ __align__(8) uint64_t bar[8];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < stages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+    if (blockIdx.x == 0) g_p3_t[0] = t0;
+    const int ngr = (rows + box_h - 1) / box_h, nk = (cols + box_w - 1) / box_w;
+    int q = 0;
+    for (int gr = blockIdx.x; gr < ngr; gr += gridDim.x)
+        for (int k = 0; k < nk; ++k, ++q) {
+            const int s = q % stages;
+            if (q >= stages) mbar_wait(&bar[s], ((q / stages) - 1) & 1);
+            mbar_arrive_expect_tx(&bar[s], box_bytes);
+            tma_load_2d(smem + s * box_bytes, &tm, k * box_w, gr * box_h, &bar[s]);
+        }
+    for (int i = (q > stages ? q - stages : 0); i < q; ++i) mbar_wait(&bar[i % stages], (i / stages) & 1);
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+    atomicMax(&g_p3_t[1], t1);
+}
+}  // namespace
+}  // namespace vnm
+
+extern "C" int vnm_probe_stream_boxes(const uint16_t* A, int32_t rows, int32_t cols, int64_t ld, int32_t box_h,
+                                      int32_t box_w, int32_t stages, int32_t grid, unsigned long long* ns) {
+    using namespace vnm;
+    CUtensorMap tm;
+    if (!encode_2d(&tm, A, cols, rows, ld * 2, box_w, box_h, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return 2;
+    const uint32_t box_bytes = box_h * box_w * 2;
+    const size_t smem = static_cast<size_t>(stages) * box_bytes + 128;
+    if (cudaFuncSetAttribute(stream_boxes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return 3;
+    unsigned long long z[2] = {0, 0};
+    cudaMemcpyToSymbol(g_p3_t, z, sizeof(z));
+    stream_boxes_kernel<<<grid, 32, smem>>>(tm, rows, cols, box_h, box_w, stages, box_bytes);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    unsigned long long h[2];
+    cudaMemcpyFromSymbol(h, g_p3_t, sizeof(h));
+    *ns = h[1] - h[0];
+    return 0;
+}

@@ -285,7 +285,7 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
 
 int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
-    if (g.V != 64 || g.M > 8) return kLaunchUnsupported;
+    if (g.V < 32 || g.V > 128 || g.M > 8) return kLaunchUnsupported;  // window form: rows independent of V
     TcArgs a;
     a.meta_tc = L.P->meta_tc;
     a.YT = L.YT;

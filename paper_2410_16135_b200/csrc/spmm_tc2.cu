@@ -10,17 +10,18 @@
 // 256 output rows.  Rows are independent in the window form (each row carries its own 2:4 metadata over
 // the block's 8-channel window), so any V works as long as the window form was built for it.
 //
-// Tile = 256 output rows (row tiles 2p, 2p+1; CTA rank r owns 2p+r) x 256 tokens (rank r loads B for
-// tokens 128r..128r+127).  Stage = 4 MMAs (16 blocks; 32 for M = 4).
+// Tile = 256 output rows (row tiles 2p, 2p+1; CTA rank r owns 2p+r) x NT tokens (rank r holds B for tokens
+// r*NT/2 .. (r+1)*NT/2 - 1, loaded as two 64-token boxes).  Stage = 4 MMAs (16 blocks; 32 for M = 4).
+// NT = 256: one accumulator (256 TMEM columns) — long K, the per-tile hand-off is amortised; NT = 192: two
+// accumulators (2 x 192 columns) so the epilogue of tile i overlaps the MMAs of tile i + 1 — short K.
 //   warp 0       TMA (both CTAs): own A (values_tc 128 x 64), own metadata chunk, own half of the X^T
 //                window rows; completion counted on the leader's full barrier (cta_group::2 TMA);
 //   warp 1       TMEM allocation (both CTAs) and, in the leader only, the MMA thread: tcgen05.cp of both
 //                CTAs' metadata -> their TMEM, 4 x tcgen05.mma.sp.cta_group::2, commits multicast to both;
-//   warps 4-11   epilogue (both CTAs): warp 4 + q + 4h drains TMEM lanes 32q.. x columns 128h.. into
-//                registers, releases the accumulator (leader's tmem_empty, 16 arrivals), then converts and
-//                writes Y^T through swizzled shared staging with TMA tensor stores — so the store of tile i
-//                overlaps the main loop of tile i + 1 although the accumulator is single-buffered
-//                (256 fp32 columns + the metadata ring fill the 512 TMEM columns).
+//   warps 4..    epilogue (both CTAs): warp 4 + q + 4c drains TMEM lanes 32q.. x the 64 columns of token
+//                chunk c into registers, releases the accumulator (leader's tmem_empty), then converts and
+//                writes Y^T through swizzled shared staging with TMA tensor stores, overlapping the next
+//                tile's main loop.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -35,13 +36,10 @@
 namespace vnm {
 namespace {
 
-constexpr int kThreads = 384;
-constexpr int kNT = 256;                    // tokens per pair tile
-constexpr int kNH = kNT / 2;                // tokens per CTA of B
 constexpr uint32_t kABytes = 128 * 128;     // 128 rows x 64 bf16 (SW128)
 constexpr uint32_t kEBytes = 128 * 16;      // 128 lanes x 4 words
 constexpr uint32_t kYSlot = 32 * 128;       // one 32 row x 128 B staging slot (SW128)
-constexpr uint32_t kMetaCol = 256;          // TMEM: accumulator columns 0..255, metadata ring from 256
+constexpr uint32_t kBChunk = 64;            // tokens per B box / per epilogue chunk
 
 struct Tc2Args {
     int32_t T, rows, M;
@@ -55,11 +53,23 @@ struct Tc2Args {
     int32_t y_slots;     // epilogue staging slots per warp (1 or 2)
     uint32_t b_bytes, stage_bytes, res_bytes;
     int32_t trace;       // VNM_SPMM_TRACE: per-CTA wait / busy cycle counters into g_tc2_t
+    int32_t stg;         // bf16 epilogue: 1 = 16-byte global stores from registers (no shared staging)
+    void* YT;
+    int64_t ldy;
 };
 
 // VNM_SPMM_TRACE counters per CTA: MMA wait full, MMA wait tmem_empty, MMA loop total, producer wait empty,
 // epilogue (warp 4) wait tmem_full, drain, store, tiles
 __device__ unsigned long long g_tc2_t[8][160];
+
+template <int NT>
+struct Cfg {
+    static constexpr int kNACC = NT == 256 ? 1 : 2;             // accumulators in TMEM
+    static constexpr uint32_t kMetaCol = kNACC * NT;             // metadata ring after the accumulators
+    static constexpr int kChunks = NT / kBChunk;                 // 64-token chunks per tile
+    static constexpr int kEpiWarps = 4 * kChunks;                // one warp per (lane quadrant, chunk)
+    static constexpr int kThreads = 128 + 32 * kEpiWarps;
+};
 
 // i-th tile (row pair rp, token tile tt) of cluster cid; false past the end
 __device__ __forceinline__ bool tile_of(const Tc2Args& a, int cid, int ncl, int i, int& rp, int& tt) {
@@ -110,22 +120,25 @@ __device__ __forceinline__ void stage_store(uint8_t* buf, int nslot, int c, int 
     }
 }
 
-template <bool kBf16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int NT, bool kBf16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1)
     vnm_spmm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                         const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_y,
                         const Tc2Args a) {
+    using C = Cfg<NT>;
+    constexpr int kNH = NT / 2;  // tokens per CTA of B
+    constexpr uint32_t kMetaCol = C::kMetaCol;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = a.stages;
     // [resident A (n_stage x 16 KB) | resident E (n_stage x 2 KB)] (a_res only), ring, Y staging, barriers
     uint8_t* ring = smem + a.res_bytes;
     uint8_t* sY = ring + S * a.stage_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sY + 8 * a.y_slots * kYSlot);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sY + C::kEpiWarps * a.y_slots * kYSlot);
     uint64_t* empty = full + S;
-    uint64_t* tmem_full = empty + S;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint64_t* res_full = tmem_empty + 1;
+    uint64_t* tmem_full = empty + S;        // [kNACC]
+    uint64_t* tmem_empty = tmem_full + 2;   // [kNACC]
+    uint64_t* res_full = tmem_empty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 1);
     const uint32_t b_off = a.a_res ? 0u : kABytes, e_off = kABytes + a.b_bytes;
     uint8_t* resE = smem + a.n_stage * kABytes;
@@ -139,8 +152,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 16);
+        for (int i = 0; i < C::kNACC; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 2 * C::kEpiWarps);
+        }
         mbar_init(res_full, 1);
         fence_mbar_init();
     }
@@ -164,7 +179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int i = 0; tile_of(a, cid, ncl, i, rp, tt); ++i) {
                 const int rt = 2 * rp + static_cast<int>(rank);  // row tiles past n_rt read as zeros (TMA OOB)
                 const int rte = rt < a.n_rt ? rt : 0;             // ... with valid metadata
-                const int n0 = tt * kNT + kNH * static_cast<int>(rank);
+                const int n0 = tt * NT + kNH * static_cast<int>(rank);
                 if (a.a_res && i == 0) {  // the pair's A and metadata, once
                     if (leader) mbar_arrive_expect_tx(res_full, 2 * a.n_stage * (kABytes + kEBytes));
                     for (int st = 0; st < a.n_stage; ++st) {
@@ -195,15 +210,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ MMA issuer (leader CTA)
         if (leader && lane == 0) {
             int q = 0, tl = 0, rp, tt;
-            const uint32_t idesc0 = idesc_bf16(256, kNT, true, 0, true);
-            const uint32_t idesc1 = idesc_bf16(256, kNT, true, 1, true);
+            const uint32_t idesc0 = idesc_bf16(256, NT, true, 0, true);
+            const uint32_t idesc1 = idesc_bf16(256, NT, true, 1, true);
             const uint32_t k_bytes = (a.M == 4 ? 32u : 4u * a.M) * 128u;  // B advance per MMA
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;          // K-group (window) stride
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
             for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
                 if (a.a_res && tl == 0) mbar_wait(res_full, 0);
+                const int acc = C::kNACC == 2 ? (tl & 1) : 0;
+                const uint32_t d_tmem = tmem + acc * NT;
                 c0 = clock64();
-                mbar_wait(tmem_empty, (tl & 1) ^ 1);
+                mbar_wait(&tmem_empty[acc], ((C::kNACC == 2 ? tl >> 1 : tl) & 1) ^ 1);
                 c_emp += clock64() - c0;
                 tc_fence_after();
                 for (int st = 0; st < a.n_stage; ++st, ++q) {
@@ -224,13 +241,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (mi < a.n_mma) {
                             const uint64_t bd = sdesc(b0 + k * k_bytes, a.rb * 128, sbo, kLayoutSW128);
                             const uint64_t ad = sdesc(a0 + 32 * k, 16, 1024, kLayoutSW128);
-                            mma_sp_bf16_pair(tmem, ad, bd, meta_s + (k & ~1), (k & 1) ? idesc1 : idesc0,
+                            mma_sp_bf16_pair(d_tmem, ad, bd, meta_s + (k & ~1), (k & 1) ? idesc1 : idesc0,
                                              mi > 0 ? 1u : 0u);
                         }
                     }
                     mma_commit_pair(&empty[s], 0x3);
                 }
-                mma_commit_pair(tmem_full, 0x3);
+                mma_commit_pair(&tmem_full[acc], 0x3);
             }
             if (a.trace) {
                 g_tc2_t[0][blockIdx.x] = c_full;
@@ -241,56 +258,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue (both CTAs)
-        const int ew = warp - 4, qd = ew % 4, hf = ew / 4;
+        // warp 4 + q + 4c: TMEM lanes 32q.. (rows 32q.. of the CTA's row tile) x token chunk c (64 columns)
+        const int ew = warp - 4, qd = ew % 4, ch = ew / 4;
         uint8_t* buf = sY + ew * a.y_slots * kYSlot;
-        constexpr int kCw = kBf16 ? 64 : 32;             // tokens per 128-byte chunk
-        constexpr int kChunks = kNH / kCw;               // chunks per warp per tile (2 bf16, 4 fp32)
         int tl = 0, rp, tt;
         unsigned long long c_wait = 0, c_drain = 0, c_store = 0, c0, c1;
         for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
             const int rt = 2 * rp + static_cast<int>(rank);
-            const int t0 = tt * kNT + kNH * hf;  // first token of this warp's columns
+            const int t0 = tt * NT + kBChunk * ch;  // first token of this warp's chunk
+            const int acc = C::kNACC == 2 ? (tl & 1) : 0;
             c0 = clock64();
-            mbar_wait(tmem_full, tl & 1);
+            mbar_wait(&tmem_full[acc], (C::kNACC == 2 ? tl >> 1 : tl) & 1);
             c1 = clock64();
             c_wait += c1 - c0;
             tc_fence_after();
-            const uint32_t taddr = tmem + ((32 * qd) << 16) + kNH * hf;
+            const uint32_t taddr = tmem + ((32 * qd) << 16) + acc * NT + kBChunk * ch;
             const bool store = rt < a.n_rt && t0 < a.T;
             if constexpr (kBf16) {
-                // drain the warp's 32 x 128 accumulator block into 64 packed registers, release TMEM, store
-                uint32_t pk[kNH / 2];
+                // drain the warp's 32 x 64 accumulator block (two loads, one wait) into 32 packed registers,
+                // release the accumulator, then stage + store one 128-byte-per-row chunk
+                uint32_t v[64], pk[32];
+                tmem_ld_32x32b_x32(taddr, v);
+                tmem_ld_32x32b_x32(taddr + 32, v + 32);
+                tmem_wait_ld();
+                release(&tmem_empty[acc], lane, leader);
 #pragma unroll
-                for (int c = 0; c < kNH; c += 32) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(taddr + c, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        __nv_bfloat162 b2 =
-                            __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
-                        pk[c / 2 + k] = *reinterpret_cast<uint32_t*>(&b2);
-                    }
+                for (int k = 0; k < 32; ++k) {
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                    pk[k] = *reinterpret_cast<uint32_t*>(&b2);
                 }
-                release(tmem_empty, lane, leader);
                 c0 = clock64();
                 c_drain += c0 - c1;
                 if (store) {
+                    if (a.stg) {
+                        // each lane owns one output row: 8 x 16 B straight to global (full 128-byte lines land
+                        // in L2 before they are written back); rows >= rows / tokens >= T are skipped
+                        const int row = rt * 128 + 32 * qd + lane;
+                        if (row < a.rows) {
+                            __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(a.YT) + static_cast<int64_t>(row) * a.ldy + t0;
+                            if (t0 + 64 <= a.T) {
 #pragma unroll
-                    for (int c = 0; c < kChunks; ++c)
-                        if (t0 + c * kCw < a.T) stage_store(buf, a.y_slots, c, lane, &pk[32 * c], &tmap_y, t0 + c * kCw, rt * 128 + 32 * qd);
+                                for (int k = 0; k < 8; ++k)
+                                    *reinterpret_cast<uint4*>(yr + 8 * k) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+                            } else {
+                                for (int k = 0; k < 32 && t0 + 2 * k < a.T; ++k) {
+                                    reinterpret_cast<uint16_t*>(yr)[2 * k] = static_cast<uint16_t>(pk[k]);
+                                    if (t0 + 2 * k + 1 < a.T) reinterpret_cast<uint16_t*>(yr)[2 * k + 1] = static_cast<uint16_t>(pk[k] >> 16);
+                                }
+                            }
+                        }
+                    } else {
+                        stage_store(buf, 1, 0, lane, pk, &tmap_y, t0, rt * 128 + 32 * qd);
+                    }
                 }
                 c_store += clock64() - c0;
             } else {
-                // fp32 (parity path): 32 columns at a time straight from TMEM; release at the end
+                // fp32 (parity path): two 32-token chunks straight from TMEM; release at the end
 #pragma unroll 1
-                for (int c = 0; c < kChunks; ++c) {
+                for (int c = 0; c < 2; ++c) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(taddr + 32 * c, v);
                     tmem_wait_ld();
-                    if (store && t0 + c * kCw < a.T) stage_store(buf, a.y_slots, c, lane, v, &tmap_y, t0 + c * kCw, rt * 128 + 32 * qd);
+                    if (store && t0 + 32 * c < a.T) stage_store(buf, 1, c, lane, v, &tmap_y, t0 + 32 * c, rt * 128 + 32 * qd);
                 }
-                release(tmem_empty, lane, leader);
+                release(&tmem_empty[acc], lane, leader);
             }
         }
         if (lane == 0) bulk_wait0();
@@ -308,45 +339,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
-}  // namespace
-
-// T > 64, 4 <= M <= 8 (window form).  Returns kLaunchUnsupported when the configuration does not fit.
-int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
+template <int NT>
+int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
+    using C = Cfg<NT>;
     const vnm_geom& g = L.P->g;
-    if (g.M > 8) return kLaunchUnsupported;
-    Tc2Args a;
-    a.T = L.T;
-    a.rows = g.rows;
-    a.M = g.M;
-    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
-    a.n_stage = (a.n_mma + 3) / 4;
-    a.n_rt = (g.rows_p + 127) / 128;
-    a.n_rp = (a.n_rt + 1) / 2;
-    a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
-    const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // X^T rows one stage's windows touch
-    a.rb = (need + 7) / 8 * 8;
-    a.b_bytes = static_cast<uint32_t>(2 * a.rb * 128);
+    a.n_tt = (L.T + NT - 1) / NT;
+    a.work = a.n_rp * a.n_tt;
     // resident A when the pair's whole A + metadata fit next to >= 3 X^T stages (short K: DeiT layers)
-    a.y_slots = 2;
+    a.y_slots = 1;
+    const uint32_t y_bytes = C::kEpiWarps * kYSlot;
     a.res_bytes = static_cast<uint32_t>(a.n_stage) * (kABytes + kEBytes);
     const uint32_t b_stage = (a.b_bytes + 1023) / 1024 * 1024;
     const uint32_t fixed = 1024 + 256;
-    a.a_res = a.res_bytes + 3 * b_stage + 8 * kYSlot + fixed <= kMaxSmem ? 1 : 0;
+    a.a_res = a.res_bytes + 3 * b_stage + y_bytes + fixed <= kMaxSmem ? 1 : 0;
     if (const char* e = getenv("VNM_TC2_ARES")) a.a_res = a.a_res && atoi(e) != 0;
-    a.n_tt = (L.T + kNT - 1) / kNT;
-    a.work = a.n_rp * a.n_tt;
     if (a.a_res && num_sms() / 2 < a.n_rp) a.a_res = 0;  // every row pair needs a CTA pair of its own
     if (a.a_res) {
-        a.y_slots = a.res_bytes + 3 * b_stage + 16 * kYSlot + fixed <= kMaxSmem ? 2 : 1;
         a.stage_bytes = b_stage;
     } else {
         a.res_bytes = 0;
         a.stage_bytes = (kABytes + kEBytes + a.b_bytes + 1023) / 1024 * 1024;
     }
-    const uint32_t avail = static_cast<uint32_t>(kMaxSmem) - a.res_bytes - 8 * a.y_slots * kYSlot - fixed;
+    const uint32_t avail = static_cast<uint32_t>(kMaxSmem) - a.res_bytes - y_bytes - fixed;
     a.stages = static_cast<int>(avail / a.stage_bytes);
     if (a.stages > 8) a.stages = 8;
     if (a.stages < 2) return kLaunchUnsupported;
+    if (C::kMetaCol + 4 * a.stages > 512) a.stages = (512 - C::kMetaCol) / 4;
     // the larger operand stays hot in L2 across the tiles resident at a time (see spmm_tc.cu)
     const int64_t w_bytes = static_cast<int64_t>(a.n_rt) * 128 * 16 * a.n_mma;
     a.row_major = w_bytes > static_cast<int64_t>(g.cols) * L.T ? 1 : 0;
@@ -368,8 +386,8 @@ int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
                    static_cast<uint64_t>(L.ldy) * (bf ? 2 : 4), bf ? 64 : 32, 32,
                    bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32))
         return kLaunchCudaError;
-    const size_t smem = a.res_bytes + static_cast<size_t>(a.stages) * a.stage_bytes + 8 * a.y_slots * kYSlot + 1024 + 256;
-    auto k = bf ? vnm_spmm_tc2_kernel<true> : vnm_spmm_tc2_kernel<false>;
+    const size_t smem = a.res_bytes + static_cast<size_t>(a.stages) * a.stage_bytes + y_bytes + fixed;
+    auto k = bf ? vnm_spmm_tc2_kernel<NT, true> : vnm_spmm_tc2_kernel<NT, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
     int pairs = num_sms() / 2;
@@ -380,21 +398,50 @@ int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
         pairs = a.work;
     }
     a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
-    k<<<2 * pairs, kThreads, smem, stream>>>(ta, tb, te, ty, a);
+    a.YT = L.YT;
+    a.ldy = L.ldy;
+    a.stg = 0;
+    if (const char* e = getenv("VNM_TC2_STG")) a.stg = atoi(e);
+    k<<<2 * pairs, C::kThreads, smem, stream>>>(ta, tb, te, ty, a);
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess && a.trace) {
         static unsigned long long h[8][160];
         cudaStreamSynchronize(stream);
         cudaMemcpyFromSymbol(h, g_tc2_t, sizeof(h));
-        fprintf(stderr, "tc2: grid %d stages %d a_res %d y_slots %d n_stage %d work %d row_major %d\n", 2 * pairs,
-                a.stages, a.a_res, a.y_slots, a.n_stage, a.work, a.row_major);
+        fprintf(stderr, "tc2 NT=%d: grid %d stages %d a_res %d n_stage %d work %d row_major %d\n", NT, 2 * pairs,
+                a.stages, a.a_res, a.n_stage, a.work, a.row_major);
         for (int i = 0; i < 2 * pairs; i += 9)
             fprintf(stderr, "  cta %3d tiles %llu | mma: wait_full %7llu wait_empty %7llu total %8llu | prod wait %8llu | "
                             "epi wait %8llu drain %6llu store %7llu\n", i, h[7][i], h[0][i], h[1][i], h[2][i], h[3][i],
                     h[4][i], h[5][i], h[6][i]);
     }
     return e == cudaSuccess ? 0 : kLaunchCudaError;
+}
+
+}  // namespace
+
+// T > 64, 4 <= M <= 8 (window form).  Returns kLaunchUnsupported when the configuration does not fit.
+int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
+    const vnm_geom& g = L.P->g;
+    if (g.M > 8) return kLaunchUnsupported;
+    Tc2Args a;
+    a.T = L.T;
+    a.rows = g.rows;
+    a.M = g.M;
+    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+    a.n_stage = (a.n_mma + 3) / 4;
+    a.n_rt = (g.rows_p + 127) / 128;
+    a.n_rp = (a.n_rt + 1) / 2;
+    a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
+    const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // X^T rows one stage's windows touch
+    a.rb = (need + 7) / 8 * 8;
+    a.b_bytes = static_cast<uint32_t>(2 * a.rb * 128);
+    // long K: 256-token tiles, one accumulator (the per-tile hand-off is amortised over many stages);
+    // short K: 192-token tiles with two accumulators so the epilogue overlaps the next tile
+    int nt = a.n_stage >= 12 ? 256 : 192;
+    if (const char* e = getenv("VNM_TC2_NT")) nt = atoi(e);
+    return nt == 256 ? launch_nt<256>(L, a, stream) : launch_nt<192>(L, a, stream);
 }
 
 }  // namespace vnm

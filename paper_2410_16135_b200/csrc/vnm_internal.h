@@ -52,5 +52,15 @@ size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 bool spmm_pair_applies(const vnm_geom& g, int32_t T);
 size_t spmm_pair_workspace_bytes(const vnm_geom& g, int32_t T);
 int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t stream);
+// decode plan (spmm_dec.cu): T <= 16, V >= 64, warp-level mma.sp with A straight from global memory
+bool spmm_dec_applies(const vnm_geom& g, int32_t T);
+size_t spmm_dec_workspace_bytes(const vnm_geom& g, int32_t T);
+int launch_spmm_dec(const SpmmLaunch& L, cudaStream_t stream);
+
+// RIA importance (ria.cu)
+size_t ria_workspace_bytes(int32_t rows, int32_t cols);
+int launch_ria(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const float* act, float a, float* score,
+               int64_t lds, void* ws, cudaStream_t st);
+int launch_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, float* norms, cudaStream_t st);
 
 }  // namespace vnm

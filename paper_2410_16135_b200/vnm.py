@@ -47,7 +47,8 @@ _lock = threading.Lock()
 _lib = None
 
 EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress", "vnm_pack_tc",
-           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_status_string", "vnm_launch_count"]
+           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
+           "vnm_status_string", "vnm_launch_count"]
 
 
 def lib():
@@ -77,6 +78,12 @@ def lib():
             L.vnm_spmm.restype = ctypes.c_int
             L.vnm_spmm_workspace_bytes.argtypes = [GP, i32]
             L.vnm_spmm_workspace_bytes.restype = sz
+            L.vnm_act_norms.argtypes = [P, i64, i32, i32, P, P]
+            L.vnm_act_norms.restype = ctypes.c_int
+            L.vnm_ria_workspace_bytes.argtypes = [i32, i32]
+            L.vnm_ria_workspace_bytes.restype = sz
+            L.vnm_ria_score.argtypes = [P, i64, i32, i32, P, ctypes.c_float, P, i64, P, sz, P]
+            L.vnm_ria_score.restype = ctypes.c_int
             L.vnm_status_string.argtypes = [ctypes.c_int]
             L.vnm_status_string.restype = ctypes.c_char_p
             L.vnm_launch_count.argtypes = []
@@ -249,3 +256,28 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
 
 def spmm_workspace_bytes(g: Geom, T: int) -> int:
     return int(lib().vnm_spmm_workspace_bytes(ctypes.byref(g), T))
+
+
+def act_norms(XT: torch.Tensor, T: int | None = None) -> torch.Tensor:
+    """||X_j||_2 over the tokens of every input channel (Eq. 1).  XT bf16 [cols][ldx]."""
+    XT = _as_bits16(XT)
+    _require_cuda(XT)
+    T = XT.shape[1] if T is None else T
+    out = torch.empty(XT.shape[0], dtype=torch.float32, device=XT.device)
+    _check(lib().vnm_act_norms(_ptr(XT), XT.stride(0), XT.shape[0], T, _ptr(out), _stream(XT.device)), "vnm_act_norms")
+    return out
+
+
+def ria_score(W: torch.Tensor, act: torch.Tensor | None = None, a: float = 0.5) -> torch.Tensor:
+    """RIA importance, Eq. (1), fp32 [rows][cols]; pass it as `score` to
+    prune / prune_compress.  act: fp32 [cols] activation norms (act_norms) or None (factor 1)."""
+    W = _as_bits16(W)
+    _require_cuda(W, act)
+    rows, cols = W.shape
+    lds = (cols + 3) // 4 * 4
+    score = torch.empty((rows, lds), dtype=torch.float32, device=W.device)[:, :cols]
+    nws = int(lib().vnm_ria_workspace_bytes(rows, cols))
+    ws = torch.empty(max(nws, 16) // 4 + 4, dtype=torch.float32, device=W.device)
+    _check(lib().vnm_ria_score(_ptr(W), _ld(W), rows, cols, _ptr(act), float(a), _ptr(score), score.stride(0),
+                               _ptr(ws), ws.numel() * 4, _stream(W.device)), "vnm_ria_score")
+    return score

@@ -225,3 +225,27 @@ def test_v128_without_window_form_is_unsupported():
     with pytest.raises(RuntimeError):
         vnm.spmm(to_dev_bf16(synth.activations_t(256, 128, seed=4)), P, T=128)
 
+
+
+def test_decode_mma_sp_kernel_opt_in():
+    """The register-direct mma.sp decode kernel (spmm_dec.cu, opt-in VNM_DEC=1) against the oracle, in a child
+    process so the plan switch is seen at library load."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, oracle\n"
+        "from paper_2410_16135_b200 import synth, vnm\n"
+        "from tests.gpu_util import to_dev_bf16\n"
+        "for rows, cols, M, T in [(256, 1000, 5, 1), (192, 333, 8, 16), (4096, 4096, 5, 8), (128, 64, 7, 13)]:\n"
+        "    W = synth.weights(rows, cols, seed=rows + T); XT = synth.activations_t(cols, T, seed=cols + T)\n"
+        "    mask = oracle.prune(W, 64, M)\n"
+        "    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, mask, 64, M))\n"
+        "    P = vnm.prune_compress(to_dev_bf16(W), 64, M)\n"
+        "    Y = vnm.spmm(to_dev_bf16(XT), P, T=T).cpu().numpy().astype(np.float64)\n"
+        "    assert np.all(np.abs(Y - Yref) <= oracle.tolerance(Yref, Aref)), (rows, cols, M, T)\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, VNM_DEC="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
