@@ -2,20 +2,22 @@
 // §8(d) config 4b.  PAPER.md §3 "Acceleration of V:N:M sparsity" P:106-109, App. A P:548.
 //
 // At T <= 16 the product is a stream of the packed weights (A_n 4/M B per weight, A_i2 0.5/M, A_i1) with a
-// few MACs each; the kernel is built to keep HBM busy with the least work per byte:
-//   * warp-level sparse tensor-core MMA (mma.sp m16n8k32, bf16 -> fp32): A comes straight from global
-//     memory into registers in the fragment layout — A_n already IS the 2:4-compressed operand (2 values
-//     per block = per group of 4 gathered channels, App. A) — so the weights touch neither shared
-//     memory nor a TMA pipeline; the A_i2 words are the MMA metadata (rows g, g+8 of the 16-row tile,
-//     one 16-bit half per thread pair, selector 0);
-//   * the 4 kept X^T channels of every block (A_i1) are gathered from a shared-memory copy of the CTA's
-//     X^T slice into the B fragment, once per 8 blocks and shared by the 4 row tiles of a 64-row group;
-//   * CTA = one 64-row group (rows of one V-block) x a K range; 4 warps interleave k-steps and add their
-//     partials in shared memory in warp order; K ranges of a row group (splits) meet in an fp32 workspace
-//     and the last CTA to finish adds them in split order — deterministic, no second kernel.
+// few MACs each, so the kernel is a TMA stream with light tensor-core work on top:
+//   * unit of work = one 64-row group (4 m16 tiles, rows of one V-block) x one stage of 16 k-steps
+//     (128 blocks): the A_n tile [64 x 256 values], its A_i2 tile [64 x 16 words], the X^T channels of those
+//     128 blocks [128 M x TP tokens] and the 128 A_i1 words arrive by TMA / bulk copy into a 3-deep ring
+//     (one producer warp);
+//   * warp-level sparse MMA (mma.sp::ordered_metadata m16n8k32, bf16 -> fp32): A_n already IS the
+//     2:4-compressed operand (2 values per block = per group of 4 gathered channels, App. A) and the
+//     A_i2 word of a row is its metadata (thread 4g + c, c < 2: half c of rows g and g+8); the B fragment
+//     gathers the 4 kept channels of each block (A_i1) from the staged X^T slice;
+//   * 4 consumer warps, one m16 tile each, so no cross-warp reduction; persistent CTAs take equal shares of
+//     the (row group, stage) list (stream-K); a row group cut between CTAs is finished by the last CTA to
+//     arrive, which adds the fp32 partials in stage order (deterministic, no second kernel).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -26,22 +28,25 @@
 namespace vnm {
 namespace {
 
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kRows = 64;  // rows per CTA (4 m16 tiles)
+constexpr int kCons = 4;                  // consumer warps (one m16 tile each)
+constexpr int kThreads = 32 * (kCons + 1);
+constexpr int kRows = 64;                 // rows per group (4 m16 tiles)
+constexpr int kKS = 16;                   // k-steps (8 blocks each) per stage
+constexpr int kStages = 3;
+constexpr uint32_t kABytes = kRows * kKS * 16 * 2;  // 64 rows x 256 values bf16 = 32 KB
+constexpr uint32_t kMBytes = kRows * kKS * 4;       // 64 rows x 16 words = 4 KB
+constexpr uint32_t kCBytes = kKS * 8 * 4;           // 128 A_i1 words = 512 B
 
 struct DecArgs {
-    const uint16_t* XT;
-    int64_t ldx;
-    const uint16_t* values;
     const uint8_t* col_idx;
-    const uint32_t* meta;
     void* YT;
     int64_t ldy;
-    float* ws;          // [splits][rows_p][16] fp32 partials (splits > 1)
-    uint32_t* tickets;  // [n_rg] arrival counters (splits > 1), zeroed by the launch
-    int32_t T, y_bf16, rows, cols, V, M, nb_pad, ld_val, ld_meta;
-    int32_t n_ks, splits, ks_per;  // k-steps (8 blocks each), K splits, k-steps per split
+    float* ws;          // [n_rg][n_st][64][16] fp32 partials of cut row groups
+    uint32_t* tickets;  // [n_rg] arrival counters, zeroed by the launch
+    int32_t T, y_bf16, rows, V, M, nb_pad, n_ks;
+    int32_t n_rg, n_st, units, grid;
+    int32_t xrows;      // X^T rows staged per stage (multiple of 256 >= 128 M)
+    uint32_t x_bytes, stage_bytes;
 };
 
 __device__ __forceinline__ void mma_sp_16832(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t e) {
@@ -52,173 +57,178 @@ __device__ __forceinline__ void mma_sp_16832(float (&d)[4], const uint32_t (&a)[
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(e));
 }
 
-__device__ __forceinline__ uint32_t ldg_nc(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
+__device__ __forceinline__ int unit_owner(const DecArgs& a, int u) {  // CTA whose share contains unit u
+    return static_cast<int>((static_cast<long long>(u + 1) * a.grid - 1) / a.units);
 }
 
-// NT8 = token tiles of 8 (1: T <= 8, 2: T <= 16)
 template <int NT8>
-__global__ void __launch_bounds__(kThreads) vnm_spmm_dec_kernel(const DecArgs a) {
+__global__ void __launch_bounds__(kThreads, 1)
+    vnm_spmm_dec_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_m,
+                        const __grid_constant__ CUtensorMap tm_x, const DecArgs a) {
     constexpr int TP = 8 * NT8;  // tokens held per X^T channel in shared memory
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int rg = blockIdx.x / a.splits, sp = blockIdx.x % a.splits;
-    const int ks0 = sp * a.ks_per, ks1 = min(a.n_ks, ks0 + a.ks_per);
-    const int nks = max(ks1 - ks0, 0);
-    const int row0 = rg * kRows, vb = row0 / a.V;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, c = lane % 4;
-    const int M = a.M, ch0 = ks0 * 8 * M, nch = nks * 8 * M;
-
-    uint16_t* sX = reinterpret_cast<uint16_t*>(smem);                       // [nch][TP] bf16
-    uint32_t* sC = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(a.ks_per) * 8 * M * TP * 2);  // [nks*8]
-    float* sP = reinterpret_cast<float*>(sC + a.ks_per * 8);                 // [kWarps][kRows][TP] partials
-
-    // ---- stage this CTA's X^T slice (zero past cols / T) and its A_i1 words
-    {
-        const int cpr = TP / 8;  // 16-byte chunks per channel row
-        for (int i = threadIdx.x; i < nch * cpr; i += kThreads) {
-            const int r = i / cpr, q = i % cpr, ch = ch0 + r, t = 8 * q;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (ch < a.cols && t < a.T) {
-                const uint16_t* src = a.XT + static_cast<int64_t>(ch) * a.ldx + t;
-                if (t + 8 <= a.T) {
-                    v = *reinterpret_cast<const uint4*>(src);
-                } else {
-                    uint16_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    for (int k = 0; k < a.T - t; ++k) h[k] = src[k];
-                    v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-                }
-            }
-            *reinterpret_cast<uint4*>(sX + r * TP + t) = v;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    __shared__ uint32_t last_flag;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int u0 = static_cast<int>(static_cast<long long>(blockIdx.x) * a.units / a.grid);
+    const int u1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * a.units / a.grid);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kCons);
         }
-        const uint32_t* ci = reinterpret_cast<const uint32_t*>(a.col_idx) + static_cast<int64_t>(vb) * a.nb_pad + ks0 * 8;
-        for (int i = threadIdx.x; i < nks * 8; i += kThreads) sC[i] = ci[i];
+        fence_mbar_init();
     }
     __syncthreads();
 
-    float acc[4][NT8][4];
+    if (warp == kCons) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_a);
+            tma_prefetch_desc(&tm_m);
+            tma_prefetch_desc(&tm_x);
+            for (int u = u0, q = 0; u < u1; ++u, ++q) {
+                const int rg = u / a.n_st, st = u % a.n_st, s = q % kStages;
+                mbar_wait(&empty[s], ((q / kStages) & 1) ^ 1);
+                uint8_t* base = smem + s * a.stage_bytes;
+                const int nblk = min(kKS * 8, a.nb_pad - st * kKS * 8);  // A_i1 words of this stage
+                mbar_arrive_expect_tx(&full[s], kABytes + kMBytes + a.x_bytes + 4 * nblk);
+                tma_load_2d(base, &tm_a, st * kKS * 16, rg * kRows, &full[s]);
+                tma_load_2d(base + kABytes, &tm_m, st * kKS, rg * kRows, &full[s]);
+                for (int x = 0; x < a.xrows; x += 256)
+                    tma_load_2d(base + kABytes + kMBytes + x * TP * 2, &tm_x, 0, st * kKS * 8 * a.M + x, &full[s]);
+                const int vb = rg * kRows / a.V;
+                bulk_load(base + kABytes + kMBytes + a.x_bytes,
+                          a.col_idx + (static_cast<int64_t>(vb) * a.nb_pad + st * kKS * 8) * 4, 4 * nblk, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers: warp w = m16 tile w
+    const int g = lane / 4, c = lane % 4, t = warp;
+    // kCh independent accumulator chains (k-step ks feeds chain ks % kCh) so consecutive MMAs do not wait on
+    // each other; the chains are added in a fixed order at the end of a piece
+    constexpr int kCh = 4;
+    float acc[NT8][4], ch[kCh][NT8][4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+    for (int n = 0; n < NT8; ++n)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            acc[n][k] = 0.f;
+#pragma unroll
+            for (int j = 0; j < kCh; ++j) ch[j][n][k] = 0.f;
+        }
+
+    auto store_y = [&](int r, int tk, float v) {
+        if (r < a.rows && tk < a.T) {
+            if (a.y_bf16)
+                reinterpret_cast<__nv_bfloat16*>(a.YT)[static_cast<int64_t>(r) * a.ldy + tk] = __float2bfloat16_rn(v);
+            else
+                reinterpret_cast<float*>(a.YT)[static_cast<int64_t>(r) * a.ldy + tk] = v;
+        }
+    };
+    auto flush = [&](int rg, int st0, bool whole) {
+        // D fragment: d0,d1 = row 16t + g, tokens 8n + 2c, +1; d2,d3 = row 16t + g + 8
 #pragma unroll
         for (int n = 0; n < NT8; ++n)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) acc[t][n][k] = 0.f;
-
-    // row pointers of this thread's fragment rows (g, g + 8 of each m16 tile)
-    const uint32_t* vrow = reinterpret_cast<const uint32_t*>(a.values) + static_cast<int64_t>(row0 + g) * (a.ld_val / 2) + c;
-    const uint32_t* mrow = a.meta + static_cast<int64_t>(row0 + g) * a.ld_meta;
-    const int64_t v8 = 8 * static_cast<int64_t>(a.ld_val / 2), m8 = 8 * static_cast<int64_t>(a.ld_meta);
-
-    // A fragment of tile t, k-step s (compressed column j of the step = value j of block 8s + j/2):
-    // a0 = row g cols 2c,2c+1; a1 = row g+8 cols 2c,2c+1; a2 = row g cols 2c+8,+9; a3 = row g+8 cols 2c+8,+9
-    auto load_a = [&](int s, uint32_t (&A)[4][4], uint32_t (&E)[4]) {
+            for (int k = 0; k < 4; ++k) {
+                acc[n][k] = (ch[0][n][k] + ch[1][n][k]) + (ch[2][n][k] + ch[3][n][k]);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const uint32_t* p = vrow + 16 * t * (a.ld_val / 2) + 8 * s;
-            A[t][0] = ldg_nc(p);
-            A[t][1] = ldg_nc(p + v8);
-            A[t][2] = ldg_nc(p + 4);
-            A[t][3] = ldg_nc(p + v8 + 4);
-            // metadata (selector 0): thread c = 0 / 1 of each quad carries K-groups 0-3 / 4-7 (halfword c of the
-            // A_i2 word) of row g in bits 0-15 and of row g + 8 in bits 16-31 (verified on B200 against the
-            // oracle; the same pairing as the tcgen05 M = 128 layout, profiles/r01_probes.md MB1)
-            const uint32_t* q = mrow + 16 * t * a.ld_meta + s;
-            const uint32_t w0 = ldg_nc(q), w1 = ldg_nc(q + m8);
-            const int h = 16 * (c & 1);
-            E[t] = ((w0 >> h) & 0xFFFFu) | (((w1 >> h) & 0xFFFFu) << 16);
+                for (int j = 0; j < kCh; ++j) ch[j][n][k] = 0.f;
+                const int rl = 16 * t + g + 8 * (k >> 1), tk = 8 * n + 2 * c + (k & 1);
+                if (whole)
+                    store_y(rg * kRows + rl, tk, acc[n][k]);
+                else
+                    a.ws[((static_cast<int64_t>(rg) * a.n_st + st0) * kRows + rl) * 16 + tk] = acc[n][k];
+                acc[n][k] = 0.f;
+            }
+    };
+    // a cut row group: publish, and the last CTA to arrive adds the pieces in stage order
+    auto finish_cut = [&](int rg) {
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons));
+        const int first = unit_owner(a, rg * a.n_st), last = unit_owner(a, rg * a.n_st + a.n_st - 1);
+        if (threadIdx.x == 0) last_flag = atomicAdd(&a.tickets[rg], 1u) == static_cast<uint32_t>(last - first);
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons));
+        if (!last_flag) return;
+        __threadfence();
+        for (int i = threadIdx.x; i < kRows * TP; i += 32 * kCons) {
+            const int r = i / TP, tk = i % TP;
+            float v = 0.f;
+            for (int cta = first; cta <= last; ++cta) {
+                const int ub = static_cast<int>(static_cast<long long>(cta) * a.units / a.grid);
+                const int st0 = max(ub, rg * a.n_st) - rg * a.n_st;
+                v += __ldcg(a.ws + ((static_cast<int64_t>(rg) * a.n_st + st0) * kRows + r) * 16 + tk);
+            }
+            store_y(rg * kRows + r, tk, v);
         }
+        if (threadIdx.x == 0) a.tickets[rg] = 0;  // ready for the next call (stream order)
     };
 
-    // B fragment of k-step s (k = 2c + 8r + {0, 1} -> block c/2 + 2r, A_i1 positions 2(c%2), 2(c%2) + 1),
-    // then the 4 x NT8 MMAs of the step
-    auto step = [&](int s, const uint32_t (&A)[4][4], const uint32_t (&E)[4]) {
-        const int ls = s - ks0;
-        uint32_t B[NT8][4];
+    int piece_st0 = u0 < u1 ? u0 % a.n_st : 0;
+    for (int u = u0, q = 0; u < u1; ++u, ++q) {
+        const int rg = u / a.n_st, st = u % a.n_st, s = q % kStages;
+        mbar_wait(&full[s], (q / kStages) & 1);
+        const uint8_t* base = smem + s * a.stage_bytes;
+        const uint32_t* sA = reinterpret_cast<const uint32_t*>(base);                                   // [64][128]
+        const uint32_t* sM = reinterpret_cast<const uint32_t*>(base + kABytes);                         // [64][16]
+        const uint16_t* sX = reinterpret_cast<const uint16_t*>(base + kABytes + kMBytes);               // [xrows][TP]
+        const uint32_t* sC = reinterpret_cast<const uint32_t*>(base + kABytes + kMBytes + a.x_bytes);  // [128]
+        const int nks = min(kKS, a.n_ks - st * kKS);
+        const uint32_t* arow = sA + (16 * t + g) * (kKS * 8) + c;
+        const uint32_t* mrow = sM + (16 * t + g) * kKS;
+        const int h = 16 * (c & 1);
+        auto kstep = [&](int ks, float (&cc)[NT8][4]) {
+            // A fragment (compressed column j of the step = value j of block 8 ks + j/2 of the stage)
+            uint32_t A[4];
+            A[0] = arow[8 * ks];
+            A[1] = arow[8 * ks + 8 * kKS * 8];
+            A[2] = arow[8 * ks + 4];
+            A[3] = arow[8 * ks + 8 * kKS * 8 + 4];
+            const uint32_t w0 = mrow[ks], w1 = mrow[ks + 8 * kKS];
+            const uint32_t E = ((w0 >> h) & 0xFFFFu) | (((w1 >> h) & 0xFFFFu) << 16);
+            // B fragment: k = 2c + 8r + {0,1} -> block c/2 + 2r of the step, A_i1 positions 2(c%2), 2(c%2)+1
+            uint32_t B[NT8][4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int blk = c / 2 + 2 * r;
-            const uint32_t cw = sC[ls * 8 + blk] >> (16 * (c & 1));
-            const int base = (ls * 8 + blk) * M;
-            const uint16_t* x0 = sX + (base + (cw & 0xFF)) * TP + g;
-            const uint16_t* x1 = sX + (base + ((cw >> 8) & 0xFF)) * TP + g;
+            for (int r = 0; r < 4; ++r) {
+                const int blk = ks * 8 + c / 2 + 2 * r;
+                const uint32_t cw = sC[blk] >> h;
+                const uint16_t* x0 = sX + (blk * a.M + (cw & 0xFF)) * TP + g;
+                const uint16_t* x1 = sX + (blk * a.M + ((cw >> 8) & 0xFF)) * TP + g;
 #pragma unroll
-            for (int n = 0; n < NT8; ++n) B[n][r] = static_cast<uint32_t>(x0[8 * n]) | (static_cast<uint32_t>(x1[8 * n]) << 16);
+                for (int n = 0; n < NT8; ++n) B[n][r] = static_cast<uint32_t>(x0[8 * n]) | (static_cast<uint32_t>(x1[8 * n]) << 16);
+            }
+#pragma unroll
+            for (int n = 0; n < NT8; ++n) mma_sp_16832(cc[n], A, B[n], E);
+        };
+        if (nks == kKS) {
+#pragma unroll
+            for (int ks = 0; ks < kKS; ++ks) kstep(ks, ch[ks % kCh]);
+        } else {
+            for (int ks = 0; ks < nks; ks += kCh) {
+#pragma unroll
+                for (int j = 0; j < kCh; ++j)
+                    if (ks + j < nks) kstep(ks + j, ch[j]);
+            }
         }
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int n = 0; n < NT8; ++n) mma_sp_16832(acc[t][n], A[t], B[n], E[t]);
-    };
-
-    // warp w takes k-steps ks0 + w, + 4, ...; A of the next step is in flight while this one computes
-    uint32_t A0[4][4], E0[4], A1[4][4], E1[4];
-    int s = ks0 + warp;
-    if (s < ks1) load_a(s, A0, E0);
-    for (; s < ks1; s += 2 * kWarps) {
-        if (s + kWarps < ks1) load_a(s + kWarps, A1, E1);
-        step(s, A0, E0);
-        if (s + kWarps >= ks1) break;
-        if (s + 2 * kWarps < ks1) load_a(s + 2 * kWarps, A0, E0);
-        step(s + kWarps, A1, E1);
-    }
-
-    // ---- warp partials -> shared, added in warp order
-    // D fragment: d0,d1 = row g, tokens 2c, 2c+1; d2,d3 = row g+8
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-        for (int n = 0; n < NT8; ++n) {
-            float* p = sP + (warp * kRows + 16 * t + g) * TP + 8 * n + 2 * c;
-            p[0] = acc[t][n][0];
-            p[1] = acc[t][n][1];
-            p[8 * TP] = acc[t][n][2];
-            p[8 * TP + 1] = acc[t][n][3];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // end of a piece: the row group changes or the share ends
+        if (st == a.n_st - 1 || u + 1 == u1) {
+            const bool whole = piece_st0 == 0 && st == a.n_st - 1;
+            flush(rg, piece_st0, whole);
+            if (!whole) finish_cut(rg);
+            piece_st0 = 0;
         }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kRows * TP; i += kThreads) {
-        float v = sP[i];
-#pragma unroll
-        for (int w = 1; w < kWarps; ++w) v += sP[w * kRows * TP + i];
-        sP[i] = v;
     }
-    __syncthreads();
-
-    auto store_y = [&](int i, float v) {
-        const int r = row0 + i / TP, t = i % TP;
-        if (r >= a.rows || t >= a.T) return;
-        if (a.y_bf16)
-            reinterpret_cast<__nv_bfloat16*>(a.YT)[static_cast<int64_t>(r) * a.ldy + t] = __float2bfloat16_rn(v);
-        else
-            reinterpret_cast<float*>(a.YT)[static_cast<int64_t>(r) * a.ldy + t] = v;
-    };
-    if (a.splits == 1) {
-        for (int i = threadIdx.x; i < kRows * TP; i += kThreads) store_y(i, sP[i]);
-        return;
-    }
-    // ---- split-K: publish this split's partial; the last CTA of the row group adds all splits in order
-    float* wsp = a.ws + (static_cast<int64_t>(sp) * a.rows + row0) * 16;
-    for (int i = threadIdx.x; i < kRows * TP; i += kThreads)
-        if (row0 + i / TP < a.rows) wsp[(i / TP) * 16 + i % TP] = sP[i];
-    __threadfence();
-    __syncthreads();
-    __shared__ uint32_t last;
-    if (threadIdx.x == 0) last = atomicAdd(&a.tickets[rg], 1u) == static_cast<uint32_t>(a.splits - 1);
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    for (int i = threadIdx.x; i < kRows * TP; i += kThreads) {
-        if (row0 + i / TP >= a.rows) continue;
-        float v = 0.f;
-        for (int q = 0; q < a.splits; ++q)
-            v += __ldcg(a.ws + (static_cast<int64_t>(q) * a.rows + row0 + i / TP) * 16 + i % TP);
-        store_y(i, v);
-    }
-    if (threadIdx.x == 0) a.tickets[rg] = 0;  // ready for the next call (same stream order)
 }
 
 struct DecPlan {
-    int n_rg, n_ks, splits, ks_per;
+    int n_rg, n_ks, n_st, units, grid, tp, xrows;
+    uint32_t x_bytes, stage_bytes;
     size_t smem;
 };
 
@@ -226,32 +236,28 @@ DecPlan make_plan(const vnm_geom& g, int T) {
     DecPlan p;
     p.n_rg = g.rows_p / kRows;
     p.n_ks = g.nb_pad / 8;
-    const int tp = T <= 8 ? 8 : 16;
-    // enough CTAs for ~4 per SM, while one CTA's X^T slice stays <= 40 KB
-    int splits = (4 * num_sms() + p.n_rg - 1) / p.n_rg;
-    const int per_ks = 8 * g.M * tp * 2;
-    const int min_splits = (p.n_ks * per_ks + 40 * 1024 - 1) / (40 * 1024);
-    if (splits < min_splits) splits = min_splits;
-    if (splits > p.n_ks) splits = p.n_ks;
-    if (splits < 1) splits = 1;
-    p.ks_per = (p.n_ks + splits - 1) / splits;
-    p.splits = (p.n_ks + p.ks_per - 1) / p.ks_per;
-    p.smem = static_cast<size_t>(p.ks_per) * per_ks + static_cast<size_t>(p.ks_per) * 8 * 4 +
-             static_cast<size_t>(kWarps) * kRows * tp * 4;
+    p.n_st = (p.n_ks + kKS - 1) / kKS;
+    p.units = p.n_rg * p.n_st;
+    p.grid = p.units < num_sms() ? p.units : num_sms();
+    p.tp = T <= 8 ? 8 : 16;
+    p.xrows = (kKS * 8 * g.M + 255) / 256 * 256;
+    p.x_bytes = static_cast<uint32_t>(p.xrows * p.tp * 2);
+    p.stage_bytes = (kABytes + kMBytes + p.x_bytes + kCBytes + 127) / 128 * 128;
+    p.smem = static_cast<size_t>(kStages) * p.stage_bytes + 128;
     return p;
 }
 
 }  // namespace
 
 bool spmm_dec_applies(const vnm_geom& g, int32_t T) {
-    return T >= 1 && T <= 16 && g.V >= 64 && g.nb_pad > 0 && g.rows_p % kRows == 0;
+    return T >= 1 && T <= 16 && g.V >= 64 && g.M <= 8 && g.nb_pad > 0 && g.rows_p % kRows == 0 &&
+           make_plan(g, T).smem <= kMaxSmem;
 }
 
 size_t spmm_dec_workspace_bytes(const vnm_geom& g, int32_t T) {
     if (!spmm_dec_applies(g, T)) return 0;
     const DecPlan p = make_plan(g, T);
-    if (p.splits == 1) return 0;
-    const size_t ws = static_cast<size_t>(p.splits) * g.rows * 16 * 4;
+    const size_t ws = static_cast<size_t>(p.n_rg) * p.n_st * kRows * 16 * 4;
     return (ws + 255) / 256 * 256 + static_cast<size_t>(p.n_rg) * 4;
 }
 
@@ -259,39 +265,43 @@ int launch_spmm_dec(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
     if (!spmm_dec_applies(g, L.T)) return kLaunchUnsupported;
     const DecPlan p = make_plan(g, L.T);
+    const size_t need = spmm_dec_workspace_bytes(g, L.T);
+    if (!L.workspace || L.workspace_bytes < need) return kLaunchUnsupported;
     DecArgs a;
-    a.XT = L.XT;
-    a.ldx = L.ldx;
-    a.values = L.P->values;
     a.col_idx = L.P->col_idx;
-    a.meta = L.P->meta;
     a.YT = L.YT;
     a.ldy = L.ldy;
+    a.ws = static_cast<float*>(L.workspace);
+    a.tickets = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(L.workspace) + (need - static_cast<size_t>(p.n_rg) * 4));
     a.T = L.T;
     a.y_bf16 = L.y_dtype == VNM_BF16;
     a.rows = g.rows;
-    a.cols = g.cols;
     a.V = g.V;
     a.M = g.M;
     a.nb_pad = g.nb_pad;
-    a.ld_val = g.ld_val;
-    a.ld_meta = g.ld_meta;
     a.n_ks = p.n_ks;
-    a.splits = p.splits;
-    a.ks_per = p.ks_per;
-    a.ws = nullptr;
-    a.tickets = nullptr;
-    if (p.splits > 1) {
-        const size_t need = spmm_dec_workspace_bytes(g, L.T);
-        if (!L.workspace || L.workspace_bytes < need) return kLaunchUnsupported;
-        a.ws = static_cast<float*>(L.workspace);
-        a.tickets = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(L.workspace) + (need - static_cast<size_t>(p.n_rg) * 4));
-        cudaMemsetAsync(a.tickets, 0, static_cast<size_t>(p.n_rg) * 4, stream);
-    }
+    a.n_rg = p.n_rg;
+    a.n_st = p.n_st;
+    a.units = p.units;
+    a.grid = p.grid;
+    a.xrows = p.xrows;
+    a.x_bytes = p.x_bytes;
+    a.stage_bytes = p.stage_bytes;
+    CUtensorMap ta, tmm, tx;
+    if (!encode_2d(&ta, L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
+                   static_cast<uint64_t>(g.ld_val) * 2, kKS * 16, kRows, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_2d(&tmm, L.P->meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
+                   static_cast<uint64_t>(g.ld_meta) * 4, kKS, kRows, CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                   CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_2d(&tx, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
+                   p.tp, 256, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return kLaunchCudaError;
+    cudaMemsetAsync(a.tickets, 0, static_cast<size_t>(p.n_rg) * 4, stream);
     auto k = L.T <= 8 ? vnm_spmm_dec_kernel<1> : vnm_spmm_dec_kernel<2>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)) != cudaSuccess)
         return kLaunchCudaError;
-    k<<<p.n_rg * p.splits, kThreads, p.smem, stream>>>(a);
+    k<<<p.grid, kThreads, p.smem, stream>>>(ta, tmm, tx, a);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }

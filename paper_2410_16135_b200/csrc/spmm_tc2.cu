@@ -53,9 +53,6 @@ struct Tc2Args {
     int32_t y_slots;     // epilogue staging slots per warp (1 or 2)
     uint32_t b_bytes, stage_bytes, res_bytes;
     int32_t trace;       // VNM_SPMM_TRACE: per-CTA wait / busy cycle counters into g_tc2_t
-    int32_t stg;         // bf16 epilogue: 1 = 16-byte global stores from registers (no shared staging)
-    void* YT;
-    int64_t ldy;
 };
 
 // VNM_SPMM_TRACE counters per CTA: MMA wait full, MMA wait tmem_empty, MMA loop total, producer wait empty,
@@ -289,28 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                 }
                 c0 = clock64();
                 c_drain += c0 - c1;
-                if (store) {
-                    if (a.stg) {
-                        // each lane owns one output row: 8 x 16 B straight to global (full 128-byte lines land
-                        // in L2 before they are written back); rows >= rows / tokens >= T are skipped
-                        const int row = rt * 128 + 32 * qd + lane;
-                        if (row < a.rows) {
-                            __nv_bfloat16* yr = reinterpret_cast<__nv_bfloat16*>(a.YT) + static_cast<int64_t>(row) * a.ldy + t0;
-                            if (t0 + 64 <= a.T) {
-#pragma unroll
-                                for (int k = 0; k < 8; ++k)
-                                    *reinterpret_cast<uint4*>(yr + 8 * k) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                            } else {
-                                for (int k = 0; k < 32 && t0 + 2 * k < a.T; ++k) {
-                                    reinterpret_cast<uint16_t*>(yr)[2 * k] = static_cast<uint16_t>(pk[k]);
-                                    if (t0 + 2 * k + 1 < a.T) reinterpret_cast<uint16_t*>(yr)[2 * k + 1] = static_cast<uint16_t>(pk[k] >> 16);
-                                }
-                            }
-                        }
-                    } else {
-                        stage_store(buf, 1, 0, lane, pk, &tmap_y, t0, rt * 128 + 32 * qd);
-                    }
-                }
+                if (store) stage_store(buf, 1, 0, lane, pk, &tmap_y, t0, rt * 128 + 32 * qd);
                 c_store += clock64() - c0;
             } else {
                 // fp32 (parity path): two 32-token chunks straight from TMEM; release at the end
@@ -398,10 +374,6 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
         pairs = a.work;
     }
     a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
-    a.YT = L.YT;
-    a.ldy = L.ldy;
-    a.stg = 0;
-    if (const char* e = getenv("VNM_TC2_STG")) a.stg = atoi(e);
     k<<<2 * pairs, C::kThreads, smem, stream>>>(ta, tb, te, ty, a);
     count_launch();
     cudaError_t e = cudaGetLastError();

@@ -90,3 +90,23 @@ def test_no_cpu_path():
     W = torch.zeros(128, 64, dtype=torch.bfloat16)
     with pytest.raises(ValueError):
         vnm.prune(W, 64, 8)
+
+
+def test_ria_argument_errors():
+    """vnm_act_norms / vnm_ria_score reject bad arguments on the host, before any launch (NEXT-2)."""
+    L = vnm.lib()
+    assert L.vnm_ria_workspace_bytes(-1, 4) == 0
+    assert L.vnm_ria_workspace_bytes(64, 512) == (1 * 512 + 1 * 64 + 2 * 512 + 64) * 4
+    P = ctypes.c_void_p
+    # negative shape, ld < cols, negative exponent
+    assert L.vnm_ria_score(P(16), 8, -1, 4, None, 0.5, P(16), 8, P(16), 1 << 20, None) == vnm.VNM_ERR_SHAPE
+    assert L.vnm_ria_score(P(16), 2, 4, 4, None, 0.5, P(16), 8, P(16), 1 << 20, None) == vnm.VNM_ERR_SHAPE
+    assert L.vnm_ria_score(P(16), 8, 4, 4, None, -1.0, P(16), 8, P(16), 1 << 20, None) == vnm.VNM_ERR_SHAPE
+    # missing workspace / too small, misaligned pointers
+    assert L.vnm_ria_score(P(16), 8, 4, 4, None, 0.5, P(16), 8, None, 0, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_ria_score(P(16), 8, 4, 4, None, 0.5, P(16), 8, P(16), 8, None) == vnm.VNM_ERR_SHAPE
+    assert L.vnm_ria_score(P(18), 8, 4, 4, None, 0.5, P(16), 8, P(16), 1 << 20, None) == vnm.VNM_ERR_ALIGN
+    assert L.vnm_ria_score(P(16), 8, 0, 4, None, 0.5, None, 8, None, 0, None) == vnm.VNM_OK
+    assert L.vnm_act_norms(P(16), 4, 3, 8, P(16), None) == vnm.VNM_ERR_SHAPE  # ldx < T
+    assert L.vnm_act_norms(P(16), 8, 3, 8, None, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_act_norms(P(18), 8, 3, 8, P(16), None) == vnm.VNM_ERR_ALIGN
