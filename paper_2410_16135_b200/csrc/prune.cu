@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) prune_pack_kernel(const PruneArgs a)
     uint8_t* sNib = p;
     p += static_cast<size_t>(RT) * CB;
     // window form staging (only when a.values_tc): 4 values and a nibble pair per row-block
-    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    p = smem + ((p - smem + 15) & ~static_cast<ptrdiff_t>(15));  // 16-B aligned, still a shared pointer
     uint16_t* sTcv = reinterpret_cast<uint16_t*>(p);
     p += static_cast<size_t>(RT) * 4 * CB * 2;
     uint8_t* sTcn = p;

@@ -199,8 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const SpmmArgs a) {
     using C = Cfg<NT>;
     constexpr int S = C::kStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];  // (not re-aligned through an integer: keeps LDS/STS)
     uint8_t* sA = smem;
     uint8_t* sB = smem + S * kABytes;
     uint32_t* sMeta = reinterpret_cast<uint32_t*>(sB + S * C::kBBytes);  // [S][64][4]

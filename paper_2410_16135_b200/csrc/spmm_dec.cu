@@ -11,9 +11,13 @@
 //     2:4-compressed operand (2 values per block = per group of 4 gathered channels, App. A) and the
 //     A_i2 word of a row is its metadata (thread 4g + c, c < 2: half c of rows g and g+8); the B fragment
 //     gathers the 4 kept channels of each block (A_i1) from the staged X^T slice;
-//   * 4 consumer warps, one m16 tile each, so no cross-warp reduction; persistent CTAs take equal shares of
-//     the (row group, stage) list (stream-K); a row group cut between CTAs is finished by the last CTA to
-//     arrive, which adds the fp32 partials in stage order (deterministic, no second kernel).
+//   * 16 consumer warps: warp w owns m16 tile w % 4 and the k-steps = w / 4 (mod 4) of every stage (one warp
+//     per tile left every SM sub-partition with a single dependent chain: 2.7 us per stage, measured); the
+//     4 partials of a tile are added in warp order through shared memory at the end of a row group; A_n tiles
+//     arrive as 128-byte-swizzled TMA boxes so the 8 rows of a fragment hit 8 different bank groups;
+//   * persistent CTAs take equal shares of the (row group, stage) list (stream-K); a row group cut between
+//     CTAs is finished by the last CTA to arrive, which adds the fp32 partials in stage order
+//     (deterministic, no second kernel).
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -28,12 +32,12 @@
 namespace vnm {
 namespace {
 
-constexpr int kCons = 4;                  // consumer warps (one m16 tile each)
+constexpr int kCons = 16;                 // consumer warps: m16 tile w % 4, k-steps = w / 4 (mod 4)
 constexpr int kThreads = 32 * (kCons + 1);
 constexpr int kRows = 64;                 // rows per group (4 m16 tiles)
 constexpr int kKS = 16;                   // k-steps (8 blocks each) per stage
 constexpr int kStages = 3;
-constexpr uint32_t kABytes = kRows * kKS * 16 * 2;  // 64 rows x 256 values bf16 = 32 KB
+constexpr uint32_t kABytes = kRows * kKS * 16 * 2;  // 64 rows x 256 values bf16 = 32 KB (4 SW128 boxes of 64)
 constexpr uint32_t kMBytes = kRows * kKS * 4;       // 64 rows x 16 words = 4 KB
 constexpr uint32_t kCBytes = kKS * 8 * 4;           // 128 A_i1 words = 512 B
 
@@ -46,8 +50,18 @@ struct DecArgs {
     int32_t T, y_bf16, rows, V, M, nb_pad, n_ks;
     int32_t n_rg, n_st, units, grid;
     int32_t xrows;      // X^T rows staged per stage (multiple of 256 >= 128 M)
+    const uint16_t* XT; // dense X^T (ldx == TP): the stage's slice is one contiguous bulk copy
+    int32_t x_dense, cols;
     uint32_t x_bytes, stage_bytes;
+    int32_t trace;  // VNM_SPMM_TRACE: %globaltimer of CTA 0 per unit (issue, data ready, consumed)
 };
+
+__device__ unsigned long long g_dec_t[3][64];
+__device__ __forceinline__ unsigned long long dtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ void mma_sp_16832(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[4], uint32_t e) {
     asm volatile(
@@ -66,8 +80,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     vnm_spmm_dec_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_m,
                         const __grid_constant__ CUtensorMap tm_x, const DecArgs a) {
     constexpr int TP = 8 * NT8;  // tokens held per X^T channel in shared memory
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    // declared 1024-aligned (not re-aligned through an integer): the compiler then keeps plain loads from it
+    // as shared-memory loads (LDS) instead of generic ones
+    extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     __shared__ uint32_t last_flag;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -80,6 +95,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_mbar_init();
     }
+    if (a.x_dense) {  // X^T rows past cols are never copied in the dense path: they must read as zero
+        for (int s = 0; s < kStages; ++s) {
+            uint4* x4 = reinterpret_cast<uint4*>(smem + s * a.stage_bytes + kABytes + kMBytes);
+            for (int i = threadIdx.x; i < static_cast<int>(a.x_bytes / 16); i += blockDim.x) x4[i] = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async_smem();
+    }
     __syncthreads();
 
     if (warp == kCons) {
@@ -91,13 +113,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = u0, q = 0; u < u1; ++u, ++q) {
                 const int rg = u / a.n_st, st = u % a.n_st, s = q % kStages;
                 mbar_wait(&empty[s], ((q / kStages) & 1) ^ 1);
+                if (a.trace && blockIdx.x == 0 && q < 64) g_dec_t[0][q] = dtime();
                 uint8_t* base = smem + s * a.stage_bytes;
                 const int nblk = min(kKS * 8, a.nb_pad - st * kKS * 8);  // A_i1 words of this stage
-                mbar_arrive_expect_tx(&full[s], kABytes + kMBytes + a.x_bytes + 4 * nblk);
-                tma_load_2d(base, &tm_a, st * kKS * 16, rg * kRows, &full[s]);
+                const uint32_t xb = a.x_dense ? min(kKS * 8 * a.M, a.cols - st * kKS * 8 * a.M) * TP * 2 : a.x_bytes;
+                mbar_arrive_expect_tx(&full[s], kABytes + kMBytes + xb + 4 * nblk);
+                for (int b = 0; b < 4; ++b) tma_load_2d(base + b * 8192, &tm_a, st * kKS * 16 + 64 * b, rg * kRows, &full[s]);
                 tma_load_2d(base + kABytes, &tm_m, st * kKS, rg * kRows, &full[s]);
-                for (int x = 0; x < a.xrows; x += 256)
-                    tma_load_2d(base + kABytes + kMBytes + x * TP * 2, &tm_x, 0, st * kKS * 8 * a.M + x, &full[s]);
+                const int ch0 = st * kKS * 8 * a.M;
+                if (a.x_dense) {
+                    // rows [ch0, ch0 + 128 M) are contiguous: one bulk copy; the tail past cols is zeroed once
+                    // by the consumers at start (never overwritten: the copy length stops at cols)
+                    const int nr = min(kKS * 8 * a.M, a.cols - ch0);
+                    bulk_load(base + kABytes + kMBytes, a.XT + static_cast<int64_t>(ch0) * TP, nr * TP * 2, &full[s]);
+                } else {
+                    for (int x = 0; x < a.xrows; x += 256)
+                        tma_load_2d(base + kABytes + kMBytes + x * TP * 2, &tm_x, 0, ch0 + x, &full[s]);
+                }
                 const int vb = rg * kRows / a.V;
                 bulk_load(base + kABytes + kMBytes + a.x_bytes,
                           a.col_idx + (static_cast<int64_t>(vb) * a.nb_pad + st * kKS * 8) * 4, 4 * nblk, &full[s]);
@@ -106,19 +138,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         return;
     }
 
-    // ---------------------------------------------------------------- consumers: warp w = m16 tile w
-    const int g = lane / 4, c = lane % 4, t = warp;
-    // kCh independent accumulator chains (k-step ks feeds chain ks % kCh) so consecutive MMAs do not wait on
-    // each other; the chains are added in a fixed order at the end of a piece
-    constexpr int kCh = 4;
-    float acc[NT8][4], ch[kCh][NT8][4];
+    // ---------------------------------------------------------------- consumers
+    const int g = lane / 4, c = lane % 4, t = warp % 4, kq = warp / 4;
+    float* red = reinterpret_cast<float*>(smem + kStages * a.stage_bytes);  // [kCons][16 rows][16 tokens]
+    // two accumulator chains (alternate k-steps), added in a fixed order at the end of a piece
+    float acc[NT8][4], ch[2][NT8][4];
 #pragma unroll
     for (int n = 0; n < NT8; ++n)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             acc[n][k] = 0.f;
-#pragma unroll
-            for (int j = 0; j < kCh; ++j) ch[j][n][k] = 0.f;
+            ch[0][n][k] = 0.f;
+            ch[1][n][k] = 0.f;
         }
 
     auto store_y = [&](int r, int tk, float v) {
@@ -130,21 +161,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
     auto flush = [&](int rg, int st0, bool whole) {
-        // D fragment: d0,d1 = row 16t + g, tokens 8n + 2c, +1; d2,d3 = row 16t + g + 8
+        // this warp's partial of tile t -> shared; the kq = 0 warp of each tile adds the 4 in warp order
+        // D fragment: d0,d1 = row g, tokens 8n + 2c, +1; d2,d3 = row g + 8 (within the m16 tile)
 #pragma unroll
         for (int n = 0; n < NT8; ++n)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                acc[n][k] = (ch[0][n][k] + ch[1][n][k]) + (ch[2][n][k] + ch[3][n][k]);
-#pragma unroll
-                for (int j = 0; j < kCh; ++j) ch[j][n][k] = 0.f;
-                const int rl = 16 * t + g + 8 * (k >> 1), tk = 8 * n + 2 * c + (k & 1);
-                if (whole)
-                    store_y(rg * kRows + rl, tk, acc[n][k]);
-                else
-                    a.ws[((static_cast<int64_t>(rg) * a.n_st + st0) * kRows + rl) * 16 + tk] = acc[n][k];
-                acc[n][k] = 0.f;
+                red[(warp * 16 + g + 8 * (k >> 1)) * 16 + 8 * n + 2 * c + (k & 1)] = ch[0][n][k] + ch[1][n][k];
+                ch[0][n][k] = 0.f;
+                ch[1][n][k] = 0.f;
             }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons));
+        if (kq == 0) {
+#pragma unroll
+            for (int n = 0; n < NT8; ++n)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int rl = g + 8 * (k >> 1), tk = 8 * n + 2 * c + (k & 1);
+                    float v = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v += red[((t + 4 * j) * 16 + rl) * 16 + tk];
+                    if (whole)
+                        store_y(rg * kRows + 16 * t + rl, tk, v);
+                    else
+                        a.ws[((static_cast<int64_t>(rg) * a.n_st + st0) * kRows + 16 * t + rl) * 16 + tk] = v;
+                }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons));
     };
     // a cut row group: publish, and the last CTA to arrive adds the pieces in stage order
     auto finish_cut = [&](int rg) {
@@ -172,22 +215,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = u0, q = 0; u < u1; ++u, ++q) {
         const int rg = u / a.n_st, st = u % a.n_st, s = q % kStages;
         mbar_wait(&full[s], (q / kStages) & 1);
+        if (a.trace && blockIdx.x == 0 && q < 64 && threadIdx.x == 0) g_dec_t[1][q] = dtime();
         const uint8_t* base = smem + s * a.stage_bytes;
-        const uint32_t* sA = reinterpret_cast<const uint32_t*>(base);                                   // [64][128]
         const uint32_t* sM = reinterpret_cast<const uint32_t*>(base + kABytes);                         // [64][16]
         const uint16_t* sX = reinterpret_cast<const uint16_t*>(base + kABytes + kMBytes);               // [xrows][TP]
         const uint32_t* sC = reinterpret_cast<const uint32_t*>(base + kABytes + kMBytes + a.x_bytes);  // [128]
         const int nks = min(kKS, a.n_ks - st * kKS);
-        const uint32_t* arow = sA + (16 * t + g) * (kKS * 8) + c;
+        // A_n tile: 4 boxes [64 rows][64 values], 128-byte swizzle: 16-byte chunk q of row r sits at q ^ (r % 8)
+        const uint8_t* abox = base + (16 * t + g) * 128 + 4 * c;
         const uint32_t* mrow = sM + (16 * t + g) * kKS;
         const int h = 16 * (c & 1);
         auto kstep = [&](int ks, float (&cc)[NT8][4]) {
-            // A fragment (compressed column j of the step = value j of block 8 ks + j/2 of the stage)
+            // A fragment: words 8 ks + c (+4) of rows g, g + 8 = chunks 2 (ks % 4) (+1) of box ks / 4
+            const uint8_t* bp = abox + (ks >> 2) * 8192;
+            const int q0 = (2 * (ks & 3)) ^ g, q1 = (2 * (ks & 3) + 1) ^ g;  // (row + 8) % 8 == row % 8
             uint32_t A[4];
-            A[0] = arow[8 * ks];
-            A[1] = arow[8 * ks + 8 * kKS * 8];
-            A[2] = arow[8 * ks + 4];
-            A[3] = arow[8 * ks + 8 * kKS * 8 + 4];
+            A[0] = *reinterpret_cast<const uint32_t*>(bp + 16 * q0);
+            A[1] = *reinterpret_cast<const uint32_t*>(bp + 8 * 128 + 16 * q0);
+            A[2] = *reinterpret_cast<const uint32_t*>(bp + 16 * q1);
+            A[3] = *reinterpret_cast<const uint32_t*>(bp + 8 * 128 + 16 * q1);
             const uint32_t w0 = mrow[ks], w1 = mrow[ks + 8 * kKS];
             const uint32_t E = ((w0 >> h) & 0xFFFFu) | (((w1 >> h) & 0xFFFFu) << 16);
             // B fragment: k = 2c + 8r + {0,1} -> block c/2 + 2r of the step, A_i1 positions 2(c%2), 2(c%2)+1
@@ -204,18 +250,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int n = 0; n < NT8; ++n) mma_sp_16832(cc[n], A, B[n], E);
         };
-        if (nks == kKS) {
 #pragma unroll
-            for (int ks = 0; ks < kKS; ++ks) kstep(ks, ch[ks % kCh]);
-        } else {
-            for (int ks = 0; ks < nks; ks += kCh) {
-#pragma unroll
-                for (int j = 0; j < kCh; ++j)
-                    if (ks + j < nks) kstep(ks + j, ch[j]);
-            }
+        for (int i = 0; i < kKS / 4; ++i) {
+            const int ks = kq + 4 * i;
+            if (ks < nks) kstep(ks, ch[i & 1]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+        if (a.trace && blockIdx.x == 0 && q < 64 && threadIdx.x == 0) g_dec_t[2][q] = dtime();
         // end of a piece: the row group changes or the share ends
         if (st == a.n_st - 1 || u + 1 == u1) {
             const bool whole = piece_st0 == 0 && st == a.n_st - 1;
@@ -242,8 +284,8 @@ DecPlan make_plan(const vnm_geom& g, int T) {
     p.tp = T <= 8 ? 8 : 16;
     p.xrows = (kKS * 8 * g.M + 255) / 256 * 256;
     p.x_bytes = static_cast<uint32_t>(p.xrows * p.tp * 2);
-    p.stage_bytes = (kABytes + kMBytes + p.x_bytes + kCBytes + 127) / 128 * 128;
-    p.smem = static_cast<size_t>(kStages) * p.stage_bytes + 128;
+    p.stage_bytes = (kABytes + kMBytes + p.x_bytes + kCBytes + 1023) / 1024 * 1024;
+    p.smem = static_cast<size_t>(kStages) * p.stage_bytes + static_cast<size_t>(kCons) * 16 * 16 * 4 + 1024;
     return p;
 }
 
@@ -287,10 +329,13 @@ int launch_spmm_dec(const SpmmLaunch& L, cudaStream_t stream) {
     a.xrows = p.xrows;
     a.x_bytes = p.x_bytes;
     a.stage_bytes = p.stage_bytes;
+    a.XT = L.XT;
+    a.cols = g.cols;
+    a.x_dense = L.ldx == p.tp && (reinterpret_cast<uintptr_t>(L.XT) & 15u) == 0 ? 1 : 0;
     CUtensorMap ta, tmm, tx;
     if (!encode_2d(&ta, L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
-                   static_cast<uint64_t>(g.ld_val) * 2, kKS * 16, kRows, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                   CU_TENSOR_MAP_SWIZZLE_NONE) ||
+                   static_cast<uint64_t>(g.ld_val) * 2, 64, kRows, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   CU_TENSOR_MAP_SWIZZLE_128B) ||
         !encode_2d(&tmm, L.P->meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
                    static_cast<uint64_t>(g.ld_meta) * 4, kKS, kRows, CU_TENSOR_MAP_DATA_TYPE_UINT32,
                    CU_TENSOR_MAP_SWIZZLE_NONE) ||
@@ -301,8 +346,19 @@ int launch_spmm_dec(const SpmmLaunch& L, cudaStream_t stream) {
     auto k = L.T <= 8 ? vnm_spmm_dec_kernel<1> : vnm_spmm_dec_kernel<2>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)) != cudaSuccess)
         return kLaunchCudaError;
+    a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
     k<<<p.grid, kThreads, p.smem, stream>>>(ta, tmm, tx, a);
     count_launch();
+    if (a.trace) {
+        unsigned long long h[3][64];
+        cudaStreamSynchronize(stream);
+        cudaMemcpyFromSymbol(h, g_dec_t, sizeof(h));
+        const int n = static_cast<int>(static_cast<long long>(1) * p.units / p.grid);
+        fprintf(stderr, "dec: grid %d units %d (CTA 0: %d) stage %u B\n", p.grid, p.units, n, p.stage_bytes);
+        for (int q = 0; q < n && q < 64; ++q)
+            fprintf(stderr, "  unit %d: issue %llu ready %llu done %llu ns\n", q, h[0][q] - h[0][0], h[1][q] - h[0][0],
+                    h[2][q] - h[0][0]);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
 

@@ -179,8 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_x,
                          const PairArgs a) {
     const int S = a.ring;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];  // (not re-aligned through an integer: keeps LDS/STS)
     uint8_t* sA = smem;                       // [S][16384]  SW128
     uint8_t* sB = sA + S * kABytes;           // [B][16384]  SW128
     uint8_t* sE = sB + kBRing * kBBytes;      // [B][2048]   metadata images

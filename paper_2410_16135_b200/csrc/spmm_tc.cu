@@ -60,8 +60,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kChunks = NT / 64;
     constexpr int NACC = 2 * RT * NT + 16 * RT <= 512 ? 2 : 1;
     constexpr uint32_t kMetaCol = NACC * RT * NT;  // TMEM: accumulators, then 4 metadata columns per stage & tile
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];  // (not re-aligned through an integer: keeps LDS/STS)
     const int S = a.stages;
     // per stage: [A x RT][B chunks][E x RT]; then 4 epilogue staging buffers, then the barriers
     uint8_t* sY = smem + S * a.stage_bytes;

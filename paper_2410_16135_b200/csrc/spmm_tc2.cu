@@ -125,8 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
     using C = Cfg<NT>;
     constexpr int kNH = NT / 2;  // tokens per CTA of B
     constexpr uint32_t kMetaCol = C::kMetaCol;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem[];  // (not re-aligned through an integer: keeps LDS/STS)
     const int S = a.stages;
     // [resident A (n_stage x 16 KB) | resident E (n_stage x 2 KB)] (a_res only), ring, Y staging, barriers
     uint8_t* ring = smem + a.res_bytes;
