@@ -158,6 +158,22 @@ size_t vnm_ria_workspace_bytes(int32_t rows, int32_t cols);
 vnm_status vnm_ria_score(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const float* act_norms, float a,
                          float* score, int64_t lds, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
 
+/* ---- Channel-permutation gain scores: the cost matrix of the linear sum assignment
+ * that approximates the input-permutation step of the V:N:M-specific channel permutation, Eq. (7)
+ * `eq:admm1` (§4.2; "approximately modeled as the traditional linear sum assignment
+ * problem").  The Hungarian solve stays with the caller (host).
+ *   cost[j][b*M + s] = sum over the V-row stripes of the retained score that input channel j contributes when
+ *   it replaces the occupant of slot s of column block b (every other column frozen) and the block is
+ *   re-pruned by S_{V:N:M} (same tie rules and fp32 L1 tree as vnm_prune); "contributes" = the sum
+ *   of e_j = |score[.][j]| over the rows that keep slot s (reading Q22).  With the identity
+ *   assignment the costs add up to the retained score of the pruned matrix.
+ *   score fp32 [g->rows][lds] (4-B aligned), cost fp32 [g->cols_p][ldc], ldc >= cols_p (caller-owned);
+ *   workspace >= vnm_permute_gain_workspace_bytes(g), 16-B aligned.  V <= 64 and M <= 8
+ *   (VNM_ERR_UNSUPPORTED otherwise).  Deterministic (fp32 sums in stripe order).                         */
+size_t vnm_permute_gain_workspace_bytes(const vnm_geom* g);
+vnm_status vnm_permute_gain(const float* score, int64_t lds, const vnm_geom* g, float* cost, int64_t ldc,
+                            void* workspace, size_t workspace_bytes, vnm_stream_t stream);
+
 /* Human-readable text of a status (static storage).                                                   */
 const char* vnm_status_string(vnm_status s);
 

@@ -68,6 +68,7 @@ def lib():
             L.vnmo_retained_score.restype = ctypes.c_double
             L.vnmo_act_norms.argtypes = [P, i64, i32, i32, P]
             L.vnmo_ria.argtypes = [P, i64, i32, i32, P, ctypes.c_double, P, i64, P]
+            L.vnmo_permute_gain.argtypes = [P, i64, i32, i32, i32, i32, P]
             _lib = L
     return _lib
 
@@ -236,3 +237,18 @@ def ria(W: np.ndarray, act: np.ndarray | None = None, a: float = 0.5, want_f64: 
     if st:
         raise ValueError(f"vnmo_ria status {st}")
     return (out, s64) if want_f64 else out
+
+
+def permute_gain(score: np.ndarray, V: int, M: int) -> np.ndarray:
+    """LSA cost of the input-channel permutation step (Eq. 7, Q22):
+    cost[j][b*M + s] = retained score channel j contributes in slot s of block b (others frozen), summed over
+    the V-row stripes.  score fp32 [rows][cols]; returns fp64 [cols_p][cols_p]."""
+    score = np.ascontiguousarray(score, dtype=np.float32)
+    rows, cols = score.shape
+    g = geometry(rows, cols, V, M)
+    K = g["cols_p"]
+    cost = np.zeros((K, K), np.float64)
+    st = lib().vnmo_permute_gain(_p(score), cols, rows, cols, V, M, _p(cost))
+    if st:
+        raise ValueError(f"vnmo_permute_gain status {st}")
+    return cost

@@ -411,3 +411,66 @@ int vnmo_ria(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const d
     free(rowsum);
     return VNMO_OK;
 }
+
+/* ---------------------------------------------------------------------------------------------------
+ * Channel-permutation gain scores: the cost matrix of the linear sum assignment
+ * that approximates the input-permutation step, Eq. (7) `eq:admm1` (LSA modelling P:213):
+ *   cost[j][b*M + s] = sum over V-row stripes of the retained score contributed by channel j when it
+ *   replaces the occupant of slot s of column block b (every other column frozen) and the block is
+ *   re-pruned by S_{V:N:M} (column L1 top-4, then per-row top-2; §3, the same decision rules
+ *   and the same fp32 stride-halving L1 as vnmo_prune).
+ * "Contributed by channel j" = the sum of e_j over the rows that keep slot s (reading Q22), so
+ * that with the identity assignment the costs add up to the retained score of the actual pruning.
+ * score fp32 [rows][lds] (e = |score|, zero-padded to rows_p x cols_p); cost fp64 [cols_p][cols_p].
+ * ------------------------------------------------------------------------------------------------- */
+int vnmo_permute_gain(const float* score, int64_t lds, int32_t rows, int32_t cols, int32_t V, int32_t M,
+                      double* cost) {
+    vnmo_geom g;
+    int st = vnmo_geometry(rows, cols, V, M, &g);
+    if (st) return st;
+    if (!score || !cost || M > 64) return VNMO_ERR_ARG;
+    float* E = importance_padded(NULL, 0, score, lds, &g);
+    if (!E) return VNMO_ERR_ARG;
+    const int32_t K = g.cols_p, nvb = g.rows_p / V;
+    int32_t P = 1;
+    while (P < V) P <<= 1;
+#pragma omp parallel for schedule(dynamic)
+    for (int32_t j = 0; j < K; ++j) {
+        float* s = (float*)malloc(sizeof(float) * (size_t)P);
+        float* col = (float*)malloc(sizeof(float) * (size_t)V * (size_t)M);  /* hypothetical block [V][M] */
+        float L[64];
+        for (int32_t b = 0; b < g.nb; ++b)
+            for (int32_t sl = 0; sl < M; ++sl) {
+                double acc = 0.0;
+                for (int32_t vb = 0; vb < nvb; ++vb) {
+                    for (int32_t i = 0; i < V; ++i)
+                        for (int32_t c = 0; c < M; ++c)
+                            col[i * M + c] = E[(int64_t)(vb * V + i) * K + (c == sl ? j : b * M + c)];
+                    for (int32_t c = 0; c < M; ++c) {  /* O3: the stride-halving tree of the block's columns */
+                        for (int32_t r = 0; r < P; ++r) s[r] = r < V ? col[r * M + c] : 0.0f;
+                        for (int32_t stride = P / 2; stride >= 1; stride /= 2)
+                            for (int32_t r = 0; r < stride; ++r) s[r] = s[r] + s[r + stride];
+                        L[c] = s[0];
+                    }
+                    uint8_t kept[4];
+                    top4_columns(L, M, kept);
+                    int ks = -1;
+                    for (int q = 0; q < 4; ++q)
+                        if (kept[q] == sl) ks = q;
+                    if (ks < 0) continue;  /* slot s pruned in this stripe */
+                    for (int32_t i = 0; i < V; ++i) {
+                        float e4[4];
+                        for (int q = 0; q < 4; ++q) e4[q] = col[i * M + kept[q]];
+                        uint8_t lo, hi;
+                        top2_positions(e4, &lo, &hi);
+                        if (lo == ks || hi == ks) acc += (double)col[i * M + sl];
+                    }
+                }
+                cost[(int64_t)j * K + (int64_t)b * M + sl] = acc;
+            }
+        free(s);
+        free(col);
+    }
+    free(E);
+    return VNMO_OK;
+}

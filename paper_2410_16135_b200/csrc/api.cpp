@@ -253,6 +253,25 @@ vnm_status vnm_ria_score(const uint16_t* W, int64_t ldw, int32_t rows, int32_t c
                                        reinterpret_cast<cudaStream_t>(stream)));
 }
 
+size_t vnm_permute_gain_workspace_bytes(const vnm_geom* g) {
+    if (check_geom(g) != VNM_OK) return 0;
+    return vnm::permute_gain_workspace_bytes(*g);
+}
+
+vnm_status vnm_permute_gain(const float* score, int64_t lds, const vnm_geom* g, float* cost, int64_t ldc,
+                            void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if (g->V > 64 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (lds < g->cols || ldc < g->cols_p) return VNM_ERR_SHAPE;
+    if (g->rows == 0 || g->cols == 0) return VNM_OK;
+    if (!score || !cost || !workspace) return VNM_ERR_ARG;
+    if (workspace_bytes < vnm::permute_gain_workspace_bytes(*g)) return VNM_ERR_SHAPE;
+    if ((reinterpret_cast<uintptr_t>(score) & 3u) || (reinterpret_cast<uintptr_t>(cost) & 3u) || !aligned16(workspace))
+        return VNM_ERR_ALIGN;
+    return from_launch(vnm::launch_permute_gain(score, lds, *g, cost, ldc, workspace, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 const char* vnm_status_string(vnm_status s) {
     switch (s) {
         case VNM_OK: return "ok";

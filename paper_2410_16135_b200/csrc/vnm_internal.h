@@ -63,4 +63,9 @@ int launch_ria(const uint16_t* W, int64_t ldw, int32_t rows, int32_t cols, const
                int64_t lds, void* ws, cudaStream_t st);
 int launch_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, float* norms, cudaStream_t st);
 
+// channel-permutation gain scores (permute.cu)
+size_t permute_gain_workspace_bytes(const vnm_geom& g);
+int launch_permute_gain(const float* score, int64_t lds, const vnm_geom& g, float* cost, int64_t ldc, void* ws,
+                        cudaStream_t st);
+
 }  // namespace vnm

@@ -48,7 +48,7 @@ _lib = None
 
 EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress", "vnm_pack_tc",
            "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
-           "vnm_status_string", "vnm_launch_count"]
+           "vnm_permute_gain_workspace_bytes", "vnm_permute_gain", "vnm_status_string", "vnm_launch_count"]
 
 
 def lib():
@@ -84,6 +84,10 @@ def lib():
             L.vnm_ria_workspace_bytes.restype = sz
             L.vnm_ria_score.argtypes = [P, i64, i32, i32, P, ctypes.c_float, P, i64, P, sz, P]
             L.vnm_ria_score.restype = ctypes.c_int
+            L.vnm_permute_gain_workspace_bytes.argtypes = [GP]
+            L.vnm_permute_gain_workspace_bytes.restype = sz
+            L.vnm_permute_gain.argtypes = [P, i64, GP, P, i64, P, sz, P]
+            L.vnm_permute_gain.restype = ctypes.c_int
             L.vnm_status_string.argtypes = [ctypes.c_int]
             L.vnm_status_string.restype = ctypes.c_char_p
             L.vnm_launch_count.argtypes = []
@@ -281,3 +285,19 @@ def ria_score(W: torch.Tensor, act: torch.Tensor | None = None, a: float = 0.5) 
     _check(lib().vnm_ria_score(_ptr(W), _ld(W), rows, cols, _ptr(act), float(a), _ptr(score), score.stride(0),
                                _ptr(ws), ws.numel() * 4, _stream(W.device)), "vnm_ria_score")
     return score
+
+
+def permute_gain(score: torch.Tensor, V: int, M: int) -> torch.Tensor:
+    """LSA cost matrix of the input-channel permutation step (Eq. 7): fp32
+    [cols_p][cols_p], cost[j][b*M + s] = retained score channel j contributes in slot s of block b."""
+    _require_cuda(score)
+    if score.dtype != torch.float32:
+        raise TypeError("score must be fp32")
+    rows, cols = score.shape
+    g = geometry(rows, cols, V, M)
+    cost = torch.empty((g.cols_p, g.cols_p), dtype=torch.float32, device=score.device)
+    nws = int(lib().vnm_permute_gain_workspace_bytes(ctypes.byref(g)))
+    ws = torch.empty(max(nws, 16) // 4 + 4, dtype=torch.float32, device=score.device)
+    _check(lib().vnm_permute_gain(_ptr(score), _ld(score), ctypes.byref(g), _ptr(cost), cost.stride(0), _ptr(ws),
+                                  ws.numel() * 4, _stream(score.device)), "vnm_permute_gain")
+    return cost
