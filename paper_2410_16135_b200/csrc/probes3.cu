@@ -153,3 +153,44 @@ extern "C" int vnm_probe_stream_boxes(const uint16_t* A, int32_t rows, int32_t c
     *ns = h[1] - h[0];
     return 0;
 }
+
+// ---- legacy warp-level sparse MMA rate: every warp issues `iters` x 4 independent mma.sp m16n8k32 (bf16)
+namespace vnm {
+namespace {
+__global__ void __launch_bounds__(512) bench_mma_sync_sp_kernel(uint32_t iters, float* sink) {
+    float d[4][4] = {};
+    uint32_t a[4] = {0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u}, b[4] = {0x3f803f80u, 0, 0, 0};
+    const uint32_t e = 0x44444444u;
+    for (uint32_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            asm volatile(
+                "mma.sp::ordered_metadata.sync.aligned.m16n8k32.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, "
+                "%6, %7}, {%8, %9, %10, %11}, {%0, %1, %2, %3}, %12, 0x0;"
+                : "+f"(d[k][0]), "+f"(d[k][1]), "+f"(d[k][2]), "+f"(d[k][3])
+                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(e));
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += d[k][0] + d[k][1] + d[k][2] + d[k][3];
+    if (s == 12345.f) sink[threadIdx.x] = s;
+}
+}  // namespace
+}  // namespace vnm
+
+// returns ns for grid x warps_per_cta warps each issuing iters x 4 MMAs
+extern "C" int vnm_probe_mma_sync_sp(uint32_t iters, int grid, int warps, float* sink, unsigned long long* ns) {
+    using namespace vnm;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    bench_mma_sync_sp_kernel<<<grid, 32 * warps>>>(16, sink);
+    cudaEventRecord(e0);
+    bench_mma_sync_sp_kernel<<<grid, 32 * warps>>>(iters, sink);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) return 4;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ns = static_cast<unsigned long long>(ms * 1e6);
+    return 0;
+}

@@ -39,8 +39,8 @@
 namespace vnm {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+// NW warps per CTA: 8 (3 CTAs per SM, large weights) or 16 (one tile per CTA for small weights: the per-tile
+// latency halves, the row pass being the longest phase)
 constexpr int kCB = 32;  // column blocks per tile (one per lane in the row pass)
 
 struct Prune2Args {
@@ -75,8 +75,9 @@ struct Maps {
     CUtensorMap val, tcv, met; // stores: A_n [rows_p][ld_val], values_tc [rows_w][ld_tc], A_i2 [rows_p][ld_meta]
 };
 
-template <int V, int M>
-__global__ void __launch_bounds__(kThreads, 3) prune2_kernel(const __grid_constant__ Maps tm, const Prune2Args a) {
+template <int V, int M, int NW>
+__global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const __grid_constant__ Maps tm, const Prune2Args a) {
+    constexpr int kWarps = NW, kThreads = 32 * NW;
     constexpr int TC = kCB * M;  // tile columns (<= 256)
     constexpr int P = TC / 2;    // words per W row in shared memory
     constexpr int RPW = V / kWarps;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 3) prune2_kernel(const __grid_consta
 
         // ---- column L1: lane q = lane & 1 owns rows q + 2i; strides V/2 .. 2 in registers, 1 by shuffle
 #pragma unroll 1
-        for (int cp = warp * 16 + (lane >> 1); cp < (P + 127) / 128 * 128; cp += 128) {
+        for (int cp = warp * 16 + (lane >> 1); cp < (P + 16 * NW - 1) / (16 * NW) * (16 * NW); cp += 16 * NW) {
             const int q = lane & 1;
             float lo = 0.f, hi = 0.f;
             if (cp < P) {
@@ -386,9 +387,10 @@ __global__ void __launch_bounds__(kThreads, 3) prune2_kernel(const __grid_consta
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-template <int V, int M>
+template <int V, int M, int NW>
 cudaError_t launch2(const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
-    auto k = prune2_kernel<V, M>;
+    constexpr int kThreads = 32 * NW;
+    auto k = prune2_kernel<V, M, NW>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -409,16 +411,24 @@ cudaError_t launch2(const Maps& tm, const Prune2Args& a, size_t smem, cudaStream
     return cudaGetLastError();
 }
 
-template <int V>
-cudaError_t launch_v2(int M, const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
+template <int V, int NW>
+cudaError_t launch_m(int M, const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
     switch (M) {
-        case 4: return launch2<V, 4>(tm, a, smem, st);
-        case 5: return launch2<V, 5>(tm, a, smem, st);
-        case 6: return launch2<V, 6>(tm, a, smem, st);
-        case 7: return launch2<V, 7>(tm, a, smem, st);
-        case 8: return launch2<V, 8>(tm, a, smem, st);
+        case 4: return launch2<V, 4, NW>(tm, a, smem, st);
+        case 5: return launch2<V, 5, NW>(tm, a, smem, st);
+        case 6: return launch2<V, 6, NW>(tm, a, smem, st);
+        case 7: return launch2<V, 7, NW>(tm, a, smem, st);
+        case 8: return launch2<V, 8, NW>(tm, a, smem, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+template <int V>
+cudaError_t launch_v2(int M, const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
+    // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
+    const int ntiles = ((a.nb_pad + kCB - 1) / kCB) * (a.rows_p / V);
+    if (V <= 64 && ntiles < num_sms()) return launch_m<V, 16>(M, tm, a, smem, st);
+    return launch_m<V, 8>(M, tm, a, smem, st);
 }
 
 }  // namespace
