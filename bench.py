@@ -143,10 +143,24 @@ def run_gpu(args):
 
     # ---- synthetic inputs (host, seeded per rank), then resident copies in HBM
     layers = []
-    for li, (name, rows, cols) in enumerate(wl["layers"]):
-        W = synth.weights(rows, cols, seed=synth.seed(cfgi, 0) + 10 * li + 100 * rank, kind="outlier")
+    out_mode = args.mode == "out"
+    use_tc0 = T > 64 and M <= 8 and V == 64
+    for li, (name, rows_full, cols) in enumerate(wl["layers"]):
+        # token mode: every rank its own tokens (seeded per rank) and a full weight; out mode: the same weight
+        # and tokens on every rank, rank r owns a V-block-aligned row shard (whole 128-row tiles for the
+        # window form) and Y^T is all-gathered
+        rs = 0 if out_mode else 100 * rank
+        W = synth.weights(rows_full, cols, seed=synth.seed(cfgi, 0) + 10 * li + rs, kind="outlier")
         ldx = -(-T // 8) * 8
-        XT = synth.activations_t(cols, T, seed=synth.seed(cfgi, 1) + 10 * li + 100 * rank, ld=ldx)
+        XT = synth.activations_t(cols, T, seed=synth.seed(cfgi, 1) + 10 * li + rs, ld=ldx)
+        rows, shard_rows, r0 = rows_full, rows_full, 0
+        if out_mode:
+            from paper_2410_16135_b200 import dist as vdist
+            al = 128 // V if use_tc0 else 1
+            r0, r1 = vdist.shard_rows_for_prune(rows_full, V, rank, world, al)
+            shard_rows = vdist.vblocks_per_rank(-(-rows_full // V) * V, V, world, al) * V
+            W = np.ascontiguousarray(W[r0:r1]) if r1 > r0 else np.zeros((V, cols), np.uint16)
+            rows = max(r1 - r0, V)
         Wh = torch.from_numpy(W.view(np.int16)).pin_memory()
         Xh = torch.from_numpy(XT.view(np.int16)).pin_memory()
         Wd = Wh.to(dev).view(torch.bfloat16)
@@ -155,8 +169,12 @@ def run_gpu(args):
         P = vnm.Packed.empty(g, dev)
         Yd = torch.empty((rows, ldx), dtype=torch.bfloat16, device=dev)
         Yh = torch.empty((rows, ldx), dtype=torch.int16).pin_memory()
-        layers.append(dict(name=name, rows=rows, cols=cols, W=Wd, X=Xd, Wh=Wh, Xh=Xh, P=P, Y=Yd, Yh=Yh,
-                           n=geom_numbers(rows, cols, V, M, T)))
+        lay = dict(name=name, rows=rows, cols=cols, W=Wd, X=Xd, Wh=Wh, Xh=Xh, P=P, Y=Yd, Yh=Yh,
+                   n=geom_numbers(rows, cols, V, M, T), n_full=geom_numbers(rows_full, cols, V, M, T))
+        if out_mode:
+            lay["Ysh"] = torch.zeros((shard_rows, ldx), dtype=torch.bfloat16, device=dev)
+            lay["Yall"] = torch.empty((world * shard_rows, ldx), dtype=torch.bfloat16, device=dev)
+        layers.append(lay)
     del W, XT
     L = vnm.lib()
     stream = torch.cuda.current_stream(dev)
@@ -199,6 +217,12 @@ def run_gpu(args):
                         ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
         assert st == 0, vnm.status_string(st)
 
+    def gather(l):
+        # out mode: this rank's Y^T rows -> the padded shard -> one NCCL all-gather (feature-major: contiguous)
+        if out_mode and world > 1:
+            l["Ysh"][:l["rows"]].copy_(l["Y"])
+            dist.all_gather_into_tensor(l["Yall"], l["Ysh"])
+
     def step(ev=None):
         for i, l in enumerate(layers):
             if ev is not None:
@@ -209,6 +233,7 @@ def run_gpu(args):
             spmm(l)
             if ev is not None:
                 ev[i][2].record()
+            gather(l)
 
     def step_e2e():
         for l in layers:
@@ -216,6 +241,7 @@ def run_gpu(args):
             l["X"].view(torch.int16).copy_(l["Xh"], non_blocking=True)
             prune_compress(l)
             spmm(l)
+            gather(l)
             l["Yh"].copy_(l["Y"].view(torch.int16), non_blocking=True)
 
     def barrier():
@@ -270,9 +296,10 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    useful = sum(l["n"]["useful_flops"] for l in layers)
-    dense = sum(l["n"]["dense_flops"] for l in layers)
-    value = world * useful / (ms_per_step * 1e-3) / 1e12
+    # token mode: every rank does the full layers on its own tokens; out mode: the ranks share the full layers
+    useful = sum(l["n_full" if out_mode else "n"]["useful_flops"] for l in layers)
+    dense = sum(l["n_full" if out_mode else "n"]["dense_flops"] for l in layers)
+    value = (1 if out_mode else world) * useful / (ms_per_step * 1e-3) / 1e12  # out mode: useful = full layers
 
     # ---- roofline of the dominant kernel (vnm_spmm), measured live above
     sp_bytes = sum(l["n"]["packed_bytes"] + l["n"]["xt_bytes"] + l["n"]["yt_bytes"] for l in layers)
@@ -347,7 +374,7 @@ def run_gpu(args):
         detail["speedup_vs_dense"] = round(base["dense_ms"] / (sp_t * 1e3), 3)
     if base.get("cslt_ms") is not None:
         detail["speedup_vs_24"] = round(base["cslt_ms"] / (sp_t * 1e3), 3)
-    detail["dense_equiv_tflops"] = round(world * dense / (ms_per_step * 1e-3) / 1e12, 2)
+    detail["dense_equiv_tflops"] = round((1 if out_mode else world) * dense / (ms_per_step * 1e-3) / 1e12, 2)
     detail["prune_compress_share"] = round(pc_t / (ms_per_step * 1e-3), 4)
     detail["step_ms_min"] = round(min(step_ms), 4)
 
@@ -357,10 +384,11 @@ def run_gpu(args):
     if rank == 0:
         out = {"metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "scaling": "strong" if out_mode else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                "config": {"workload": f"{args.workload} V:N:M {V}:2:{M}", "tokens_per_gpu": T,
                           "layers": [f"{n} {c}->{r}" for n, r, c in wl["layers"]],
-                          "parallelism": f"token-sharded x{world}" if world > 1 else "single GPU",
+                          "parallelism": (f"output-feature sharded x{world} + NCCL all-gather of Y^T" if out_mode else
+                                          f"token-sharded x{world}") if world > 1 else "single GPU",
                           "l2": "flushed between timed steps (256 MB write, then a 256 MB read so its write-back happens before the timing)",
                           "launch": "timed steps replay one CUDA graph of the step; e2e launches eagerly"},
                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roofline,
@@ -512,6 +540,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="deit_s", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="vnm", choices=["vnm", "reference"])
+    ap.add_argument("--mode", default="token", choices=["token", "out"],
+                    help="multi-GPU partitioning: token sharding (weak scaling, no collective) or V-block-aligned "
+                         "output sharding + NCCL all-gather of Y^T (strong scaling)")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

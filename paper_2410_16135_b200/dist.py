@@ -22,23 +22,37 @@ import torch.distributed as dist
 from . import vnm
 
 
-def vblocks_per_rank(rows_p: int, V: int, world: int) -> int:
-    return math.ceil((rows_p // V) / world) if rows_p else 0
+def vblocks_per_rank(rows_p: int, V: int, world: int, align: int = 1) -> int:
+    """V-blocks per rank, rounded up to a multiple of `align` (the window form needs 128-row shards)."""
+    if not rows_p:
+        return 0
+    s = math.ceil((rows_p // V) / world)
+    return math.ceil(s / align) * align
 
 
 def shard_packed(P: vnm.Packed, rank: int, world: int) -> tuple[vnm.Packed, int, int]:
-    """Rows [r0, r0 + rows_local) of the packed weight as a zero-copy view.
+    """Rows [r0, r0 + rows_local) of the packed weight as a zero-copy view (A_n / A_i1 / A_i2 and, when
+    present, the window form: then shards hold whole 128-row tiles, the unit of its metadata layout).
 
     Returns (packed shard, r0, padded shard rows S*V)."""
     g = P.g
     V = g.V
-    S = vblocks_per_rank(g.rows_p, V, world)
+    tc = P.values_tc is not None and P.meta_tc is not None
+    S = vblocks_per_rank(g.rows_p, V, world, max(1, 128 // V) if tc else 1)
     vb0 = min(rank * S, g.rows_p // V)
     vb1 = min(vb0 + S, g.rows_p // V)
     r0 = vb0 * V
     rows_local = max(0, min(g.rows, vb1 * V) - r0)
     gl = vnm.geometry(rows_local, g.cols, V, g.M)
     sub = vnm.Packed(gl, P.values[r0:r0 + gl.rows_p], P.col_idx[vb0:vb0 + gl.rows_p // V], P.meta[r0:r0 + gl.rows_p])
+    if tc and gl.rows_p > 0:
+        # include/vnm.h window form: values_tc [rows_w][16 n_mma], meta_tc [rows_w/128][n_stage][128][4]
+        n_mma = g.nb_pad // (8 if g.M == 4 else 4)
+        ld_tc, n_stage = 16 * n_mma, (n_mma + 3) // 4
+        rows_w = math.ceil(gl.rows_p / 128) * 128
+        sub.values_tc = P.values_tc[r0 * ld_tc:(r0 + rows_w) * ld_tc]
+        t0 = r0 // 128
+        sub.meta_tc = P.meta_tc[t0 * n_stage * 512:(t0 + rows_w // 128) * n_stage * 512]
     return sub, r0, S * V
 
 
@@ -82,10 +96,11 @@ def spmm_token_sharded(XT: torch.Tensor, P: vnm.Packed, rank: int, world: int,
     return y, t0
 
 
-def shard_rows_for_prune(rows: int, V: int, rank: int, world: int) -> tuple[int, int]:
-    """Mask/compress pass partitioned by V-stripes (no collective): rows [r0, r1) of W for this rank."""
+def shard_rows_for_prune(rows: int, V: int, rank: int, world: int, align: int = 1) -> tuple[int, int]:
+    """Mask/compress pass partitioned by V-stripes (no collective): rows [r0, r1) of W for this rank
+    (align: V-blocks per shard rounded to a multiple of it, e.g. 128 / V for window-form shards)."""
     rows_p = math.ceil(rows / V) * V if rows else 0
-    S = vblocks_per_rank(rows_p, V, world)
+    S = vblocks_per_rank(rows_p, V, world, align)
     r0 = min(rank * S * V, rows)
     return r0, min(r0 + S * V, rows)
 

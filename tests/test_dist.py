@@ -103,3 +103,31 @@ def test_shard_boundaries():
         total += sub.g.rows
     assert total == rows
     assert vdist.shard_rows_for_prune(rows, V, 7, 8) == (7 * 22 * 64, rows)
+
+
+@pytest.mark.parametrize("rows,world", [(1152, 2), (11008, 8), (384, 3), (200, 4)])
+def test_window_form_shards_are_whole_tiles(rows, world):
+    """With the window form present, output shards hold whole 128-row tiles and their values_tc / meta_tc
+    views start at the shard's tile (include/vnm.h layouts); shards tile the rows exactly."""
+    V, M, cols = 64, 5, 384
+    g = vnm.geometry(rows, cols, V, M)
+    n_mma = g.nb_pad // 4
+    ld_tc, n_stage = 16 * n_mma, (n_mma + 3) // 4
+    rows_w = (g.rows_p + 127) // 128 * 128
+    P = vnm.Packed(g, torch.zeros((g.rows_p, g.ld_val), dtype=torch.bfloat16),
+                   torch.zeros((g.rows_p // V, g.nb_pad, 4), dtype=torch.uint8),
+                   torch.zeros((g.rows_p, g.ld_meta), dtype=torch.int32),
+                   torch.arange(rows_w * ld_tc, dtype=torch.int32).to(torch.float32).to(torch.bfloat16),
+                   torch.arange(rows_w // 128 * n_stage * 512, dtype=torch.int32))
+    covered = 0
+    for r in range(world):
+        sub, r0, rows_shard = vdist.shard_packed(P, r, world)
+        assert rows_shard % 128 == 0 and r0 % 128 == 0
+        if sub.g.rows == 0:
+            continue
+        assert r0 == covered
+        covered += sub.g.rows
+        assert sub.meta_tc.numel() == (sub.g.rows_p + 127) // 128 * n_stage * 512
+        assert int(sub.meta_tc[0]) == (r0 // 128) * n_stage * 512
+        assert sub.values_tc.numel() == (sub.g.rows_p + 127) // 128 * 128 * ld_tc
+    assert covered == rows
