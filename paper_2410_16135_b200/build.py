@@ -17,7 +17,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
          "-Xptxas", "-warn-spills"]
 
 LIBS = {
-    "libvnm.so": ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu", "spmm_tc.cu", "spmm_tc2.cu", "spmm_dec.cu", "ria.cu", "permute.cu"],
+    "libvnm.so": ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu", "spmm_tc.cu", "spmm_tc2.cu", "spmm_tc3.cu", "spmm_dec.cu", "ria.cu", "permute.cu"],
     "libvnm_probe.so": ["probes.cu", "probes2.cu", "probes3.cu"],
 }
 

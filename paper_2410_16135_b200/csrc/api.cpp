@@ -205,6 +205,10 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         // VNM_TC_PLAN=1 / 2 forces the single-CTA / pair kernel (comparisons).
         static const int force = [] { const char* e = getenv("VNM_TC_PLAN"); return e ? atoi(e) : 0; }();
         const int n_stage = (g->nb_pad / (g->M == 4 ? 8 : 4) + 3) / 4, n_rt = (g->rows_p + 127) / 128;
+        if (force == 3) {
+            const int rc = vnm::launch_spmm_tc3(L, reinterpret_cast<cudaStream_t>(stream));
+            if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
+        }
         const bool pair = force ? force == 2 : (n_stage >= 12 && n_rt % 2 == 0);
         if (pair) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
         return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));

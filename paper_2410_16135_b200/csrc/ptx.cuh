@@ -250,6 +250,16 @@ __device__ __forceinline__ void mbar_arrive_cluster(const void* own_bar, uint32_
         "r"(cta)
         : "memory");
 }
+// the same arrive with the default (CTA-scope) release: for signals that publish no memory writes to the peer,
+// e.g. "my tcgen05.ld reads of the accumulator are complete" (tcgen05.wait::ld + fence::before_thread_sync
+// order those); the cluster-scope release costs a MEMBAR.ALL.GPU per arrival (profiles/r01c_*)
+__device__ __forceinline__ void mbar_arrive_remote(const void* own_bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(own_bar)),
+        "r"(cta)
+        : "memory");
+}
 // 2D TMA load into this CTA's shared memory whose completion is counted on the LEADER CTA's mbarrier
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, int32_t x, int32_t y, uint64_t* bar) {
     asm volatile(
@@ -305,5 +315,74 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t* r) 
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+}  // namespace vnm
+
+namespace vnm {
+// ---------------------------------------------------------------- warp-converged stage issue (window form)
+// One stage of the window-form main loop, issued by ONE elected lane of a CONVERGED warp (all 32 lanes call
+// it with the same arguments): keeping the issuing warp converged lets ptxas hold the descriptors in uniform
+// registers, so the MMAs leave back to back (a lane-0 branch cost ~30 dependent instructions per MMA and
+// capped the tensor pipe at ~210 cycles per MMA, profiles/r01c_*).
+// n (2 or 4) sparse MMAs k = 0..n-1: A descriptor + 2 (32 B) per k, B descriptor + b_step per k, metadata
+// column e for k < 2 and e + 2 for k >= 2, id2 = k & 1 (idesc0 / idesc1); `accumulate` applies to k = 0.
+template <int CG>
+__device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t bd, uint64_t b_step, uint32_t e,
+                                             uint32_t idesc0, uint32_t idesc1, uint32_t accumulate, uint32_t n) {
+    static_assert(CG == 1 || CG == 2, "cta_group");
+    if constexpr (CG == 1) {
+        asm volatile(
+            "{\n\t.reg .pred p, p3, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b32 e2;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "setp.ne.b32 acc, %6, 0;\n\t"
+            "setp.eq.b32 one, 0, 0;\n\t"
+            "setp.gt.and.u32 p3, %8, 2, p;\n\t"
+            "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+            "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"
+            "add.u32 e2, %3, 2;\n\t"
+            "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, acc;\n\t"
+            "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a1, b1, [%3], %5, one;\n\t"
+            "@p3 tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a2, b2, [e2], %4, one;\n\t"
+            "@p3 tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a3, b3, [e2], %5, one;\n\t"
+            "}" ::"r"(d),
+            "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p, p3, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b32 e2;\n\t"
+            "elect.sync _|p, 0xffffffff;\n\t"
+            "setp.ne.b32 acc, %6, 0;\n\t"
+            "setp.eq.b32 one, 0, 0;\n\t"
+            "setp.gt.and.u32 p3, %8, 2, p;\n\t"
+            "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+            "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"
+            "add.u32 e2, %3, 2;\n\t"
+            "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%3], %4, acc;\n\t"
+            "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a1, b1, [%3], %5, one;\n\t"
+            "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a2, b2, [e2], %4, one;\n\t"
+            "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a3, b3, [e2], %5, one;\n\t"
+            "}" ::"r"(d),
+            "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n)
+            : "memory");
+    }
+}
+// tcgen05.cp 128x128b (smem [128 rows][16 B] -> TMEM), elected lane of a converged warp
+template <int CG>
+__device__ __forceinline__ void tmem_cp_elect(uint32_t taddr, uint64_t d) {
+    if constexpr (CG == 1)
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p tcgen05.cp.cta_group::1.128x128b [%0], %1;\n\t}" ::"r"(taddr), "l"(d)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p tcgen05.cp.cta_group::2.128x128b [%0], %1;\n\t}" ::"r"(taddr), "l"(d)
+                     : "memory");
+}
+// commit of the pair's tcgen05 ops, multicast to the CTAs of `mask`, elected lane of a converged warp
+__device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 }  // namespace vnm

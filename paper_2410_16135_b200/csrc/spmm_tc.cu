@@ -48,6 +48,7 @@ struct TcArgs {
     int32_t rb;          // B rows per stage per chunk (multiple of 8)
     int32_t stages;      // pipeline depth
     uint32_t b_stage_bytes, stage_bytes;
+    int32_t abl;         // VNM_ABL (timing ablations only, results invalid): see spmm_tc2.cu
 };
 
 
@@ -105,6 +106,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = q % S;
                     mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
                     uint8_t* base = smem + s * a.stage_bytes;
+                    if (a.abl & 4) {
+                        mbar_arrive(&full[s]);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[s], RT * (kABytes + kEBytes) + a.b_stage_bytes);
 #pragma unroll
                     for (int j = 0; j < RT; ++j) {
@@ -121,44 +126,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            int q = 0, tl = 0;
-            const uint32_t idesc0 = idesc_bf16(128, NT, true, 0, true);
-            const uint32_t idesc1 = idesc_bf16(128, NT, true, 1, true);
-            const uint32_t k_bytes = (a.M == 4 ? 32u : 4u * a.M) * 128u;  // B advance per MMA
-            const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;          // K-group (window) stride
-            for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++tl) {
-                const int acc = NACC == 2 ? (tl & 1) : 0;
-                mbar_wait(&tmem_empty[acc], ((NACC == 2 ? (tl >> 1) : tl) & 1) ^ 1);
+        // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
+        int q = 0, tl = 0;
+        const uint32_t idesc0 = idesc_bf16(128, NT, true, 0, true);
+        const uint32_t idesc1 = idesc_bf16(128, NT, true, 1, true);
+        const uint64_t b_step = (a.M == 4 ? 32u : 4u * a.M) * 128u >> 4;  // B descriptor advance per MMA
+        const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
+        const uint32_t b_lbo = a.rb * 128;
+        for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++tl) {
+            const int acc = NACC == 2 ? (tl & 1) : 0;
+            mbar_wait(&tmem_empty[acc], ((NACC == 2 ? (tl >> 1) : tl) & 1) ^ 1);
+            tc_fence_after();
+            for (int st = 0; st < a.n_stage; ++st, ++q) {
+                const int s = q % S;
+                mbar_wait(&full[s], (q / S) & 1);
                 tc_fence_after();
-                for (int st = 0; st < a.n_stage; ++st, ++q) {
-                    const int s = q % S;
-                    mbar_wait(&full[s], (q / S) & 1);
-                    tc_fence_after();
-                    uint8_t* base = smem + s * a.stage_bytes;
-                    const uint32_t meta_s = tmem + kMetaCol + 4 * RT * s;
+                uint8_t* base = smem + s * a.stage_bytes;
+                const uint32_t meta_s = tmem + kMetaCol + 4 * RT * s;
+                if (!(a.abl & 8) || q < S) {
 #pragma unroll
                     for (int j = 0; j < RT; ++j)
-                        tmem_cp_128x128b(meta_s + 4 * j, sdesc(smem_u32(base + e_off + j * kEBytes), 16, 128, 0));
-                    const uint32_t b0 = smem_u32(base + b_off);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int mi = st * 4 + k;
-                        if (mi < a.n_mma) {
-                            const uint64_t bd = sdesc(b0 + k * k_bytes, a.rb * 128, sbo, kLayoutSW128);
-#pragma unroll
-                            for (int j = 0; j < RT; ++j) {
-                                const uint64_t ad = sdesc(smem_u32(base + j * kABytes) + 32 * k, 16, 1024, kLayoutSW128);
-                                mma_sp_bf16(tmem + (acc * RT + j) * NT, ad, bd, meta_s + 4 * j + (k & ~1),
-                                            (k & 1) ? idesc1 : idesc0, mi > 0 ? 1u : 0u);
-                            }
-                        }
-                    }
-                    mma_commit(&empty[s]);
+                        tmem_cp_elect<1>(meta_s + 4 * j, sdesc(smem_u32(base + e_off + j * kEBytes), 16, 128, 0));
                 }
-                mma_commit(&tmem_full[acc]);
+                const uint64_t bd = sdesc(smem_u32(base + b_off), b_lbo, sbo, kLayoutSW128);
+                const int left = a.n_mma - st * 4;
+                const uint32_t n = left < 4 ? static_cast<uint32_t>(left) : 4u;
+#pragma unroll
+                for (int j = 0; j < RT; ++j)
+                    mma_sp_stage<1>(tmem + (acc * RT + j) * NT, sdesc(smem_u32(base + j * kABytes), 16, 1024, kLayoutSW128),
+                                    bd, b_step, meta_s + 4 * j, idesc0, idesc1, st > 0 ? 1u : 0u, n);
+                mma_commit_elect(&empty[s]);
             }
+            mma_commit_elect(&tmem_full[acc]);
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
@@ -179,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int j = 0; j < RT; ++j) {
                 const int rt = rg * RT + j;
-                if (rt >= a.n_rt) break;
+                if (rt >= a.n_rt || (a.abl & 1)) break;
 #pragma unroll 1
                 for (int c = 0; c < NT && n0 + c < a.T; c += cw) {
                     uint32_t pk[32];
@@ -206,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int k = 0; k < 16; ++k) pk[16 * hh + k] = v[k];
                         }
                     }
+                    if (a.abl & 2) continue;
                     if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
                     __syncwarp();
 #pragma unroll
@@ -275,6 +275,7 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
     const int grid = a.work < num_sms() ? a.work : num_sms();
+    a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
     k<<<grid, kThreads, smem, stream>>>(ta, tb, ty, a);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;

@@ -53,6 +53,8 @@ struct Tc2Args {
     int32_t y_slots;     // epilogue staging slots per warp (1 or 2)
     uint32_t b_bytes, stage_bytes, res_bytes;
     int32_t trace;       // VNM_SPMM_TRACE: per-CTA wait / busy cycle counters into g_tc2_t
+    int32_t abl;         // VNM_ABL (timing ablations only, results invalid): 1 no epilogue, 2 no Y stores,
+                         // 4 no X^T loads, 8 no metadata copies after the first stage
 };
 
 // VNM_SPMM_TRACE counters per CTA: MMA wait full, MMA wait tmem_empty, MMA loop total, producer wait empty,
@@ -89,7 +91,7 @@ __device__ __forceinline__ void release(uint64_t* tmem_empty, int lane, bool lea
     __syncwarp();
     if (lane == 0) {
         if (leader) mbar_arrive(tmem_empty);
-        else mbar_arrive_cluster(tmem_empty, 0);
+        else mbar_arrive_remote(tmem_empty, 0);
     }
 }
 
@@ -189,6 +191,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
                     c_emp += clock64() - c0;
                     uint8_t* base = ring + s * a.stage_bytes;
+                    if (a.abl & 4) {
+                        if (leader) mbar_arrive(&full[s]);
+                        continue;
+                    }
                     if (a.a_res) {
                         if (leader) mbar_arrive_expect_tx(&full[s], 2 * a.b_bytes);
                     } else {
@@ -203,13 +209,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
             if (a.trace) g_tc2_t[3][blockIdx.x] = c_emp;
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer (leader CTA)
-        if (leader && lane == 0) {
+        // ------------------------------------------------------------ MMA issuer (leader CTA; converged warp,
+        // elected lane: see mma_sp_stage)
+        if (leader) {
             int q = 0, tl = 0, rp, tt;
             const uint32_t idesc0 = idesc_bf16(256, NT, true, 0, true);
             const uint32_t idesc1 = idesc_bf16(256, NT, true, 1, true);
-            const uint32_t k_bytes = (a.M == 4 ? 32u : 4u * a.M) * 128u;  // B advance per MMA
-            const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;          // K-group (window) stride
+            const uint64_t b_step = (a.M == 4 ? 32u : 4u * a.M) * 128u >> 4;  // B descriptor advance per MMA
+            const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
+            const uint32_t b_lbo = a.rb * 128;
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
             for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
                 if (a.a_res && tl == 0) mbar_wait(res_full, 0);
@@ -228,24 +236,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     uint8_t* base = ring + s * a.stage_bytes;
                     const uint32_t meta_s = tmem + kMetaCol + 4 * s;
                     const uint32_t e_s = a.a_res ? smem_u32(resE + st * kEBytes) : smem_u32(base + e_off);
-                    tmem_cp_128x128b_pair(meta_s, sdesc(e_s, 16, 128, 0));
-                    const uint32_t b0 = smem_u32(base + b_off);
+                    if (!(a.abl & 8) || q < S) tmem_cp_elect<2>(meta_s, sdesc(e_s, 16, 128, 0));
                     const uint32_t a0 = a.a_res ? smem_u32(smem + st * kABytes) : smem_u32(base);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int mi = st * 4 + k;
-                        if (mi < a.n_mma) {
-                            const uint64_t bd = sdesc(b0 + k * k_bytes, a.rb * 128, sbo, kLayoutSW128);
-                            const uint64_t ad = sdesc(a0 + 32 * k, 16, 1024, kLayoutSW128);
-                            mma_sp_bf16_pair(d_tmem, ad, bd, meta_s + (k & ~1), (k & 1) ? idesc1 : idesc0,
-                                             mi > 0 ? 1u : 0u);
-                        }
-                    }
-                    mma_commit_pair(&empty[s], 0x3);
+                    const int left = a.n_mma - st * 4;
+                    mma_sp_stage<2>(d_tmem, sdesc(a0, 16, 1024, kLayoutSW128),
+                                    sdesc(smem_u32(base + b_off), b_lbo, sbo, kLayoutSW128), b_step, meta_s, idesc0,
+                                    idesc1, st > 0 ? 1u : 0u, left < 4 ? static_cast<uint32_t>(left) : 4u);
+                    mma_commit_pair_elect(&empty[s], 0x3);
                 }
-                mma_commit_pair(&tmem_full[acc], 0x3);
+                mma_commit_pair_elect(&tmem_full[acc], 0x3);
             }
-            if (a.trace) {
+            if (a.trace && lane == 0) {
                 g_tc2_t[0][blockIdx.x] = c_full;
                 g_tc2_t[1][blockIdx.x] = c_emp;
                 g_tc2_t[2][blockIdx.x] = clock64() - c_all;
@@ -269,7 +270,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
             c_wait += c1 - c0;
             tc_fence_after();
             const uint32_t taddr = tmem + ((32 * qd) << 16) + acc * NT + kBChunk * ch;
-            const bool store = rt < a.n_rt && t0 < a.T;
+            const bool store = rt < a.n_rt && t0 < a.T && !(a.abl & 2);
+            if (a.abl & 1) {
+                release(&tmem_empty[acc], lane, leader);
+                continue;
+            }
             if constexpr (kBf16) {
                 // drain the warp's 32 x 64 accumulator block (two loads, one wait) into 32 packed registers,
                 // release the accumulator, then stage + store one 128-byte-per-row chunk
@@ -373,6 +378,7 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
         pairs = a.work;
     }
     a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
+    a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
     k<<<2 * pairs, C::kThreads, smem, stream>>>(ta, tb, te, ty, a);
     count_launch();
     cudaError_t e = cudaGetLastError();

@@ -10,6 +10,9 @@ rows, cols, M, T = map(int, sys.argv[1:5])
 tc = len(sys.argv) > 5 and sys.argv[5] == "tc"
 W = synth.weights(rows, cols, seed=1)
 X = synth.activations_t(cols, T, seed=2)
+z = os.environ.get("VNM_TS_ZERO", "")  # power probe: zero activations and / or weights
+if "x" in z: X = X * 0
+if "w" in z: W = W * 0
 P = vnm.prune_compress(to_dev_bf16(W), 64, M, tc=tc)
 Xd = to_dev_bf16(X)
 Y = torch.empty((rows, (T + 7) // 8 * 8), dtype=torch.bfloat16, device="cuda")
