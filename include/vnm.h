@@ -118,6 +118,16 @@ vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, co
 vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
                               const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
 
+/* vnm_prune_compress of n weights in ONE launch (e.g. every linear layer of a model at a mask update: the
+ * mask + compression pass is re-run for all layers at once).  Entry i has the meaning of one
+ * vnm_prune_compress call: W[i] / ldw[i] / score[i] (NULL: ABS) / lds[i] / out[i] (out[i]->g is the geometry)
+ * / mask[i] (NULL: none).  Outputs are byte-identical to n separate calls.  1 <= n <= 8 weights sharing one
+ * (V, M) run as one kernel when 32 <= V <= 128 and M <= 8; other batches run as n launches on `stream`.
+ * Errors: VNM_ERR_ARG (n out of range, NULL arrays), else the first failing entry's status (nothing launched). */
+vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const int64_t* ldw,
+                                      const float* const* score, const int64_t* lds, vnm_packed* const* out,
+                                      uint32_t* const* mask, vnm_stream_t stream);
+
 /* Fill P->values_tc / P->meta_tc (caller-allocated, vnm_bytes 4 / 5) from the canonical A_n / A_i1 / A_i2
  * of P.  VNM_ERR_UNSUPPORTED unless 32 <= V <= 128 and 4 <= M <= 8; VNM_ERR_ARG if a tc pointer is NULL.       */
 vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);

@@ -165,6 +165,51 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
     return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const int64_t* ldw,
+                                      const float* const* score, const int64_t* lds, vnm_packed* const* out,
+                                      uint32_t* const* mask, vnm_stream_t stream) {
+    if (n < 1 || n > 64 || !W || !ldw || !out) return VNM_ERR_ARG;
+    vnm::PruneLaunch Ls[64];
+    int live = 0;
+    bool same = true;
+    for (int i = 0; i < n; ++i) {
+        if (!out[i]) return VNM_ERR_ARG;
+        const vnm_geom* g = &out[i]->g;
+        const float* sc = score ? score[i] : nullptr;
+        const int64_t ls = lds ? lds[i] : 0;
+        uint32_t* mk = mask ? mask[i] : nullptr;
+        vnm_status s = check_geom(g);
+        if (s) return s;
+        if ((s = check_w(W[i], ldw[i], g))) return s;
+        if ((s = check_score(sc, ls, g))) return s;
+        if ((s = check_packed(out[i], g))) return s;
+        if (mk && !aligned16(mk)) return VNM_ERR_ALIGN;
+        if (g->rows_p == 0 || g->nb_pad == 0) continue;
+        if (!W[i]) return VNM_ERR_ARG;
+        vnm::PruneLaunch L{g, W[i], ldw[i], sc, ls, nullptr, mk, out[i]->values, out[i]->col_idx, out[i]->meta, nullptr};
+        if (out[i]->values_tc || out[i]->meta_tc) {
+            if (g->V < 32 || g->V > 128 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+            if (!out[i]->values_tc || !out[i]->meta_tc) return VNM_ERR_ARG;
+            if (!aligned16(out[i]->values_tc) || !aligned16(out[i]->meta_tc)) return VNM_ERR_ALIGN;
+            L.values_tc = out[i]->values_tc;
+            L.meta_tc = out[i]->meta_tc;
+        }
+        if (live > 0 && (g->V != Ls[0].g->V || g->M != Ls[0].g->M)) same = false;
+        Ls[live++] = L;
+    }
+    if (live == 0) return VNM_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (same && live <= 8) {
+        const int rc = vnm::launch_prune2_batch(Ls, live, st);
+        if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
+    }
+    for (int i = 0; i < live; ++i) {
+        const vnm_status s = from_launch(vnm::launch_prune_pack(Ls[i], st));
+        if (s) return s;
+    }
+    return VNM_OK;
+}
+
 vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream) {
     if (!P) return VNM_ERR_ARG;
     const vnm_geom* g = &P->g;
@@ -205,7 +250,12 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         // VNM_TC_PLAN=1 / 2 forces the single-CTA / pair kernel (comparisons).
         static const int force = [] { const char* e = getenv("VNM_TC_PLAN"); return e ? atoi(e) : 0; }();
         const int n_stage = (g->nb_pad / (g->M == 4 ? 8 : 4) + 3) / 4, n_rt = (g->rows_p + 127) / 128;
-        if (force == 3) {
+        // CTA pairs with the row pair's A resident (spmm_tc3.cu): measured faster for short K, M <= 6 and >= 6
+        // row tiles at large T (DeiT-S qkv / fc1: profiles/r01c_probes.md); slower for M = 8 and 3-row-tile
+        // layers, where the single-CTA kernel stays.
+        const int n_mma = g->nb_pad / (g->M == 4 ? 8 : 4);
+        const bool tc3 = force ? force == 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192);
+        if (tc3) {
             const int rc = vnm::launch_spmm_tc3(L, reinterpret_cast<cudaStream_t>(stream));
             if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
         }

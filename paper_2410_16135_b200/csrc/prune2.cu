@@ -75,19 +75,30 @@ struct Maps {
     CUtensorMap val, tcv, met; // stores: A_n [rows_p][ld_val], values_tc [rows_w][ld_tc], A_i2 [rows_p][ld_meta]
 };
 
+// Several weights of the same (V, M) in one launch (vnm_prune_compress_batched): tiles are numbered across the
+// problems (tile0 = prefix sums of the per-problem tile counts) and each tile reads its own problem's maps and
+// arguments; the shared-memory layout is sized for the largest problem.
+constexpr int kMaxBatch = 8;
+struct Batch {
+    int32_t n;
+    int32_t tile0[kMaxBatch + 1];
+    int32_t any_score, any_mask;
+    Maps tm[kMaxBatch];
+    Prune2Args a[kMaxBatch];
+};
+
 template <int V, int M, int NW>
-__global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const __grid_constant__ Maps tm, const Prune2Args a) {
+__global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const __grid_constant__ Batch B) {
     constexpr int kWarps = NW, kThreads = 32 * NW;
     constexpr int TC = kCB * M;  // tile columns (<= 256)
     constexpr int P = TC / 2;    // words per W row in shared memory
     constexpr int RPW = V / kWarps;
     constexpr uint32_t kWBytes = V * TC * 2, kSBytes = V * TC * 4;
     extern __shared__ __align__(128) uint8_t smem[];
-    const bool has_score = a.has_score, tc = a.has_tc;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     // two tile buffers (W [+ score]) for the TMA double buffer, the output staging, then the scratch
-    const uint32_t buf_bytes = kWBytes + (has_score ? kSBytes : 0);
+    const uint32_t buf_bytes = kWBytes + (B.any_score ? kSBytes : 0);
     uint32_t* sVal = reinterpret_cast<uint32_t*>(smem + 2 * buf_bytes);    // [V][kCB] A_n pairs
     uint2* sTcv = reinterpret_cast<uint2*>(sVal + V * kCB);                 // [V][kCB] window values (M > 4)
     uint32_t* sMet = reinterpret_cast<uint32_t*>(sTcv + V * kCB);           // [V][4] A_i2 words
@@ -96,17 +107,24 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
     uint32_t* sUni = sKp + kCB;                                             // [kCB] kept positions carrying bits
     uint2* sTab = reinterpret_cast<uint2*>(sUni + kCB);                     // [8 * 8] window-form encodings
     uint32_t* sBits = reinterpret_cast<uint32_t*>(sTab + 64);               // [V][kCB] (mask_out)
-    uint8_t* sNib = reinterpret_cast<uint8_t*>(sBits + (a.mask_out ? V * kCB : 0));  // [V][kCB] A_i2 nibbles
+    uint8_t* sNib = reinterpret_cast<uint8_t*>(sBits + (B.any_mask ? V * kCB : 0));  // [V][kCB] A_i2 nibbles
     uint8_t* sTcn = sNib + V * kCB;                                                   // [V][kCB] window nibbles
     __shared__ __align__(8) uint64_t bar[2];
 
-    const int ntx = (a.nb_pad + kCB - 1) / kCB, ntiles = ntx * (a.rows_p / V);
+    const int ntiles = B.tile0[B.n];
+    auto problem = [&](int tile) {
+        int p = 0;
+        while (p + 1 < B.n && tile >= B.tile0[p + 1]) ++p;
+        return p;
+    };
     auto issue = [&](int tile, int bi) {
-        const int bx = tile % ntx, by = tile / ntx;
+        const int p = problem(tile), lt = tile - B.tile0[p];
+        const Prune2Args& ap = B.a[p];
+        const int ntx = (ap.nb_pad + kCB - 1) / kCB, bx = lt % ntx, by = lt / ntx;
         uint8_t* dst = smem + bi * buf_bytes;
-        mbar_arrive_expect_tx(&bar[bi], buf_bytes);
-        tma_load_2d(dst, &tm.w, bx * kCB * M, by * V, &bar[bi]);
-        if (has_score) tma_load_2d(dst + kWBytes, &tm.s, bx * kCB * M, by * V, &bar[bi]);
+        mbar_arrive_expect_tx(&bar[bi], kWBytes + (ap.has_score ? kSBytes : 0));
+        tma_load_2d(dst, &B.tm[p].w, bx * kCB * M, by * V, &bar[bi]);
+        if (ap.has_score) tma_load_2d(dst + kWBytes, &B.tm[p].s, bx * kCB * M, by * V, &bar[bi]);
     };
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -115,7 +133,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
         if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
     }
     if (threadIdx.x < kCB) sUni[threadIdx.x] = 0u;
-    if (M > 4 && tc && threadIdx.x < 64) {
+    if (M > 4 && threadIdx.x < 64) {
         // window-form encoding of the kept pair (cl, ch) = (t / 8, t % 8), cl < ch (tc_form.cuh): byte-permute
         // selectors placing v_lo / v_hi / 0 in the 4 slots, and the two group nibbles
         const int cl = threadIdx.x / 8, ch = threadIdx.x % 8;
@@ -128,10 +146,18 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
     __syncthreads();
 
     int it = 0;
-    PTRACE(0)
+    {
+        const Prune2Args& a = B.a[0];
+        PTRACE(0)
+    }
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int bi = it & 1;
-        const int bx = tile % ntx, by = tile / ntx;
+        const int p = problem(tile), lt = tile - B.tile0[p];
+        const Prune2Args& a = B.a[p];
+        const Maps& tm = B.tm[p];
+        const bool has_score = a.has_score, tc = a.has_tc;
+        const int ntx = (a.nb_pad + kCB - 1) / kCB;
+        const int bx = lt % ntx, by = lt / ntx;
         const int b0 = bx * kCB, r0 = by * V;
         // prefetch the next tile into the other buffer (its previous contents were consumed last iteration)
         if (threadIdx.x == 0 && tile + static_cast<int>(gridDim.x) < ntiles) issue(tile + gridDim.x, bi ^ 1);
@@ -388,7 +414,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
 }
 
 template <int V, int M, int NW>
-cudaError_t launch2(const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
+cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     constexpr int kThreads = 32 * NW;
     auto k = prune2_kernel<V, M, NW>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -396,12 +422,12 @@ cudaError_t launch2(const Maps& tm, const Prune2Args& a, size_t smem, cudaStream
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    const int ntiles = ((a.nb_pad + kCB - 1) / kCB) * (a.rows_p / V);
+    const int ntiles = B.tile0[B.n];
     int grid = num_sms() * per_sm;
     if (grid > ntiles) grid = ntiles;
-    k<<<grid, kThreads, smem, st>>>(tm, a);
+    k<<<grid, kThreads, smem, st>>>(B);
     count_launch();
-    if (a.trace) {
+    if (B.a[0].trace) {
         unsigned long long h[8];
         cudaStreamSynchronize(st);
         cudaMemcpyFromSymbol(h, g_prune2_t, sizeof(h));
@@ -412,44 +438,48 @@ cudaError_t launch2(const Maps& tm, const Prune2Args& a, size_t smem, cudaStream
 }
 
 template <int V, int NW>
-cudaError_t launch_m(int M, const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
+cudaError_t launch_m(int M, const Batch& B, size_t smem, cudaStream_t st) {
     switch (M) {
-        case 4: return launch2<V, 4, NW>(tm, a, smem, st);
-        case 5: return launch2<V, 5, NW>(tm, a, smem, st);
-        case 6: return launch2<V, 6, NW>(tm, a, smem, st);
-        case 7: return launch2<V, 7, NW>(tm, a, smem, st);
-        case 8: return launch2<V, 8, NW>(tm, a, smem, st);
+        case 4: return launch2<V, 4, NW>(B, smem, st);
+        case 5: return launch2<V, 5, NW>(B, smem, st);
+        case 6: return launch2<V, 6, NW>(B, smem, st);
+        case 7: return launch2<V, 7, NW>(B, smem, st);
+        case 8: return launch2<V, 8, NW>(B, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
 template <int V>
-cudaError_t launch_v2(int M, const Maps& tm, const Prune2Args& a, size_t smem, cudaStream_t st) {
+cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
     // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
-    const int ntiles = ((a.nb_pad + kCB - 1) / kCB) * (a.rows_p / V);
-    if (V <= 64 && ntiles < num_sms()) return launch_m<V, 16>(M, tm, a, smem, st);
-    return launch_m<V, 8>(M, tm, a, smem, st);
+    if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16>(M, B, smem, st);
+    return launch_m<V, 8>(M, B, smem, st);
 }
 
 }  // namespace
 
-// Returns kLaunchUnsupported when this kernel does not apply (the caller falls back to prune.cu).
-int launch_prune2(const PruneLaunch& L, cudaStream_t stream) {
+static bool L_unsupported(const PruneLaunch& L) {
     const vnm_geom& g = *L.g;
-    if (L.mask_in || g.V < 32 || g.V > 128 || g.M > 8 || g.rows == 0 || g.cols == 0) return kLaunchUnsupported;
+    return L.mask_in || g.V < 32 || g.V > 128 || g.M > 8 || g.rows == 0 || g.cols == 0 ||
+           (L.values_tc && (!L.meta_tc || !L.values));
+}
+
+// Per-problem tensor maps and arguments (+ the pad-row memsets of the window form); false: not applicable.
+static bool setup_problem(const PruneLaunch& L, Maps& tm, Prune2Args& a, cudaStream_t stream) {
+    const vnm_geom& g = *L.g;
+    if (L.mask_in || g.V < 32 || g.V > 128 || g.M > 8 || g.rows == 0 || g.cols == 0) return false;
     const bool has_score = L.score != nullptr, tc = L.values_tc != nullptr, vals = L.values != nullptr;
-    if (tc && (!L.meta_tc || !vals)) return kLaunchUnsupported;
+    if (tc && (!L.meta_tc || !vals)) return false;
     const int tile_cols = kCB * g.M;
-    Maps tm;
     if (!encode_2d(&tm.w, L.W, static_cast<uint64_t>(g.cols), static_cast<uint64_t>(g.rows),
                    static_cast<uint64_t>(L.ldw) * 2, tile_cols, g.V, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                    CU_TENSOR_MAP_SWIZZLE_NONE))
-        return kLaunchUnsupported;
+        return false;
     tm.s = tm.w;
     if (has_score && !encode_2d(&tm.s, L.score, static_cast<uint64_t>(g.cols), static_cast<uint64_t>(g.rows),
                                 static_cast<uint64_t>(L.lds) * 4, tile_cols, g.V, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                                 CU_TENSOR_MAP_SWIZZLE_NONE))
-        return kLaunchUnsupported;
+        return false;
     tm.val = tm.tcv = tm.met = tm.w;
     int n_mma = 0, ld_tc = 0;
     if (vals) {
@@ -459,7 +489,7 @@ int launch_prune2(const PruneLaunch& L, cudaStream_t stream) {
             !encode_2d(&tm.met, L.meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
                        static_cast<uint64_t>(g.ld_meta) * 4, kCB / 8, g.V, CU_TENSOR_MAP_DATA_TYPE_UINT32,
                        CU_TENSOR_MAP_SWIZZLE_NONE))
-            return kLaunchUnsupported;
+            return false;
     }
     if (tc) {
         n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
@@ -468,9 +498,8 @@ int launch_prune2(const PruneLaunch& L, cudaStream_t stream) {
         if (!encode_2d(&tm.tcv, L.values_tc, static_cast<uint64_t>(ld_tc), static_cast<uint64_t>(g.rows_p),
                        static_cast<uint64_t>(ld_tc) * 2, vpb * kCB, g.V, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                        CU_TENSOR_MAP_SWIZZLE_NONE))
-            return kLaunchUnsupported;
+            return false;
     }
-    Prune2Args a;
     a.mask_out = L.mask_out; a.col_idx = L.col_idx; a.meta = L.meta; a.meta_tc = L.meta_tc;
     a.ld_meta = g.ld_meta;
     a.has_values = vals ? 1 : 0; a.has_tc = tc ? 1 : 0;
@@ -489,19 +518,46 @@ int launch_prune2(const PruneLaunch& L, cudaStream_t stream) {
                               0x44, static_cast<size_t>(128 - l0) * 16, a.n_stage_tc, stream);
         }
     }
-    const size_t buf = static_cast<size_t>(g.V) * tile_cols * 2 + (has_score ? static_cast<size_t>(g.V) * tile_cols * 4 : 0);
-    const size_t smem = 2 * buf + static_cast<size_t>(g.V) * kCB * (4 + 8) + static_cast<size_t>(g.V) * 16 + 256 * 4 +
-                        2 * kCB * 4 + 64 * 8 + (L.mask_out ? static_cast<size_t>(g.V) * kCB * 4 : 0) +
-                        2 * static_cast<size_t>(g.V) * kCB;
+    return true;
+}
+
+// n problems of one (V, M) in one launch.  kLaunchUnsupported when this kernel does not apply to all of them
+// (the caller then falls back to one launch per problem).
+int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream) {
+    if (n < 1 || n > kMaxBatch) return kLaunchUnsupported;
+    const int V = Ls[0].g->V, M = Ls[0].g->M;
+    for (int i = 0; i < n; ++i) {
+        const vnm_geom& g = *Ls[i].g;
+        if (g.V != V || g.M != M || L_unsupported(Ls[i])) return kLaunchUnsupported;
+    }
+    static Batch B;  // host staging of the kernel parameters (copied at launch)
+    B.n = n;
+    B.tile0[0] = 0;
+    B.any_score = B.any_mask = 0;
+    for (int i = 0; i < n; ++i) {
+        if (!setup_problem(Ls[i], B.tm[i], B.a[i], stream)) return kLaunchUnsupported;
+        const vnm_geom& g = *Ls[i].g;
+        B.tile0[i + 1] = B.tile0[i] + ((g.nb_pad + kCB - 1) / kCB) * (g.rows_p / V);
+        B.any_score |= B.a[i].has_score;
+        B.any_mask |= Ls[i].mask_out != nullptr;
+    }
+    const int tile_cols = kCB * M;
+    const size_t buf = static_cast<size_t>(V) * tile_cols * 2 + (B.any_score ? static_cast<size_t>(V) * tile_cols * 4 : 0);
+    const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (4 + 8) + static_cast<size_t>(V) * 16 + 256 * 4 +
+                        2 * kCB * 4 + 64 * 8 + (B.any_mask ? static_cast<size_t>(V) * kCB * 4 : 0) +
+                        2 * static_cast<size_t>(V) * kCB;
     if (smem > kMaxSmem) return kLaunchUnsupported;
     cudaError_t e;
-    switch (g.V) {
-        case 32: e = launch_v2<32>(g.M, tm, a, smem, stream); break;
-        case 64: e = launch_v2<64>(g.M, tm, a, smem, stream); break;
-        case 128: e = launch_v2<128>(g.M, tm, a, smem, stream); break;
+    switch (V) {
+        case 32: e = launch_v2<32>(M, B, smem, stream); break;
+        case 64: e = launch_v2<64>(M, B, smem, stream); break;
+        case 128: e = launch_v2<128>(M, B, smem, stream); break;
         default: return kLaunchUnsupported;
     }
     return e == cudaSuccess ? 0 : kLaunchCudaError;
 }
+
+// Returns kLaunchUnsupported when this kernel does not apply (the caller falls back to prune.cu).
+int launch_prune2(const PruneLaunch& L, cudaStream_t stream) { return launch_prune2_batch(&L, 1, stream); }
 
 }  // namespace vnm

@@ -54,6 +54,10 @@ struct Tc3Args {
     uint32_t ring_rows;  // S * rows_stage + 8 (shadow): rows per token-chunk region
     uint32_t stage_tx, shadow_tx;  // expect_tx bytes for both CTAs
     int32_t trace;
+    int32_t epi;  // 1: Y^T written with coalesced st.global from a warp-private shared transpose; 0: TMA stores
+    void* Y;
+    int64_t ldy;
+    int32_t rows;
     int32_t abl;  // VNM_ABL timing ablations (results invalid): 1 no epilogue, 2 no Y stores, 4 no X^T loads
 };
 
@@ -283,11 +287,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 if (!rows_ok || t0 >= a.T) continue;
                 d0 = clock64();
+                const uint32_t row = smem_u32(slot) + lane * 128;
+                if (a.epi) {
+                    // rows -> the warp's slot (SW128: chunk k of row r at k ^ (r % 8), conflict-free), then read
+                    // back 4 rows x 8 chunks per instruction (8 lanes per 128-byte row, conflict-free) and store
+                    // full 128-byte lines with st.global.v4: no TMA, no proxy fence, no bulk-group waits
+                    __syncwarp();  // the previous chunk's reads of the slot are done
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((k ^ lane) & 7) << 4)),
+                                     "r"(w[4 * k]), "r"(w[4 * k + 1]), "r"(w[4 * k + 2]), "r"(w[4 * k + 3])
+                                     : "memory");
+                    __syncwarp();
+                    c_st += clock64() - d0;
+                    d0 = clock64();
+                    constexpr int kEl = kBf16 ? 8 : 4;  // elements per 16 bytes
+                    const int cc = lane & 7, tok = t0 + cc * kEl;
+                    const int t_end = min(a.T, tt * NT + NT);
+                    const int grow0 = rt * 128 + 32 * qd;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int r = 4 * j + (lane >> 3);
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                     : "r"(smem_u32(slot) + r * 128 + (((cc ^ r) & 7) << 4)));
+                        const int grow = grow0 + r;
+                        if (grow >= a.rows || tok >= t_end) continue;
+                        uint8_t* dst = static_cast<uint8_t*>(a.Y) + (static_cast<int64_t>(grow) * a.ldy + tok) * (kBf16 ? 2 : 4);
+                        if (tok + kEl <= t_end) {
+                            asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(x0), "r"(x1), "r"(x2),
+                                         "r"(x3)
+                                         : "memory");
+                        } else {  // ragged token tail: element by element
+                            const uint32_t xs[4] = {x0, x1, x2, x3};
+                            for (int e = 0; e < t_end - tok; ++e) {
+                                if constexpr (kBf16)
+                                    reinterpret_cast<uint16_t*>(dst)[e] = static_cast<uint16_t>(xs[e >> 1] >> (16 * (e & 1)));
+                                else
+                                    reinterpret_cast<uint32_t*>(dst)[e] = xs[e];
+                            }
+                        }
+                    }
+                    c_iss += clock64() - d0;
+                    continue;
+                }
                 if (lane == 0) bulk_wait_read<0>();  // the previous store has read the slot
                 __syncwarp();
                 c_slot += clock64() - d0;
                 d0 = clock64();
-                const uint32_t row = smem_u32(slot) + lane * 128;
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((k ^ lane) & 7) << 4)),
@@ -380,6 +428,10 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, cudaStream_t stream) {
         return kLaunchCudaError;
     a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
     a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
+    a.epi = getenv("VNM_TC3_EPI") ? atoi(getenv("VNM_TC3_EPI")) : 1;
+    a.Y = L.YT;
+    a.ldy = L.ldy;
+    a.rows = g.rows;
     k<<<2 * pairs, kThreads, smem, stream>>>(ta, te, tb0, tb1, ts0, ts1, ty, tyt, a);
     count_launch();
     cudaError_t e = cudaGetLastError();

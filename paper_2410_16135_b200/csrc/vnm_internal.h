@@ -31,6 +31,7 @@ struct PruneLaunch {
 };
 int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream);
 int launch_prune2(const PruneLaunch& L, cudaStream_t stream);  // V >= 32 (prune2.cu)
+int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream);  // n <= 8 weights, one (V, M)
 
 struct SpmmLaunch {
     const vnm_packed* P;

@@ -46,7 +46,8 @@ class CPacked(ctypes.Structure):
 _lock = threading.Lock()
 _lib = None
 
-EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress", "vnm_pack_tc",
+EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress",
+           "vnm_prune_compress_batched", "vnm_pack_tc",
            "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
            "vnm_permute_gain_workspace_bytes", "vnm_permute_gain", "vnm_status_string", "vnm_launch_count"]
 
@@ -72,6 +73,8 @@ def lib():
             L.vnm_compress.restype = ctypes.c_int
             L.vnm_prune_compress.argtypes = [P, i64, P, i64, GP, PP, P, P]
             L.vnm_prune_compress.restype = ctypes.c_int
+            L.vnm_prune_compress_batched.argtypes = [i32, P, P, P, P, P, P, P]
+            L.vnm_prune_compress_batched.restype = ctypes.c_int
             L.vnm_pack_tc.argtypes = [PP, P]
             L.vnm_pack_tc.restype = ctypes.c_int
             L.vnm_spmm.argtypes = [P, i64, i32, PP, P, i64, ctypes.c_int, P, sz, P]
@@ -227,6 +230,37 @@ def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None =
                                     ctypes.byref(g), ctypes.byref(cp), _ptr(mask), _stream(W.device)),
            "vnm_prune_compress")
     return (P, mask) if want_mask else P
+
+
+def prune_compress_batched(Ws: list, V: int, M: int, scores: list | None = None, want_mask: bool = False,
+                           tc: bool = False):
+    """vnm_prune_compress_batched: prune + compress several weights of one (V, M) in one launch (byte-identical
+    to one prune_compress per weight).  Returns the list of Packed (and the list of masks if asked)."""
+    n = len(Ws)
+    Ws = [_as_bits16(W) for W in Ws]
+    scores = scores if scores is not None else [None] * n
+    _require_cuda(*Ws, *scores)
+    Ps, masks, cps = [], [], []
+    for W in Ws:
+        g = geometry(W.shape[0], W.shape[1], V, M)
+        P = Packed.empty(g, W.device)
+        if tc and 32 <= V <= 128 and M <= 8:
+            nv, nm = tc_bytes(g)
+            P.values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=W.device)
+            P.meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=W.device)
+        Ps.append(P)
+        masks.append(torch.empty((g.rows_p, g.ld_mask), dtype=torch.int32, device=W.device) if want_mask else None)
+        cps.append(P.c())
+    arr = lambda ty, xs: (ty * n)(*xs)
+    pw = arr(ctypes.c_void_p, [_ptr(W) for W in Ws])
+    lw = arr(ctypes.c_int64, [_ld(W) for W in Ws])
+    ps = arr(ctypes.c_void_p, [_ptr(s) for s in scores])
+    ls = arr(ctypes.c_int64, [_ld(s) if s is not None else 0 for s in scores])
+    po = arr(ctypes.c_void_p, [ctypes.cast(ctypes.pointer(cp), ctypes.c_void_p) for cp in cps])
+    pm = arr(ctypes.c_void_p, [_ptr(m) for m in masks])
+    _check(lib().vnm_prune_compress_batched(n, pw, lw, ps, ls, po, pm, _stream(Ws[0].device)),
+           "vnm_prune_compress_batched")
+    return (Ps, masks) if want_mask else Ps
 
 
 def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | None = None,

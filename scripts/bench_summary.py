@@ -13,7 +13,8 @@ for fn in sys.argv[1:]:
     print(fn, d["config"]["workload"], "value", d["value"], d["unit"], "ms", d["ms_per_step"],
           "roof", r.get("bound"), r.get("achieved"), r.get("unit"), r.get("frac"),
           "e2e", d.get("e2e", {}).get("value"), "clk", d.get("clocks", {}).get("sm_mhz"),
-          "vs_dense", det.get("speedup_vs_dense"), "vs_24", det.get("speedup_vs_24"))
+          "vs_dense", det.get("speedup_vs_dense"), "vs_24", det.get("speedup_vs_24"),
+          "prune_batched_us", det.get("prune_compress_batched_us"), det.get("prune_gbs"), "GB/s")
     for l in det.get("layers", []):
         print("   ", l["name"], f"spmm {l['spmm_us']}us {l['spmm_useful_tflops']}TF {l['spmm_gbs']}GB/s",
-              f"prune {l['prune_compress_us']}us {l['prune_gbs']}GB/s", "dense", l.get("dense_us"), "cslt", l.get("cslt_us"))
+              "dense", l.get("dense_us"), "cslt", l.get("cslt_us"))

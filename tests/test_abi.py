@@ -81,6 +81,15 @@ def test_status_codes_without_launch():
     assert L.vnm_compress(fake, 64, fake, ctypes.byref(g), ctypes.byref(P2), None, None) == vnm.VNM_ERR_SHAPE
     # T = 0 is a no-op
     assert L.vnm_spmm(fake, 16, 0, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_OK
+    # batched prune: n out of range / NULL arrays are argument errors; an entry's error is returned before launch
+    assert L.vnm_prune_compress_batched(0, None, None, None, None, None, None, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_prune_compress_batched(65, None, None, None, None, None, None, None) == vnm.VNM_ERR_ARG
+    Pg = vnm.CPacked(g, 1 << 20, 1 << 20, 1 << 20)
+    pw = (ctypes.c_void_p * 2)(fake, odd)
+    lw = (ctypes.c_int64 * 2)(64, 64)
+    po = (ctypes.c_void_p * 2)(ctypes.cast(ctypes.pointer(Pg), ctypes.c_void_p),
+                               ctypes.cast(ctypes.pointer(Pg), ctypes.c_void_p))
+    assert L.vnm_prune_compress_batched(2, pw, lw, None, None, po, None, None) == vnm.VNM_ERR_ALIGN
     for s in (0, -1, -2, -3, -4, -5):
         assert vnm.status_string(s)
 

@@ -162,3 +162,41 @@ def test_llama_scale_bitexact(V, M, kind):
     """Full-width weight (4096 x 4096-ish, ragged) through the V >= 32 kernel, every byte vs the oracle."""
     W = synth.weights(4160 if V <= 64 else 4096, 4100, seed=V * 31 + M, kind=kind)
     check(W, V, M)
+
+
+@pytest.mark.parametrize("shapes,V,M,tc", [
+    ([(1152, 384), (384, 384), (1536, 384), (384, 1536)], 64, 5, True),   # the DeiT-S layers (one launch)
+    ([(2304, 768), (768, 768), (3072, 768), (768, 3072)], 64, 8, True),   # DeiT-B
+    ([(70, 23), (128, 64), (200, 333)], 64, 7, False),                    # ragged
+    ([(256, 640), (128, 100)], 32, 6, True),
+    ([(96, 200), (40, 120)], 8, 9, False),                                # not the batched kernel: n launches
+])
+def test_batched_equals_single(shapes, V, M, tc):
+    """vnm_prune_compress_batched == one vnm_prune_compress per weight, byte for byte (masks, A_n, A_i1, A_i2,
+    window form), and the first weight == the oracle."""
+    Ws = [synth.weights(r, c, seed=r + 3 * c + M) for r, c in shapes]
+    Wd = [to_dev_bf16(W) for W in Ws]
+    Ps, masks = vnm.prune_compress_batched(Wd, V, M, want_mask=True, tc=tc)
+    for W, P, mk in zip(Wd, Ps, masks):
+        Q, mq = vnm.prune_compress(W, V, M, want_mask=True, tc=tc)
+        torch.cuda.synchronize()
+        assert torch.equal(mk, mq)
+        for a, b in zip(packed_np(P), packed_np(Q)):
+            assert np.array_equal(a, b)
+        if tc:
+            assert torch.equal(P.values_tc.view(torch.int16), Q.values_tc.view(torch.int16))
+            assert torch.equal(P.meta_tc, Q.meta_tc)
+    mask_ref = oracle.prune(Ws[0], V, M)
+    assert np.array_equal(u32(masks[0]), mask_ref)
+
+
+def test_batched_with_scores():
+    Ws = [synth.weights(r, c, seed=r + c) for r, c in [(256, 500), (192, 320)]]
+    Ss = [np.abs(synth.weights(r, c, seed=r * c)).astype(np.float32) * 3 for r, c in [(256, 500), (192, 320)]]
+    Ps = vnm.prune_compress_batched([to_dev_bf16(W) for W in Ws], 64, 6, scores=[to_dev_f32(S) for S in Ss])
+    torch.cuda.synchronize()
+    for W, S, P in zip(Ws, Ss, Ps):
+        mask_ref = oracle.prune(W, 64, 6, score=S)
+        st, v_ref, c_ref, m_ref = oracle.pack(W, mask_ref, 64, 6)
+        v, c, m = packed_np(P)
+        assert np.array_equal(v, v_ref) and np.array_equal(c, c_ref) and np.array_equal(m, m_ref)
