@@ -241,15 +241,33 @@ def run_gpu(args):
                 ev[i][2].record()
             gather(l)
 
+    # e2e: host->device copies on one stream, compute on the main stream, device->host on a third, chained by
+    # events per layer so the copies of layer i+1 / i-1 overlap the SpMM of layer i (PCIe is full duplex)
+    s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
     def step_e2e():
-        for l in layers:
-            l["W"].view(torch.int16).copy_(l["Wh"], non_blocking=True)
-            l["X"].view(torch.int16).copy_(l["Xh"], non_blocking=True)
+        ev_w, ev_x, ev_y = torch.cuda.Event(), [torch.cuda.Event() for _ in layers], [torch.cuda.Event() for _ in layers]
+        s_h2d.wait_stream(stream)
+        with torch.cuda.stream(s_h2d):
+            for l in layers:
+                l["W"].view(torch.int16).copy_(l["Wh"], non_blocking=True)
+            ev_w.record(s_h2d)
+            for i, l in enumerate(layers):
+                l["X"].view(torch.int16).copy_(l["Xh"], non_blocking=True)
+                ev_x[i].record(s_h2d)
+        stream.wait_event(ev_w)
         prune_all()
-        for l in layers:
+        s_d2h.wait_stream(stream)
+        for i, l in enumerate(layers):
+            stream.wait_event(ev_x[i])
             spmm(l)
             gather(l)
-            l["Yh"].copy_(l["Y"].view(torch.int16), non_blocking=True)
+            ev_y[i].record(stream)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_y[i])
+                l["Yh"].copy_(l["Y"].view(torch.int16), non_blocking=True)
+        stream.wait_stream(s_d2h)
+        stream.wait_stream(s_h2d)
 
     def barrier():
         torch.cuda.synchronize(dev)

@@ -19,7 +19,7 @@
 //    alternate 64-token chunks: a 4-warp epilogue could not keep up with the pair's store rate), one
 //    staging slot each.
 //
-// Roles: warp 0 TMA producer (both CTAs), warp 1 MMA (leader CTA, converged warp, elected lane), warps 4-11
+// Roles: warps 0 and 2 TMA producers (both CTAs), warp 1 MMA (leader CTA, converged warp, elected lane), warps 4-11
 // epilogue (both CTAs: TMEM lanes 32q.. = rows 32q.. of the CTA's 128-row tile).
 #include <cstdint>
 #include <cstdio>
@@ -39,7 +39,7 @@ constexpr uint32_t kABytes = 128 * 128;  // one 4-MMA chunk of A: 128 rows x 64 
 constexpr uint32_t kEBytes = 128 * 16;   // one 4-MMA chunk of metadata: 128 lanes x 4 words
 constexpr uint32_t kYSlot = 32 * 128;    // epilogue staging slot: 32 rows x 128 B (SW128)
 constexpr int kEpi = 8;                  // epilogue warps: 2 per TMEM lane quadrant, alternating token chunks
-constexpr int kThreads = 128 + 32 * kEpi;  // warps 0 TMA, 1 MMA, 2-3 idle, 4.. epilogue
+constexpr int kThreads = 128 + 32 * kEpi;  // warps 0 + 2 TMA, 1 MMA, 3 idle, 4.. epilogue
 
 struct Tc3Args {
     int32_t T, M;
@@ -54,6 +54,7 @@ struct Tc3Args {
     uint32_t ring_rows;  // S * rows_stage + 8 (shadow): rows per token-chunk region
     uint32_t stage_tx, shadow_tx;  // expect_tx bytes for both CTAs
     int32_t trace;
+    int32_t peek; // windows cross stage boundaries (5 <= M <= 7: an 8-channel window is wider than a block)
     int32_t epi;  // 1: Y^T written with coalesced st.global from a warp-private shared transpose; 0: TMA stores
     void* Y;
     int64_t ldy;
@@ -140,14 +141,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (warp == 0 || warp == 2) {
+        // ------------------------------------------------------------ TMA producers (both CTAs): warp 0 the
+        // resident A / metadata, the expect_tx and the 64-token box, warp 2 the narrower box — two issuing
+        // threads (one TMA-issuing thread capped the X^T stream, profiles/r01c_probes.md)
+        const int pb = warp / 2;
         if (lane == 0) {
             int q = 0, rp, tt;
             unsigned long long c_emp = 0, c0;
             for (int i = 0; tile3(a, cid, i, rp, tt); ++i) {
                 const int rt = 2 * rp + static_cast<int>(rank);  // row tiles past n_rt read as zeros (TMA OOB)
-                if (i == 0) {  // the pair's A and metadata, once
+                if (i == 0 && pb == 0) {  // the pair's A and metadata, once
                     const int rte = rt < a.n_rt ? rt : 0;
                     if (leader) mbar_arrive_expect_tx(res_full, 2 * a.n_chunk * (kABytes + kEBytes));
                     for (int c = 0; c < a.n_chunk; ++c) {
@@ -162,22 +166,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
                     c_emp += clock64() - c0;
                     if (a.abl & 4) {
-                        if (leader) mbar_arrive(&full[s]);
+                        if (leader && pb == 0) mbar_arrive(&full[s]);
                         continue;
                     }
-                    if (leader) mbar_arrive_expect_tx(&full[s], a.stage_tx + (s == 0 ? a.shadow_tx : 0u));
+                    // (box 1's bytes may land before box 0's thread registers the stage's expect_tx: the
+                    // phase still needs that arrival, and the transaction count is signed)
+                    if (leader && pb == 0) mbar_arrive_expect_tx(&full[s], a.stage_tx + (s == 0 ? a.shadow_tx : 0u));
                     const int y = st * a.rows_stage;
-                    uint8_t* dst = ring + static_cast<uint32_t>(s * a.rows_stage) * 128u;
-                    tma_load_2d_pair(dst, &tmap_b0, x0, y, &full[s]);
-                    tma_load_2d_pair(dst + region, &tmap_b1, x0 + 64, y, &full[s]);
+                    uint8_t* dst = ring + static_cast<uint32_t>(s * a.rows_stage) * 128u + pb * region;
+                    tma_load_2d_pair(dst, pb ? &tmap_b1 : &tmap_b0, x0 + 64 * pb, y, &full[s]);
                     if (s == 0) {  // the shadow after the last slot: a copy of slot 0's first 8 rows
-                        uint8_t* sh = ring + static_cast<uint32_t>(S * a.rows_stage) * 128u;
-                        tma_load_2d_pair(sh, &tmap_s0, x0, y, &full[s]);
-                        tma_load_2d_pair(sh + region, &tmap_s1, x0 + 64, y, &full[s]);
+                        uint8_t* sh = ring + static_cast<uint32_t>(S * a.rows_stage) * 128u + pb * region;
+                        tma_load_2d_pair(sh, pb ? &tmap_s1 : &tmap_s0, x0 + 64 * pb, y, &full[s]);
                     }
                 }
             }
-            if (a.trace) g_tc3_t[3][blockIdx.x] = c_emp;
+            if (a.trace && pb == 0) g_tc3_t[3][blockIdx.x] = c_emp;
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer (leader; converged warp)
@@ -204,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int s = q % S;
                     c0 = clock64();
                     mbar_wait(&full[s], (q / S) & 1);
-                    if (st + 1 < a.n_st) mbar_wait(&full[(q + 1) % S], ((q + 1) / S) & 1);  // window overhang
+                    if (a.peek && st + 1 < a.n_st) mbar_wait(&full[(q + 1) % S], ((q + 1) / S) & 1);  // window overhang
                     c_full += clock64() - c0;
                     tc_fence_after();
                     const int mi0 = st * a.ms;
@@ -467,6 +471,7 @@ int launch_spmm_tc3(const SpmmLaunch& L, cudaStream_t stream) {
     a.ms = g.M >= 7 ? 2 : 4;
     if (const char* e = getenv("VNM_TC3_MS")) a.ms = atoi(e) == 2 ? 2 : 4;
     a.n_st = (a.n_mma + a.ms - 1) / a.ms;
+    a.peek = g.M >= 5 && g.M <= 7;
     a.rows_stage = a.ms * (g.M == 4 ? 32 : 4 * g.M);
     int nt = 224;
     if (const char* e = getenv("VNM_TC3_NT")) nt = atoi(e);
