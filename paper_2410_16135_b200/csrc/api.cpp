@@ -254,9 +254,9 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         // row tiles at large T (DeiT-S qkv / fc1: profiles/r01c_probes.md); slower for M = 8 and 3-row-tile
         // layers, where the single-CTA kernel stays.
         const int n_mma = g->nb_pad / (g->M == 4 ? 8 : 4);
-        const bool tc3 = force ? force == 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192);
-        if (tc3) {
-            const int rc = vnm::launch_spmm_tc3(L, reinterpret_cast<cudaStream_t>(stream));
+        const bool tc3 = force ? force >= 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192);
+        if (tc3) {  // VNM_TC_PLAN=4: the same kernel with A streamed
+            const int rc = vnm::launch_spmm_tc3(L, force == 4 ? 0 : (force == 3 ? -1 : 1), reinterpret_cast<cudaStream_t>(stream));
             if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
         }
         const bool pair = force ? force == 2 : (n_stage >= 12 && n_rt % 2 == 0);

@@ -47,7 +47,8 @@ struct SpmmLaunch {
 int launch_spmm(const SpmmLaunch& L, cudaStream_t stream);
 int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream);   // window form (values_tc / meta_tc), 1 CTA
 int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream);  // window form on CTA pairs (M = 256)
-int launch_spmm_tc3(const SpmmLaunch& L, cudaStream_t stream);  // pairs, resident A, short K
+// pairs, K-ring; mode 1 resident A (short K), 0 streamed A, -1 resident when it fits (spmm_tc3.cu)
+int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream);
 int launch_pack_tc(const vnm_packed& P, cudaStream_t stream);
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 // small-T plan (spmm_pair.cu): T <= 32, V = 64, M <= 8

@@ -249,3 +249,34 @@ def test_decode_mma_sp_kernel_opt_in():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_pair_resident_kernel_forced():
+    """The CTA-pair resident-A kernel (spmm_tc3.cu) on every shape class it accepts — fp32 and bf16 Y^T, ragged
+    rows / K / tokens (T % 8 != 0 exercises the element-wise tail stores), every window-form M, V = 32 / 128 —
+    forced with VNM_TC_PLAN=3 in a child process (the plan switch is read at library load).  By default it only
+    runs for the DeiT-S-like shapes (test_deit_sampled covers that choice)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, oracle\n"
+        "from paper_2410_16135_b200 import synth, vnm\n"
+        "from tests.gpu_util import to_dev_bf16\n"
+        "cases = [(1536, 384, 64, 5, 1000, 'f32'), (1152, 384, 64, 5, 677, 'bf16'), (200, 333, 64, 6, 193, 'f32'),\n"
+        "         (70, 23, 64, 7, 65, 'bf16'), (384, 1000, 64, 8, 500, 'f32'), (256, 640, 64, 4, 300, 'bf16'),\n"
+        "         (256, 640, 32, 5, 301, 'f32'), (384, 770, 128, 8, 129, 'bf16'), (1000, 257, 64, 5, 2049, 'f32')]\n"
+        "for rows, cols, V, M, T, od in cases:\n"
+        "    W = synth.weights(rows, cols, seed=rows + T); XT = synth.activations_t(cols, T, seed=cols + T)\n"
+        "    mask = oracle.prune(W, V, M)\n"
+        "    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, mask, V, M))\n"
+        "    P = vnm.prune_compress(to_dev_bf16(W), V, M, tc=True)\n"
+        "    dt = torch.bfloat16 if od == 'bf16' else torch.float32\n"
+        "    Y = vnm.spmm(to_dev_bf16(XT), P, T=T, out_dtype=dt).float().cpu().numpy().astype(np.float64)\n"
+        "    tol = oracle.tolerance(Yref, Aref, y_is_bf16=(od == 'bf16'))\n"
+        "    assert np.all(np.abs(Y - Yref) <= tol), (rows, cols, V, M, T, od, float(np.max(np.abs(Y - Yref) - tol)))\n"
+        "print('ok')\n")
+    env = dict(os.environ, VNM_TC_PLAN="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
