@@ -210,8 +210,7 @@ def run_gpu(args):
         assert st == 0, vnm.status_string(st)
 
     for l in layers:  # split-K scratch (small T), allocated once outside the timed region
-        nws = vnm.spmm_workspace_bytes(l["P"].g, T)
-        l["ws"] = torch.empty(max(nws, 16) // 4, dtype=torch.float32, device=dev) if nws else None
+        l["ws"] = vnm.spmm_workspace(l["P"].g, T, dev)  # zero-initialised once; vnm_spmm leaves it zeroed
 
     def spmm(l):
         cp = l["P"].c()

@@ -145,11 +145,16 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
  * M = 128 sparse MMA, split-K); otherwise the gather kernel (M = 64 sparse MMAs on the 4 kept X^T rows of each
  * block, 16-byte cp.async gathers).
  * workspace: optional device scratch (16-B aligned) used by the small-T split-K plan; pass NULL/0 to
- * let the library choose a plan without it (vnm_spmm_workspace_bytes gives the size it can use).     */
+ * let the library choose a plan without it (vnm_spmm_workspace_bytes gives the size it can use).  Its
+ * completion flags must be zero when a call starts: zero it once with vnm_spmm_workspace_init (or allocate
+ * it zero-filled); every completed vnm_spmm call leaves it zeroed again, so one initialisation serves all
+ * later calls ordered on the stream (no per-call memset).  Re-initialise after a failed launch.      */
 vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,
                     vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T);
+/* Zero-fill a vnm_spmm workspace (asynchronous on stream).  VNM_ERR_ARG if ws is NULL with bytes > 0.     */
+vnm_status vnm_spmm_workspace_init(void* ws, size_t bytes, vnm_stream_t stream);
 
 /* ---- RIA importance: the score pre-pass for vnm_prune / vnm_prune_compress.
  * Eq. (1), §3 P:86-90:

@@ -274,6 +274,12 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+vnm_status vnm_spmm_workspace_init(void* ws, size_t bytes, vnm_stream_t stream) {
+    if (bytes == 0) return VNM_OK;
+    if (!ws) return VNM_ERR_ARG;
+    return cudaMemsetAsync(ws, 0, bytes, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? VNM_OK : VNM_ERR_CUDA;
+}
+
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T) {
     if (check_geom(g) != VNM_OK || T < 0) return 0;
     size_t dec = vnm::spmm_dec_applies(*g, T) ? vnm::spmm_dec_workspace_bytes(*g, T) : 0;

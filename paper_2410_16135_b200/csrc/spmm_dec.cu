@@ -46,7 +46,7 @@ struct DecArgs {
     void* YT;
     int64_t ldy;
     float* ws;          // [n_rg][n_st][64][16] fp32 partials of cut row groups
-    uint32_t* tickets;  // [n_rg] arrival counters, zeroed by the launch
+    uint32_t* tickets;  // [n_rg] arrival counters, zero at launch and left zero
     int32_t T, y_bf16, rows, V, M, nb_pad, n_ks;
     int32_t n_rg, n_st, units, grid;
     int32_t xrows;      // X^T rows staged per stage (multiple of 256 >= 128 M)
@@ -342,7 +342,8 @@ int launch_spmm_dec(const SpmmLaunch& L, cudaStream_t stream) {
         !encode_2d(&tx, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
                    p.tp, 256, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_NONE))
         return kLaunchCudaError;
-    cudaMemsetAsync(a.tickets, 0, static_cast<size_t>(p.n_rg) * 4, stream);
+    // tickets are zero at launch (the caller zero-fills the workspace once, vnm_spmm_workspace_init) and every
+    // launch leaves them zero (the last CTA of a row group clears its ticket)
     auto k = L.T <= 8 ? vnm_spmm_dec_kernel<1> : vnm_spmm_dec_kernel<2>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)) != cudaSuccess)
         return kLaunchCudaError;

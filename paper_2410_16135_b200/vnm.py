@@ -48,7 +48,7 @@ _lib = None
 
 EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress",
            "vnm_prune_compress_batched", "vnm_pack_tc",
-           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
+           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_spmm_workspace_init", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
            "vnm_permute_gain_workspace_bytes", "vnm_permute_gain", "vnm_status_string", "vnm_launch_count"]
 
 
@@ -81,6 +81,8 @@ def lib():
             L.vnm_spmm.restype = ctypes.c_int
             L.vnm_spmm_workspace_bytes.argtypes = [GP, i32]
             L.vnm_spmm_workspace_bytes.restype = sz
+            L.vnm_spmm_workspace_init.argtypes = [P, sz, P]
+            L.vnm_spmm_workspace_init.restype = ctypes.c_int
             L.vnm_act_norms.argtypes = [P, i64, i32, i32, P, P]
             L.vnm_act_norms.restype = ctypes.c_int
             L.vnm_ria_workspace_bytes.argtypes = [i32, i32]
@@ -284,7 +286,7 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
     if workspace is None:  # split-K scratch for the small-T plan (the library allocates no device memory)
         nws = spmm_workspace_bytes(g, T)
         if nws:
-            workspace = torch.empty(nws // 4, dtype=torch.float32, device=XT.device)
+            workspace = spmm_workspace(g, T, XT.device)
     ws_ptr, ws_bytes = (_ptr(workspace), workspace.numel() * workspace.element_size()) if workspace is not None \
         else (None, 0)
     _check(lib().vnm_spmm(_ptr(XT), XT.stride(0), T, ctypes.byref(cp), _ptr(out), out.stride(0), ydt, ws_ptr,
@@ -294,6 +296,17 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
 
 def spmm_workspace_bytes(g: Geom, T: int) -> int:
     return int(lib().vnm_spmm_workspace_bytes(ctypes.byref(g), T))
+
+
+def spmm_workspace(g: Geom, T: int, device) -> torch.Tensor | None:
+    """A vnm_spmm workspace for (g, T), initialised with vnm_spmm_workspace_init (zero flags; every vnm_spmm
+    call leaves it initialised, so it can be reused by later calls on the same stream).  None if not used."""
+    nws = spmm_workspace_bytes(g, T)
+    if not nws:
+        return None
+    ws = torch.empty(max(nws, 16) // 4, dtype=torch.float32, device=device)
+    _check(lib().vnm_spmm_workspace_init(_ptr(ws), ws.numel() * 4, _stream(device)), "vnm_spmm_workspace_init")
+    return ws
 
 
 def act_norms(XT: torch.Tensor, T: int | None = None) -> torch.Tensor:

@@ -16,9 +16,8 @@ if "w" in z: W = W * 0
 P = vnm.prune_compress(to_dev_bf16(W), 64, M, tc=tc)
 Xd = to_dev_bf16(X)
 Y = torch.empty((rows, (T + 7) // 8 * 8), dtype=torch.bfloat16, device="cuda")
-ws_n = vnm.spmm_workspace_bytes(P.g, T)
-ws = torch.empty(max(ws_n, 16) // 4, dtype=torch.float32, device="cuda")
-f = lambda: vnm.spmm(Xd, P, T=T, out=Y[:, :T], workspace=ws if ws_n else None)
+ws = vnm.spmm_workspace(P.g, T, "cuda")
+f = lambda: vnm.spmm(Xd, P, T=T, out=Y[:, :T], workspace=ws)
 for _ in range(3):
     f()
 torch.cuda.synchronize()
