@@ -123,7 +123,7 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
  * vnm_prune_compress call: W[i] / ldw[i] / score[i] (NULL: ABS) / lds[i] / out[i] (out[i]->g is the geometry)
  * / mask[i] (NULL: none).  Outputs are byte-identical to n separate calls.  1 <= n <= 8 weights sharing one
  * (V, M) run as one kernel when 32 <= V <= 128 and M <= 8; other batches run as n launches on `stream`.
- * Errors: VNM_ERR_ARG (n out of range, NULL arrays), else the first failing entry's status (nothing launched). */
+ * Errors: VNM_ERR_ARG (n < 1 or n > 64, NULL arrays), else the first failing entry's status (nothing launched). */
 vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const int64_t* ldw,
                                       const float* const* score, const int64_t* lds, vnm_packed* const* out,
                                       uint32_t* const* mask, vnm_stream_t stream);

@@ -530,7 +530,7 @@ int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream) {
         const vnm_geom& g = *Ls[i].g;
         if (g.V != V || g.M != M || L_unsupported(Ls[i])) return kLaunchUnsupported;
     }
-    static Batch B;  // host staging of the kernel parameters (copied at launch)
+    Batch B;  // host staging of the kernel parameters (copied into the launch; per call: thread-safe)
     B.n = n;
     B.tile0[0] = 0;
     B.any_score = B.any_mask = 0;
