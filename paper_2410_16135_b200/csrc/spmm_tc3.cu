@@ -40,7 +40,7 @@ namespace {
 
 constexpr uint32_t kABytes = 128 * 128;  // one 4-MMA chunk of A: 128 rows x 64 bf16 (SW128)
 constexpr uint32_t kEBytes = 128 * 16;   // one 4-MMA chunk of metadata: 128 lanes x 4 words
-constexpr uint32_t kYSlot = 32 * 128;    // epilogue transpose slot: 32 rows x 128 B (SW128)
+constexpr uint32_t kYSlot = 32 * 64;     // epilogue transpose slot: 32 rows x 64 B (half a 128-byte row chunk)
 constexpr int kEpi = 8;                  // epilogue warps
 constexpr int kThreads = 128 + 32 * kEpi;  // warps 0 + 2 TMA, 1 MMA, 3 idle, 4.. epilogue
 
@@ -100,13 +100,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = a.S;
     const int na = a.a_res ? a.n_chunk : S;  // A / metadata chunks held (resident: all; streaming: one per slot)
-    // [A: na x 16 KB][E: na x 2 KB, padded to 1 KB][X^T ring: 2 token chunks x ring_rows x 128 B]
-    // [transpose slots: kEpi x 4 KB][barriers]
+    // [A: na x 16 KB][E: na x 2 KB, padded to 1 KB (unless aliased)][X^T ring: 2 token chunks x ring_rows x 128 B]
+    // [transpose slots: kEpi x 2 KB][barriers]
+    // (resident mode: the metadata staging aliases the epilogue slots — it is read once by tcgen05.cp before the
+    // first MMA, and the epilogue first touches the slots after that tile's MMAs, i.e. after the copies, completed)
+    const bool e_alias = a.a_res && a.n_chunk * kEBytes <= kEpi * kYSlot;
     uint8_t* sA = smem;
-    uint8_t* sE = smem + na * kABytes;
-    uint8_t* ring = sE + (na * kEBytes + 1023) / 1024 * 1024;
+    uint8_t* ring = smem + na * kABytes + (e_alias ? 0u : (na * kEBytes + 1023) / 1024 * 1024);
     const uint32_t region = a.ring_rows * 128u;  // bytes per token-chunk region
     uint8_t* sY = ring + 2 * region;
+    uint8_t* sE = e_alias ? sY : smem + na * kABytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(sY + kEpi * kYSlot);
     uint64_t* empty = full + S;
     uint64_t* tmem_full = empty + S;       // [2]
@@ -301,38 +304,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         auto store = [&](int rt, int c, const uint32_t (&w)[32]) {
             const int t0 = tt * NT + c * kCw;
             if (rt >= a.n_rt || t0 >= a.T || (a.abl & 2)) return;
-            const uint32_t row = srow + lane * 128;
-            __syncwarp();  // the previous chunk's reads of the slot are done
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((k ^ lane) & 7) << 4)), "r"(w[4 * k]),
-                             "r"(w[4 * k + 1]), "r"(w[4 * k + 2]), "r"(w[4 * k + 3])
-                             : "memory");
-            __syncwarp();
             constexpr int kEl = kBf16 ? 8 : 4;  // elements per 16 bytes
-            const int cc = lane & 7, tok = t0 + cc * kEl;
             const int t_end = min(a.T, tt * NT + NT);
             const int grow0 = rt * 128 + 32 * qd;
+            // two halves of 64 B per row (the slot holds 32 rows x 64 B: chunk k of row r at k ^ ((r / 2) % 4),
+            // conflict-free both ways); read back 8 rows x 4 chunks per instruction
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int r = 4 * j + (lane >> 3);
-                uint32_t x0, x1, x2, x3;
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
-                             : "r"(srow + r * 128 + (((cc ^ r) & 7) << 4)));
-                const int grow = grow0 + r;
-                if (grow >= a.rows || tok >= t_end) continue;
-                uint8_t* dst = static_cast<uint8_t*>(a.Y) + (static_cast<int64_t>(grow) * a.ldy + tok) * (kBf16 ? 2 : 4);
-                if (tok + kEl <= t_end) {
-                    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(x0), "r"(x1), "r"(x2), "r"(x3)
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int th = t0 + h2 * (kCw / 2);
+                if (th >= t_end) break;
+                __syncwarp();  // the previous reads of the slot are done
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(srow + lane * 64 + (((k ^ (lane >> 1)) & 3) << 4)),
+                                 "r"(w[16 * h2 + 4 * k]), "r"(w[16 * h2 + 4 * k + 1]), "r"(w[16 * h2 + 4 * k + 2]),
+                                 "r"(w[16 * h2 + 4 * k + 3])
                                  : "memory");
-                } else {  // ragged token tail: element by element
-                    const uint32_t xs[4] = {x0, x1, x2, x3};
-                    for (int e = 0; e < t_end - tok; ++e) {
-                        if constexpr (kBf16)
-                            reinterpret_cast<uint16_t*>(dst)[e] = static_cast<uint16_t>(xs[e >> 1] >> (16 * (e & 1)));
-                        else
-                            reinterpret_cast<uint32_t*>(dst)[e] = xs[e];
+                __syncwarp();
+                const int cc = lane & 3, tok = th + cc * kEl;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = 8 * j + (lane >> 2);
+                    uint32_t x0, x1, x2, x3;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                 : "r"(srow + r * 64 + (((cc ^ (r >> 1)) & 3) << 4)));
+                    const int grow = grow0 + r;
+                    if (grow >= a.rows || tok >= t_end) continue;
+                    uint8_t* dst = static_cast<uint8_t*>(a.Y) + (static_cast<int64_t>(grow) * a.ldy + tok) * (kBf16 ? 2 : 4);
+                    if (tok + kEl <= t_end) {
+                        asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(x0), "r"(x1), "r"(x2), "r"(x3)
+                                     : "memory");
+                    } else {  // ragged token tail: element by element
+                        const uint32_t xs[4] = {x0, x1, x2, x3};
+                        for (int e = 0; e < t_end - tok; ++e) {
+                            if constexpr (kBf16)
+                                reinterpret_cast<uint16_t*>(dst)[e] = static_cast<uint16_t>(xs[e >> 1] >> (16 * (e & 1)));
+                            else
+                                reinterpret_cast<uint32_t*>(dst)[e] = xs[e];
+                        }
                     }
                 }
             }
@@ -395,7 +405,8 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     auto ebytes = [](int n) { return static_cast<uint32_t>(n * kEBytes + 1023) / 1024 * 1024; };
     const int pairs_all = num_sms() / 2;
     // resident A when the row pair's A + metadata fit next to >= 4 ring slots and every row pair gets a pair
-    const uint32_t res = static_cast<uint32_t>(a.n_chunk) * kABytes + ebytes(a.n_chunk);
+    const bool alias = a.n_chunk * kEBytes <= kEpi * kYSlot;  // resident metadata staged in the epilogue slots
+    const uint32_t res = static_cast<uint32_t>(a.n_chunk) * kABytes + (alias ? 0u : ebytes(a.n_chunk));
     a.a_res = want_res != 0 && pairs_all >= a.n_rp && kNacc * NT + 4 * a.n_chunk <= 512 &&
               res + 2u * (4 * a.rows_stage + 8) * 128u + fixed <= kMaxSmem;
     if (want_res == 1 && !a.a_res) return kLaunchUnsupported;
@@ -441,7 +452,8 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
         return kLaunchCudaError;
     const bool bf = L.y_dtype == VNM_BF16;
     const int na = a.a_res ? a.n_chunk : S;
-    const size_t smem = static_cast<size_t>(na) * kABytes + ebytes(na) + 2u * a.ring_rows * 128u + fixed;
+    const size_t smem = static_cast<size_t>(na) * kABytes + (a.a_res && alias ? 0u : ebytes(na)) +
+                        2u * a.ring_rows * 128u + fixed;
     auto k = bf ? vnm_spmm_tc3_kernel<NT, true> : vnm_spmm_tc3_kernel<NT, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
