@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    grid_dep_wait();    // the previous kernel's outputs (e.g. this layer's inputs) are visible
+    grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
 
     if (warp >= kGather0 && warp < kGather0 + kGatherWarps) {
         // ------------------------------------------------------------ gather + metadata image
@@ -511,9 +513,9 @@ int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t st) {
     }
     cudaError_t e = cudaFuncSetAttribute(vnm_spmm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) {
-        vnm_spmm_pair_kernel<<<a.grid, kThreads, smem, st>>>(ta, tm, tc, tx, a);
+        e = launch_pdl(true, vnm_spmm_pair_kernel, dim3(a.grid), dim3(kThreads), static_cast<size_t>(smem), st, ta, tm, tc, tx, a);
         count_launch();
-        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
     }
     if (e == cudaSuccess && a.trace) {
         static unsigned long long h[4][1024];

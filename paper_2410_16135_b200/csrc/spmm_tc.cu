@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    grid_dep_wait();    // the previous kernel's outputs (e.g. this layer's inputs) are visible
+    grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
@@ -276,9 +278,9 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
         return kLaunchCudaError;
     const int grid = a.work < num_sms() ? a.work : num_sms();
     a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
-    k<<<grid, kThreads, smem, stream>>>(ta, tb, ty, a);
+    cudaError_t e = launch_pdl(false, k, dim3(grid), dim3(kThreads), smem, stream, ta, tb, ty, a);
     count_launch();
-    return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
+    return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
 
 }  // namespace

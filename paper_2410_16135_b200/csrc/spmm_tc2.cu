@@ -168,6 +168,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    grid_dep_wait();    // the previous kernel's outputs (e.g. this layer's inputs) are visible
+    grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -379,9 +381,9 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
     }
     a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
     a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
-    k<<<2 * pairs, C::kThreads, smem, stream>>>(ta, tb, te, ty, a);
+    cudaError_t e = launch_pdl(false, k, dim3(2 * pairs), dim3(C::kThreads), smem, stream, ta, tb, te, ty, a);
     count_launch();
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && a.trace) {
         static unsigned long long h[8][160];
         cudaStreamSynchronize(stream);

@@ -154,6 +154,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    grid_dep_wait();    // the previous kernel's outputs (e.g. this layer's inputs) are visible
+    grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
 
     if (warp == 0 || warp == 2) {
         // ------------------------------------------------------------ TMA producers (both CTAs): warp 0 the
@@ -462,9 +464,9 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     a.Y = L.YT;
     a.ldy = L.ldy;
     a.rows = g.rows;
-    k<<<2 * pairs, kThreads, smem, stream>>>(ta, te, tb0, tb1, ts0, ts1, a);
+    cudaError_t e = launch_pdl(false, k, dim3(2 * pairs), dim3(kThreads), smem, stream, ta, te, tb0, tb1, ts0, ts1, a);
     count_launch();
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && a.trace) {
         static unsigned long long h[8][160];
         cudaStreamSynchronize(stream);

@@ -2,6 +2,8 @@
 // (no libcuda link dependency) and the SM count.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -31,6 +33,28 @@ inline int num_sms() {
         return v;
     }();
     return n;
+}
+
+// Kernel launch, with programmatic stream serialization (PDL) when `pdl`: the kernel may start while the
+// previous kernel on the stream drains; it calls grid_dep_wait() (ptx.cuh) before touching global memory.
+// Measured (profiles/r01d_*): PDL helps the short small-T launches (decode step -3 %) and hurts the window-form
+// SpMMs of the DeiT step (+6 %), so only the small-T plan asks for it.  VNM_PDL=0 / 1 forces it off / on.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool want, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    static const int force = [] { const char* e = getenv("VNM_PDL"); return e ? (e[0] == '0' ? 0 : 1) : -1; }();
+    const bool pdl = force < 0 ? want : force == 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 inline bool encode_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
