@@ -144,7 +144,7 @@ def run_gpu(args):
     # ---- synthetic inputs (host, seeded per rank), then resident copies in HBM
     layers = []
     out_mode = args.mode == "out"
-    use_tc0 = T > 64 and M <= 8 and V == 64
+    use_tc0 = T > 64 and (M <= 8 or M % 4 == 0) and V == 64
     for li, (name, rows_full, cols) in enumerate(wl["layers"]):
         # token mode: every rank its own tokens (seeded per rank) and a full weight; out mode: the same weight
         # and tokens on every rank, rank r owns a V-block-aligned row shard (whole 128-row tiles for the
@@ -189,7 +189,7 @@ def run_gpu(args):
 
     import ctypes
 
-    use_tc = T > 64 and M <= 8 and V == 64
+    use_tc = T > 64 and (M <= 8 or M % 4 == 0) and V == 64
     if use_tc:  # window-form buffers, written by vnm_prune_compress in the same pass (include/vnm.h)
         for l in layers:
             nv, nm = vnm.tc_bytes(l["P"].g)

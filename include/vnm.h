@@ -81,7 +81,11 @@ typedef struct {
      * blocks per MMA, n_mma_w = nb_pad/bpm, n_stage_w = ceil(n_mma_w/4)):
      *   values_tc bf16 [rows_w][16*n_mma_w]       4 values per block (M >= 5: lo pair, hi pair); = A_n for M = 4
      *   meta_tc   u32  [rows_w/128][n_stage_w][128][4]   2:4 metadata of MMA (stage*4 + k) in the M = 128
-     *             TMEM lane order (lane L holds rows (L%8)+16(L/16) and +8, K-groups 4((L/8)%2)..+3).     */
+     *             TMEM lane order (lane L holds rows (L%8)+16(L/16) and +8, K-groups 4((L/8)%2)..+3).
+     * For M % 4 == 0 with M > 8 (e.g. 64:2:16) the tensor-core form is the NATURAL 2:4 form instead: a
+     * block is a whole number of 4-channel groups, so each group holds at most the row's 2 nonzeros and the
+     * masked W is 2:4-sparse in channel order; values_tc / meta_tc are the M = 4 layouts above over the
+     * groups (2 values per group, zero-completed; nb_pad -> ceil(cols_p/4 / 8)*8 groups).              */
     uint16_t* values_tc;
     uint32_t* meta_tc;
 } vnm_packed;
@@ -113,7 +117,8 @@ vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, co
                         vnm_packed* out, int32_t* d_status, vnm_stream_t stream);
 
 /* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.
- * If out->values_tc / out->meta_tc are set (32 <= V <= 128, M <= 8) the window form is written in the same pass
+ * If out->values_tc / out->meta_tc are set (32 <= V <= 128, and M <= 8 or M % 4 == 0) the tensor-core form is
+ * written too: the window form in the same pass (M <= 8), the natural 2:4 form by a second launch (M % 4 == 0)
  * (identical to vnm_pack_tc of the result).                                                             */
 vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
                               const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
@@ -129,7 +134,8 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
                                       uint32_t* const* mask, vnm_stream_t stream);
 
 /* Fill P->values_tc / P->meta_tc (caller-allocated, vnm_bytes 4 / 5) from the canonical A_n / A_i1 / A_i2
- * of P.  VNM_ERR_UNSUPPORTED unless 32 <= V <= 128 and 4 <= M <= 8; VNM_ERR_ARG if a tc pointer is NULL.       */
+ * of P.  VNM_ERR_UNSUPPORTED unless 32 <= V <= 128 and (M <= 8 or M % 4 == 0); VNM_ERR_ARG if a tc pointer
+ * is NULL.                                                                                            */
 vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
 
 /* The V:N:M SpMM (App. A):  Y^T[o][t] = sum_k W'[o][k] * X^T[k][t],  W' = unpack(P).
@@ -139,8 +145,8 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
  *       ldy % 8 == 0, ldy >= T; only rows < g.rows and columns < T are written.
  * bf16 x bf16 products, fp32 accumulation on the sparse tensor cores (tcgen05.mma.sp).
  * Supported: V == 64 (any M), and any 32 <= V <= 128 (e.g. the paper's 128:2:M) when the
- * window form is present (4 <= M <= 8); VNM_ERR_UNSUPPORTED otherwise.
- * Plans: window form present and T > 64 (or V != 64) -> window-form kernel on CTA pairs (dense X^T tiles by
+ * tensor-core form is present (M <= 8, or M % 4 == 0); VNM_ERR_UNSUPPORTED otherwise.
+ * Plans: tensor-core form present and T > 64 (or V != 64) -> window-form kernel on CTA pairs (dense X^T tiles by
  * TMA, tcgen05.mma.sp.cta_group::2 with M = 256); V = 64, T <= 32, M <= 8 -> small-T kernel (two V-blocks per
  * M = 128 sparse MMA, split-K); otherwise the gather kernel (M = 64 sparse MMAs on the 4 kept X^T rows of each
  * block, 16-byte cp.async gathers).

@@ -91,6 +91,22 @@ vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_ge
     return VNM_OK;
 }
 
+// Natural 2:4 tensor-core form (M % 4 == 0, M > 8; include/vnm.h): the masked W is 2:4-sparse in the natural
+// channel order, so the window-form kernels run it as the M = 4 layout over 4-channel groups.
+static bool nat24(const vnm_geom* g) { return g->M > 8 && g->M % 4 == 0 && g->V >= 32 && g->V <= 128; }
+// the tensor-core form applies: window form (M <= 8) or natural 2:4 form
+static bool tc_geom(const vnm_geom* g) { return g->V >= 32 && g->V <= 128 && (g->M <= 8 || g->M % 4 == 0); }
+// the M = 4 view of a natural-2:4 geometry: blocks = 4-channel groups
+static vnm_geom view4(const vnm_geom& g) {
+    vnm_geom v = g;
+    v.M = 4;
+    v.nb = g.cols_p / 4;
+    v.nb_pad = (v.nb + 7) / 8 * 8;
+    v.ld_val = 2 * v.nb_pad;
+    v.ld_meta = v.nb_pad / 8;
+    return v;
+}
+
 size_t vnm_bytes(const vnm_geom* g, int which) {
     if (check_geom(g) != VNM_OK) return 0;
     const size_t rp = static_cast<size_t>(g->rows_p);
@@ -101,10 +117,11 @@ size_t vnm_bytes(const vnm_geom* g, int which) {
         case 3: return rp * static_cast<size_t>(g->ld_mask) * 4;
         case 4:
         case 5: {
-            if (g->V < 32 || g->V > 128 || g->M > 8) return 0;
+            if (!tc_geom(g)) return 0;
             const size_t rows_w = (rp + 127) / 128 * 128;
-            const size_t bpm = g->M == 4 ? 8 : 4;
-            const size_t n_mma = static_cast<size_t>(g->nb_pad) / bpm;
+            const vnm_geom gv = nat24(g) ? view4(*g) : *g;
+            const size_t bpm = gv.M == 4 ? 8 : 4;
+            const size_t n_mma = static_cast<size_t>(gv.nb_pad) / bpm;
             const size_t n_stage = (n_mma + 3) / 4;
             return which == 4 ? rows_w * 16 * n_mma * 2 : rows_w / 128 * n_stage * 128 * 4 * 4;
         }
@@ -155,14 +172,18 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
     if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
     if (!W) return VNM_ERR_ARG;
     vnm::PruneLaunch L{g, W, ldw, score, lds, nullptr, mask, out->values, out->col_idx, out->meta, nullptr};
-    if (out->values_tc || out->meta_tc) {  // fused window form (include/vnm.h), V >= 32 and M <= 8 only
-        if (g->V < 32 || g->V > 128 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (out->values_tc || out->meta_tc) {  // tensor-core form (include/vnm.h): fused window form (M <= 8) or
+        if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;  // the natural 2:4 form packed after the pass (M % 4 == 0)
         if (!out->values_tc || !out->meta_tc) return VNM_ERR_ARG;
         if (!aligned16(out->values_tc) || !aligned16(out->meta_tc)) return VNM_ERR_ALIGN;
-        L.values_tc = out->values_tc;
-        L.meta_tc = out->meta_tc;
+        if (!nat24(g)) {
+            L.values_tc = out->values_tc;
+            L.meta_tc = out->meta_tc;
+        }
     }
-    return from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
+    const vnm_status st = from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
+    if (st || !out->values_tc || !nat24(g)) return st;
+    return from_launch(vnm::launch_pack_nat24(*out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const int64_t* ldw,
@@ -188,25 +209,36 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
         if (!W[i]) return VNM_ERR_ARG;
         vnm::PruneLaunch L{g, W[i], ldw[i], sc, ls, nullptr, mk, out[i]->values, out[i]->col_idx, out[i]->meta, nullptr};
         if (out[i]->values_tc || out[i]->meta_tc) {
-            if (g->V < 32 || g->V > 128 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+            if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;
             if (!out[i]->values_tc || !out[i]->meta_tc) return VNM_ERR_ARG;
             if (!aligned16(out[i]->values_tc) || !aligned16(out[i]->meta_tc)) return VNM_ERR_ALIGN;
-            L.values_tc = out[i]->values_tc;
-            L.meta_tc = out[i]->meta_tc;
+            if (!nat24(g)) {
+                L.values_tc = out[i]->values_tc;
+                L.meta_tc = out[i]->meta_tc;
+            }
         }
         if (live > 0 && (g->V != Ls[0].g->V || g->M != Ls[0].g->M)) same = false;
         Ls[live++] = L;
     }
     if (live == 0) return VNM_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    bool done = false;
     if (same && live <= 8) {
         const int rc = vnm::launch_prune2_batch(Ls, live, st);
-        if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
+        if (rc != vnm::kLaunchUnsupported) {
+            if (rc) return from_launch(rc);
+            done = true;
+        }
     }
-    for (int i = 0; i < live; ++i) {
+    for (int i = 0; i < live && !done; ++i) {
         const vnm_status s = from_launch(vnm::launch_prune_pack(Ls[i], st));
         if (s) return s;
     }
+    for (int i = 0; i < n; ++i)  // natural 2:4 tensor-core forms, packed after the pass
+        if (out[i]->values_tc && nat24(&out[i]->g) && out[i]->g.rows_p > 0 && out[i]->g.nb_pad > 0) {
+            const vnm_status s = from_launch(vnm::launch_pack_nat24(*out[i], st));
+            if (s) return s;
+        }
     return VNM_OK;
 }
 
@@ -216,10 +248,11 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream) {
     vnm_status s = check_geom(g);
     if (s) return s;
     if ((s = check_packed(P, g))) return s;
-    if (g->V < 32 || g->V > 128 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;
     if (g->rows_p == 0 || g->nb_pad == 0) return VNM_OK;
     if (!P->values_tc || !P->meta_tc) return VNM_ERR_ARG;
     if (!aligned16(P->values_tc) || !aligned16(P->meta_tc)) return VNM_ERR_ALIGN;
+    if (nat24(g)) return from_launch(vnm::launch_pack_nat24(*P, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_pack_tc(*P, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -232,8 +265,9 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     if ((s = check_packed(P, g))) return s;
     if (y_dtype != VNM_F32 && y_dtype != VNM_BF16) return VNM_ERR_ARG;
     if (T < 0 || ldx < T || ldy < T) return VNM_ERR_SHAPE;
-    // window form: 32 <= V <= 128 with M <= 8 (rows are independent in it); gather / small-T plans: V = 64
-    const bool tc_form = P->values_tc && P->meta_tc && g->V >= 32 && g->V <= 128 && g->M <= 8;
+    // tensor-core form: 32 <= V <= 128 with M <= 8 (window form) or M % 4 == 0 (natural 2:4 form; the kernels
+    // see its M = 4 view); gather / small-T plans: V = 64
+    const bool tc_form = P->values_tc && P->meta_tc && tc_geom(g);
     if (g->V != 64 && !tc_form) return VNM_ERR_UNSUPPORTED;
     if (T == 0 || g->rows == 0) return VNM_OK;
     if (!YT) return VNM_ERR_ARG;
@@ -243,6 +277,13 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     vnm::SpmmLaunch L{P, XT, ldx, T, YT, ldy, y_dtype, workspace, workspace ? workspace_bytes : 0};
     const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || g->V != 64);
     if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
+    vnm_packed Pv;
+    if (tc && nat24(g)) {  // the natural 2:4 form runs as the M = 4 layout over 4-channel groups
+        Pv = *P;
+        Pv.g = view4(*g);
+        L.P = &Pv;
+        g = &Pv.g;
+    }
     if (tc) {
         // Measured (profiles/r01b_*): the CTA-pair kernel wins for long K with an even number of 128-row tiles
         // (Llama layers, DeiT-B fc2) — tensor-bound; the single-CTA kernel wins for short K / HBM-bound shapes

@@ -50,6 +50,7 @@ int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream);  // window form o
 // pairs, K-ring; mode 1 resident A (short K), 0 streamed A, -1 resident when it fits (spmm_tc3.cu)
 int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream);
 int launch_pack_tc(const vnm_packed& P, cudaStream_t stream);
+int launch_pack_nat24(const vnm_packed& P, cudaStream_t stream);  // M % 4 == 0, M > 8: natural 2:4 form
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 // small-T plan (spmm_pair.cu): T <= 32, V = 64, M <= 8
 bool spmm_pair_applies(const vnm_geom& g, int32_t T);

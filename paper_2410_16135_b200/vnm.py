@@ -170,13 +170,19 @@ class Packed:
                       torch.empty((g.rows_p, g.ld_meta), dtype=torch.int32, device=device))
 
 
+def tc_applies(V: int, M: int) -> bool:
+    """The tensor-core form exists for this (V, M): window form (M <= 8) or natural 2:4 form (M % 4 == 0)."""
+    return 32 <= V <= 128 and (M <= 8 or M % 4 == 0)
+
+
 def tc_bytes(g: Geom) -> tuple[int, int]:
     L = lib()
     return int(L.vnm_bytes(ctypes.byref(g), 4)), int(L.vnm_bytes(ctypes.byref(g), 5))
 
 
 def pack_tc(P: Packed) -> Packed:
-    """Fill the tensor-core window form of P (allocating it on P's device); 32 <= V <= 128, 4 <= M <= 8 only."""
+    """Fill the tensor-core form of P (allocating it on P's device): the window form for 4 <= M <= 8, the
+    natural 2:4 form for M % 4 == 0 (include/vnm.h); 32 <= V <= 128 only."""
     _require_cuda(P.values)
     nv, nm = tc_bytes(P.g)
     if nv == 0:
@@ -217,12 +223,12 @@ def compress(W: torch.Tensor, mask: torch.Tensor, V: int, M: int, status: torch.
 def prune_compress(W: torch.Tensor, V: int, M: int, score: torch.Tensor | None = None, want_mask: bool = False,
                    tc: bool = False):
     """Fused S_{V:N:M} + compression in one pass over W.  Returns Packed (and the mask if asked); with tc=True
-    the tensor-core window form is also filled in the same pass when it applies (32 <= V <= 128, M <= 8)."""
+    the tensor-core form is also filled when it applies (32 <= V <= 128; M <= 8 or M % 4 == 0)."""
     W = _as_bits16(W)
     _require_cuda(W, score)
     g = geometry(W.shape[0], W.shape[1], V, M)
     P = Packed.empty(g, W.device)
-    if tc and 32 <= V <= 128 and M <= 8:
+    if tc and tc_applies(V, M):
         nv, nm = tc_bytes(g)
         P.values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=W.device)
         P.meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=W.device)
@@ -246,7 +252,7 @@ def prune_compress_batched(Ws: list, V: int, M: int, scores: list | None = None,
     for W in Ws:
         g = geometry(W.shape[0], W.shape[1], V, M)
         P = Packed.empty(g, W.device)
-        if tc and 32 <= V <= 128 and M <= 8:
+        if tc and tc_applies(V, M):
             nv, nm = tc_bytes(g)
             P.values_tc = torch.empty(nv // 2, dtype=torch.bfloat16, device=W.device)
             P.meta_tc = torch.empty(nm // 4, dtype=torch.int32, device=W.device)

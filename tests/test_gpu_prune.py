@@ -200,3 +200,48 @@ def test_batched_with_scores():
         st, v_ref, c_ref, m_ref = oracle.pack(W, mask_ref, 64, 6)
         v, c, m = packed_np(P)
         assert np.array_equal(v, v_ref) and np.array_equal(c, c_ref) and np.array_equal(m, m_ref)
+
+
+@pytest.mark.parametrize("V", [64, 128])
+@pytest.mark.parametrize("rows,cols,M", [(256, 640, 16), (200, 333, 12), (130, 4096, 16), (64, 96, 32)])
+def test_natural_24_form_pack(V, rows, cols, M):
+    """M % 4 == 0, M > 8: vnm_prune_compress(tc) == vnm_pack_tc of its canonical output, and the natural 2:4
+    form holds exactly the masked weights: 2 values per 4-channel group, zero-completed (values_tc rows read
+    back through the group nibbles == the oracle's masked W)."""
+    W = synth.weights(rows, cols, seed=rows + cols + M + V)
+    Wd = to_dev_bf16(W)
+    P = vnm.prune_compress(Wd, V, M, tc=True)
+    Q = vnm.prune_compress(Wd, V, M)
+    vnm.pack_tc(Q)
+    batched = vnm.prune_compress_batched([Wd, Wd], V, M, tc=True)
+    torch.cuda.synchronize()
+    for R in (Q, *batched):
+        assert torch.equal(P.values_tc.view(torch.int16), R.values_tc.view(torch.int16))
+        assert torch.equal(P.meta_tc, R.meta_tc)
+    # decode the M = 4 view on the host: values_tc [rows_w][2*ng_pad] with the group nibbles in meta_tc's
+    # lane order (lane L: rows (L%8)+16(L/16) and +8, half h = (L/8)%2 of the 8 group nibbles of MMA k)
+    g = P.g
+    ng_pad = (g.cols_p // 4 + 7) // 8 * 8
+    n_mma = ng_pad // 8
+    n_stage = (n_mma + 3) // 4
+    rows_w = (g.rows_p + 127) // 128 * 128
+    vals = P.values_tc.view(torch.int16).cpu().numpy().view(np.uint16).reshape(rows_w, 2 * ng_pad)
+    mt = P.meta_tc.cpu().numpy().view(np.uint32).reshape(rows_w // 128, n_stage, 128, 4)
+    dense = np.zeros((rows_w, 4 * ng_pad), np.uint16)
+    for r in range(rows_w):
+        t, rr = divmod(r, 128)
+        j = 0 if (rr % 16) < 8 else 1  # bits 0-15 / 16-31 of the lane word
+        for q in range(ng_pad):
+            mi, gi = divmod(q, 8)
+            st, k = divmod(mi, 4)
+            h = gi // 4
+            lane = (rr % 8) + 16 * (rr // 16) + 8 * h
+            word = int(mt[t, st, lane, k])
+            nib = (word >> (16 * j + 4 * (gi % 4))) & 0xF
+            pa, pb = nib & 3, nib >> 2
+            dense[r, 4 * q + pa] = vals[r, 2 * q]
+            dense[r, 4 * q + pb] = vals[r, 2 * q + 1]
+    mask = oracle.prune(W, V, M)
+    Wm = oracle.apply_mask(W, mask, V, M)
+    assert np.array_equal(dense[:rows, :cols], Wm)
+    assert not dense[rows:].any() and not dense[:, cols:].any()

@@ -265,7 +265,8 @@ def test_pair_resident_kernel_forced():
         "from tests.gpu_util import to_dev_bf16\n"
         "cases = [(1536, 384, 64, 5, 1000, 'f32'), (1152, 384, 64, 5, 677, 'bf16'), (200, 333, 64, 6, 193, 'f32'),\n"
         "         (70, 23, 64, 7, 65, 'bf16'), (384, 1000, 64, 8, 500, 'f32'), (256, 640, 64, 4, 300, 'bf16'),\n"
-        "         (256, 640, 32, 5, 301, 'f32'), (384, 770, 128, 8, 129, 'bf16'), (1000, 257, 64, 5, 2049, 'f32')]\n"
+        "         (256, 640, 32, 5, 301, 'f32'), (384, 770, 128, 8, 129, 'bf16'), (1000, 257, 64, 5, 2049, 'f32'),\n"
+        "         (512, 1000, 64, 16, 300, 'bf16'), (256, 333, 64, 12, 129, 'f32')]\n"
         "for rows, cols, V, M, T, od in cases:\n"
         "    W = synth.weights(rows, cols, seed=rows + T); XT = synth.activations_t(cols, T, seed=cols + T)\n"
         "    mask = oracle.prune(W, V, M)\n"
@@ -280,3 +281,21 @@ def test_pair_resident_kernel_forced():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("V", [64, 32, 128])
+@pytest.mark.parametrize("rows,cols,T,M", [(256, 640, 300, 16), (200, 333, 65, 12), (384, 1000, 129, 16),
+                                           (130, 4096, 256, 16), (64, 50, 100, 32)])
+def test_natural_24_form(V, rows, cols, T, M):
+    """M % 4 == 0, M > 8 (e.g. the 64:2:16 point of BJ config 5): the masked W is 2:4-sparse in channel order,
+    and vnm_spmm runs its natural 2:4 tensor-core form through the window-form kernels (M = 4 view)."""
+    W, XT, Wm = make(rows, cols, V, M, T, seed=V + rows + cols + M + T)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, V, M, T, tc=True), Yref, Aref)
+    assert_within(gpu_y(W, XT, V, M, T, out_dtype=torch.bfloat16, tc=True), Yref, Aref, bf16=True)
+
+
+@pytest.mark.parametrize("rows,cols", [(11008, 4096), (4096, 11008)])
+def test_llama_m16_sampled(rows, cols):
+    """BJ config 5 at M = 16, T = 2048 through the natural 2:4 form (sampled rows against the oracle)."""
+    sampled_check(rows, cols, 16, 2048, seed=rows + cols + 16, out_dtype=torch.bfloat16, tc=True)
