@@ -90,6 +90,14 @@ def test_status_codes_without_launch():
     po = (ctypes.c_void_p * 2)(ctypes.cast(ctypes.pointer(Pg), ctypes.c_void_p),
                                ctypes.cast(ctypes.pointer(Pg), ctypes.c_void_p))
     assert L.vnm_prune_compress_batched(2, pw, lw, None, None, po, None, None) == vnm.VNM_ERR_ALIGN
+    # workspace init: nothing to do for 0 bytes; NULL with bytes is an argument error (no launch)
+    assert L.vnm_spmm_workspace_init(None, 0, None) == vnm.VNM_OK
+    assert L.vnm_spmm_workspace_init(None, 64, None) == vnm.VNM_ERR_ARG
+    # the tensor-core form exists for M <= 8 (window) and M % 4 == 0 (natural 2:4), not for M = 9 / 13
+    for M, has in [(5, True), (8, True), (12, True), (16, True), (9, False), (13, False)]:
+        gm = vnm.geometry(256, 1000, 64, M)
+        assert (L.vnm_bytes(ctypes.byref(gm), 4) > 0) == has and (L.vnm_bytes(ctypes.byref(gm), 5) > 0) == has
+        assert vnm.tc_applies(64, M) == has
     for s in (0, -1, -2, -3, -4, -5):
         assert vnm.status_string(s)
 
