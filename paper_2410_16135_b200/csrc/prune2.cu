@@ -60,8 +60,10 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define PTRACE(k) \
-    if (a.trace && blockIdx.x == 0 && it == 0 && threadIdx.x == 0) g_prune2_t[k] = gtime();
+#define PTRACE(k)                                                                \
+    if (a.trace) {  /* uniform: no timer read (or its predicated issue) when off */ \
+        if (blockIdx.x == 0 && it == 0 && threadIdx.x == 0) g_prune2_t[k] = gtime(); \
+    }
 
 __device__ __forceinline__ float bf16_to_f32_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_to_f32_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
     uint8_t* sNib = reinterpret_cast<uint8_t*>(sBits + (B.any_mask ? V * kCB : 0));  // [V][kCB] A_i2 nibbles
     uint8_t* sTcn = sNib + V * kCB;                                                   // [V][kCB] window nibbles
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int3 sInfo[2];  // (problem, column tile, row tile) of the tile in each buffer, set by its issuer
 
     const int ntiles = B.tile0[B.n];
     auto problem = [&](int tile) {
@@ -117,10 +120,13 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
         while (p + 1 < B.n && tile >= B.tile0[p + 1]) ++p;
         return p;
     };
+    // one thread decodes the tile (problem lookup, 2-D split) for everyone: it writes sInfo[bi] before its
+    // arrive on bar[bi], and the other threads read it after their wait on bar[bi] (release / acquire)
     auto issue = [&](int tile, int bi) {
         const int p = problem(tile), lt = tile - B.tile0[p];
         const Prune2Args& ap = B.a[p];
         const int ntx = (ap.nb_pad + kCB - 1) / kCB, bx = lt % ntx, by = lt / ntx;
+        sInfo[bi] = make_int3(p, bx, by);
         uint8_t* dst = smem + bi * buf_bytes;
         mbar_arrive_expect_tx(&bar[bi], kWBytes + (ap.has_score ? kSBytes : 0));
         tma_load_2d(dst, &B.tm[p].w, bx * kCB * M, by * V, &bar[bi]);
@@ -152,16 +158,15 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
     }
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int bi = it & 1;
-        const int p = problem(tile), lt = tile - B.tile0[p];
-        const Prune2Args& a = B.a[p];
-        const Maps& tm = B.tm[p];
-        const bool has_score = a.has_score, tc = a.has_tc;
-        const int ntx = (a.nb_pad + kCB - 1) / kCB;
-        const int bx = lt % ntx, by = lt / ntx;
-        const int b0 = bx * kCB, r0 = by * V;
         // prefetch the next tile into the other buffer (its previous contents were consumed last iteration)
         if (threadIdx.x == 0 && tile + static_cast<int>(gridDim.x) < ntiles) issue(tile + gridDim.x, bi ^ 1);
         mbar_wait(&bar[bi], (it >> 1) & 1);
+        const int3 info = sInfo[bi];
+        const int p = info.x, bx = info.y, by = info.z;
+        const Prune2Args& a = B.a[p];
+        const Maps& tm = B.tm[p];
+        const bool has_score = a.has_score, tc = a.has_tc;
+        const int b0 = bx * kCB, r0 = by * V;
         PTRACE(1)
         const uint32_t* sW = reinterpret_cast<const uint32_t*>(smem + bi * buf_bytes);
         const float* sS = reinterpret_cast<const float*>(smem + bi * buf_bytes + kWBytes);
