@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
         const uint16_t* wcol = reinterpret_cast<const uint16_t*>(sW) + b * M + warp * TC;
         const float* scol = sS + b * M + warp * TC;
         uint32_t upos = 0;  // kept positions chosen by some row
-#pragma unroll 4
+#pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int r = warp + kWarps * i;
             const uint16_t* wr = wcol + kWarps * i * TC;
