@@ -245,3 +245,17 @@ def test_natural_24_form_pack(V, rows, cols, M):
     Wm = oracle.apply_mask(W, mask, V, M)
     assert np.array_equal(dense[:rows, :cols], Wm)
     assert not dense[rows:].any() and not dense[:, cols:].any()
+
+
+def test_batched_more_than_eight():
+    """More than 8 weights (or mixed (V, M)) run as one launch per weight — same bytes as single calls."""
+    shapes = [(64 + 8 * i, 40 + 16 * i) for i in range(10)]
+    Ws = [to_dev_bf16(synth.weights(r, c, seed=r * c)) for r, c in shapes]
+    Ps = vnm.prune_compress_batched(Ws, 64, 6, tc=True)
+    for W, P in zip(Ws, Ps):
+        Q = vnm.prune_compress(W, 64, 6, tc=True)
+        torch.cuda.synchronize()
+        for a, b in zip(packed_np(P), packed_np(Q)):
+            assert np.array_equal(a, b)
+        assert torch.equal(P.values_tc.view(torch.int16), Q.values_tc.view(torch.int16))
+        assert torch.equal(P.meta_tc, Q.meta_tc)
