@@ -246,7 +246,7 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
     a.n_tt = (L.T + NT - 1) / NT;
     a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
-    const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // rows one stage's windows touch
+    const int need = g.M == 4 ? 128 : 15 * g.M + 8;  // rows one stage's windows touch (block 15: 15M .. 15M+7)
     a.rb = (need + 7) / 8 * 8;
     a.b_stage_bytes = static_cast<uint32_t>(kChunks * a.rb * 128);
     a.stage_bytes = RT * (kABytes + kEBytes) + a.b_stage_bytes;

@@ -413,7 +413,7 @@ int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
     a.n_rt = (g.rows_p + 127) / 128;
     a.n_rp = (a.n_rt + 1) / 2;
     a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
-    const int need = g.M == 4 ? 128 : 16 * g.M + 8;  // X^T rows one stage's windows touch
+    const int need = g.M == 4 ? 128 : 15 * g.M + 8;  // X^T rows one stage's windows touch (block 15: 15M .. 15M+7)
     a.rb = (need + 7) / 8 * 8;
     a.b_bytes = static_cast<uint32_t>(2 * a.rb * 128);
     // long K: 256-token tiles, one accumulator (the per-tile hand-off is amortised over many stages);
