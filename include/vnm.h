@@ -146,15 +146,18 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
  * bf16 x bf16 products, fp32 accumulation on the sparse tensor cores (tcgen05.mma.sp).
  * Supported: V == 64 (any M), and any 32 <= V <= 128 (e.g. the paper's 128:2:M) when the
  * tensor-core form is present (M <= 8, or M % 4 == 0); VNM_ERR_UNSUPPORTED otherwise.
- * Plans: tensor-core form present and T > 64 (or V != 64) -> window-form kernel on CTA pairs (dense X^T tiles by
- * TMA, tcgen05.mma.sp.cta_group::2 with M = 256); V = 64, T <= 32, M <= 8 -> small-T kernel (two V-blocks per
+ * Plans: tensor-core form present and T > 64 (or V != 64) -> a window-form kernel (dense X^T tiles by TMA):
+ * CTA pairs with the row pair's A resident for short K (tcgen05.mma.sp.cta_group::2, M = 256), CTA pairs
+ * streaming A, or single CTAs (M = 128) — chosen by shape from measurements;
+ * V = 64, T <= 32, M <= 8 -> small-T kernel (two V-blocks per
  * M = 128 sparse MMA, split-K); otherwise the gather kernel (M = 64 sparse MMAs on the 4 kept X^T rows of each
  * block, 16-byte cp.async gathers).
  * workspace: optional device scratch (16-B aligned) used by the small-T split-K plan; pass NULL/0 to
  * let the library choose a plan without it (vnm_spmm_workspace_bytes gives the size it can use).  Its
  * completion flags must be zero when a call starts: zero it once with vnm_spmm_workspace_init (or allocate
  * it zero-filled); every completed vnm_spmm call leaves it zeroed again, so one initialisation serves all
- * later calls ordered on the stream (no per-call memset).  Re-initialise after a failed launch.      */
+ * later calls ordered on the stream (no per-call memset).  Re-initialise after a failed launch; use one
+ * workspace per concurrently running call.                                                            */
 vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,
                     vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
 
