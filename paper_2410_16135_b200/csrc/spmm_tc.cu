@@ -49,6 +49,7 @@ struct TcArgs {
     int32_t stages;      // pipeline depth
     uint32_t b_stage_bytes, stage_bytes;
     int32_t abl;         // VNM_ABL (timing ablations only, results invalid): see spmm_tc2.cu
+    int32_t pf;          // L2 prefetch distance in stages (0: none): X^T streamed from HBM
 };
 
 
@@ -124,6 +125,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < kChunks; ++c)
                         tma_load_2d(base + b_off + c * (a.rb * 128), &tmap_b, n0 + 64 * c, st * a.rows_stage, &full[s]);
+                    if (a.pf && st + a.pf < a.n_stage) {  // warm L2 for a later stage of this tile (beyond the ring)
+#pragma unroll
+                        for (int c = 0; c < kChunks; ++c)
+                            tma_prefetch_l2(&tmap_b, n0 + 64 * c, (st + a.pf) * a.rows_stage);
+                    }
                 }
             }
         }
@@ -326,6 +332,9 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
         return kLaunchCudaError;
     const int grid = a.work < num_sms() ? a.work : num_sms();
     a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
+    // opt-in (VNM_TC_PF): the 1-CTA kernel alone gained 11 % on DeiT-B fc2-sized K, but whole steps got slower
+    // (DeiT-B 0.519 -> 0.554 ms: profiles/r01f_experiments.md)
+    a.pf = getenv("VNM_TC_PF") ? atoi(getenv("VNM_TC_PF")) : 0;
     cudaError_t e = launch_pdl(false, k, dim3(grid), dim3(kThreads), smem, stream, ta, tb, ty, a);
     count_launch();
     return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;

@@ -53,6 +53,7 @@ struct Tc2Args {
     int32_t y_slots;     // epilogue staging slots per warp (1 or 2)
     uint32_t b_bytes, stage_bytes, res_bytes;
     int32_t trace;       // VNM_SPMM_TRACE: per-CTA wait / busy cycle counters into g_tc2_t
+    int32_t pf;          // L2 prefetch distance in stages (0: none): X^T streamed from HBM (long K, large T)
     int32_t abl;         // VNM_ABL (timing ablations only, results invalid): 1 no epilogue, 2 no Y stores,
                          // 4 no X^T loads, 8 no metadata copies after the first stage
 };
@@ -206,6 +207,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     }
                     tma_load_2d_pair(base + b_off, &tmap_b, n0, st * a.rows_stage, &full[s]);
                     tma_load_2d_pair(base + b_off + a.rb * 128, &tmap_b, n0 + 64, st * a.rows_stage, &full[s]);
+                    if (a.pf && st + a.pf < a.n_stage) {  // warm L2 for a later stage of this tile (beyond the ring)
+                        tma_prefetch_l2(&tmap_b, n0, (st + a.pf) * a.rows_stage);
+                        tma_prefetch_l2(&tmap_b, n0 + 64, (st + a.pf) * a.rows_stage);
+                    }
                 }
             }
             if (a.trace) g_tc2_t[3][blockIdx.x] = c_emp;
@@ -381,6 +386,8 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
     }
     a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
     a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
+    // off by default: measured in whole steps it slowed DeiT-B 0.519 -> 0.554 ms (profiles/r01f_experiments.md)
+    a.pf = getenv("VNM_TC_PF") ? atoi(getenv("VNM_TC_PF")) : 0;
     cudaError_t e = launch_pdl(false, k, dim3(2 * pairs), dim3(C::kThreads), smem, stream, ta, tb, te, ty, a);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
