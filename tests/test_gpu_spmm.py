@@ -299,3 +299,47 @@ def test_natural_24_form(V, rows, cols, T, M):
 def test_llama_m16_sampled(rows, cols):
     """BJ config 5 at M = 16, T = 2048 through the natural 2:4 form (sampled rows against the oracle)."""
     sampled_check(rows, cols, 16, 2048, seed=rows + cols + 16, out_dtype=torch.bfloat16, tc=True)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_chained_small_t_layers_see_the_previous_output(graph):
+    """Two small-T SpMMs back to back on one stream, the second reading the first's Y^T as its X^T (a decode
+    MLP), eagerly and replayed from a CUDA graph.  The small-T plan is launched with programmatic dependent
+    launch; its griddepcontrol.wait (after the prologue) is what orders the second kernel's reads after the
+    first's writes.  Y1's buffer is NaN-filled first, so a read of unwritten data shows as NaN / a mismatch.
+    (A build with the wait removed still passed this test — the race window is narrow — so it checks the
+    chained path, not the absence of the race.)"""
+    T, M = 16, 5
+    W1 = synth.weights(256, 512, seed=31)
+    W2 = synth.weights(384, 256, seed=32)
+    X = synth.activations_t(512, T, seed=33)
+    P1 = vnm.prune_compress(to_dev_bf16(W1), 64, M)
+    P2 = vnm.prune_compress(to_dev_bf16(W2), 64, M)
+    Xd = to_dev_bf16(X)
+    Y1 = torch.empty((256, T), dtype=torch.bfloat16, device="cuda")
+    Y2 = torch.empty((384, T), dtype=torch.float32, device="cuda")
+    ws1 = vnm.spmm_workspace(P1.g, T, "cuda")
+    ws2 = vnm.spmm_workspace(P2.g, T, "cuda")
+
+    def run():
+        Y1.fill_(float("nan"))
+        vnm.spmm(Xd, P1, T=T, out=Y1, workspace=ws1)
+        vnm.spmm(Y1, P2, T=T, out=Y2, workspace=ws2)
+
+    if graph:
+        run()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run()
+        for _ in range(3):
+            g.replay()
+    else:
+        for _ in range(3):
+            run()
+    torch.cuda.synchronize()
+    y1 = Y1.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert not torch.isnan(Y1).any()
+    Wm2 = oracle.apply_mask(W2, oracle.prune(W2, 64, M), 64, M)
+    Yref, Aref = oracle.gemm_ref(y1, Wm2)
+    assert_within(Y2.cpu().numpy().astype(np.float64), Yref, Aref)
