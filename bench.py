@@ -132,9 +132,12 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
+    if world > 1:
+        import datetime
+        # a bounded communicator timeout: a rank that dies or hangs fails the job instead of blocking it forever
+        dist.init_process_group("nccl", timeout=datetime.timedelta(seconds=args.nccl_timeout),
+                                device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     wl = WORKLOADS[args.workload]
     V, M, T = wl["V"], wl["M"], wl["T"]
@@ -172,8 +175,10 @@ def run_gpu(args):
         lay = dict(name=name, rows=rows, cols=cols, W=Wd, X=Xd, Wh=Wh, Xh=Xh, P=P, Y=Yd, Yh=Yh,
                    n=geom_numbers(rows, cols, V, M, T), n_full=geom_numbers(rows_full, cols, V, M, T))
         if out_mode:
+            # the SpMM writes this rank's Y^T rows straight into its padded all-gather shard (no copy)
             lay["Ysh"] = torch.zeros((shard_rows, ldx), dtype=torch.bfloat16, device=dev)
             lay["Yall"] = torch.empty((world * shard_rows, ldx), dtype=torch.bfloat16, device=dev)
+            lay["Y"] = lay["Ysh"][:rows]
         layers.append(lay)
     del W, XT
     L = vnm.lib()
@@ -223,9 +228,9 @@ def run_gpu(args):
         assert st == 0, vnm.status_string(st)
 
     def gather(l):
-        # out mode: this rank's Y^T rows -> the padded shard -> one NCCL all-gather (feature-major: contiguous)
+        # out mode: the padded shard (the SpMM wrote its rows in place) -> one NCCL all-gather (feature-major:
+        # contiguous)
         if out_mode and world > 1:
-            l["Ysh"][:l["rows"]].copy_(l["Y"])
             dist.all_gather_into_tensor(l["Yall"], l["Ysh"])
 
     def step(ev=None, ev_mid=None):
@@ -579,6 +584,27 @@ def run_reference(args):
         "gpu_launches": 0}), flush=True)
 
 
+def ensure_world(args):
+    """--gpus N is the number of ranks: without a torchrun environment and N > 1, re-execute this command under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1); under torchrun, WORLD_SIZE must
+    equal N."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is None:
+        if args.gpus > 1:
+            import socket
+            s = socket.socket()
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+            s.close()
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            sys.stdout.flush()
+            os.execv(sys.executable, cmd)
+        return
+    if int(world) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; launch one rank per GPU (--gpus = nproc)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -593,8 +619,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-tokens", type=int, default=1024)
+    ap.add_argument("--nccl-timeout", type=int, default=600, help="seconds (torch.distributed init timeout)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    ensure_world(args)
     if args.impl == "reference":
         run_reference(args)
     else:

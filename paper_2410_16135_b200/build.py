@@ -1,7 +1,8 @@
 """Build the in-tree CUDA libraries with nvcc for sm_100a (no JIT, no torch extension machinery).
 
-  libvnm.so        the product: C ABI of include/vnm.h (api.cpp + the kernels)
-  libvnm_probe.so  test-only hardware probes / microbenchmarks (probes.cu)
+  libvnm.so                    the product: C ABI of include/vnm.h (api.cpp + the kernels in csrc/)
+  tests/probes/libvnm_probe.so test-only hardware probes / microbenchmarks (tests/probes/probes*.cu); the
+                               product never loads it
 """
 from __future__ import annotations
 
@@ -16,9 +17,12 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
          "-Xptxas", "-warn-spills"]
 
+PROBES = os.path.join(HERE, "..", "tests", "probes")
+# output path -> (source directory, sources)
 LIBS = {
-    "libvnm.so": ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu", "spmm_tc.cu", "spmm_tc2.cu", "spmm_tc3.cu", "spmm_dec.cu", "ria.cu", "permute.cu"],
-    "libvnm_probe.so": ["probes.cu", "probes2.cu", "probes3.cu"],
+    os.path.join(HERE, "libvnm.so"): (CSRC, ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu",
+                                           "spmm_tc.cu", "spmm_tc2.cu", "spmm_tc3.cu", "spmm_smallt.cu", "ria.cu", "permute.cu"]),
+    os.path.join(PROBES, "libvnm_probe.so"): (PROBES, ["probes.cu", "probes2.cu", "probes3.cu"]),
 }
 
 
@@ -36,9 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> None:
     from concurrent.futures import ThreadPoolExecutor
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    for lib, files in LIBS.items():
-        srcs = [os.path.join(CSRC, f) for f in files]
-        out = os.path.join(HERE, lib)
+    for out, (srcdir, files) in LIBS.items():
+        srcs = [os.path.join(srcdir, f) for f in files]
         if not force and not _stale(out, srcs):
             continue
         objs = [os.path.join(objdir, f + ".o") for f in files]
@@ -47,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> None:
             if not force and not _stale(objs[i], [srcs[i]]):
                 return
             tmp = objs[i] + f".tmp{os.getpid()}"
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", "-o", tmp, srcs[i]]
+            cmd = [NVCC, *ARCH, *FLAGS, "-I", CSRC, "-c", "-o", tmp, srcs[i]]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.check_call(cmd)

@@ -266,16 +266,18 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     if (y_dtype != VNM_F32 && y_dtype != VNM_BF16) return VNM_ERR_ARG;
     if (T < 0 || ldx < T || ldy < T) return VNM_ERR_SHAPE;
     // tensor-core form: 32 <= V <= 128 with M <= 8 (window form) or M % 4 == 0 (natural 2:4 form; the kernels
-    // see its M = 4 view); gather / small-T plans: V = 64
+    // see its M = 4 view); small-T plan (T <= 32): any V >= 16, any M, canonical arrays; gather plan: V = 64
     const bool tc_form = P->values_tc && P->meta_tc && tc_geom(g);
-    if (g->V != 64 && !tc_form) return VNM_ERR_UNSUPPORTED;
+    static const int smallt_env = VNM_ENV_INT("VNM_SMALLT", 1);  // 0: the previous small-T plan (comparisons)
+    const bool small = smallt_env && vnm::spmm_smallt_applies(*g, T);
+    if (g->V != 64 && !tc_form && !small) return VNM_ERR_UNSUPPORTED;
     if (T == 0 || g->rows == 0) return VNM_OK;
     if (!YT) return VNM_ERR_ARG;
     if (g->cols > 0 && !XT) return VNM_ERR_ARG;
     if ((XT && !aligned16(XT)) || !aligned16(YT) || (ldx % 8) != 0 || (ldy % 8) != 0) return VNM_ERR_ALIGN;
     if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
     vnm::SpmmLaunch L{P, XT, ldx, T, YT, ldy, y_dtype, workspace, workspace ? workspace_bytes : 0};
-    const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || g->V != 64);
+    const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || (!small && g->V != 64));
     if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
     vnm_packed Pv;
     if (tc && nat24(g)) {  // the natural 2:4 form runs as the M = 4 layout over 4-channel groups
@@ -304,13 +306,7 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         if (pair) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
         return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
     }
-    // the register-direct mma.sp decode kernel (spmm_dec.cu) measured slower than the small-T TMA plan
-    // (32-byte row segments per k-step: poor DRAM locality, profiles/r01b_decode.md); opt-in VNM_DEC=1
-    static const bool use_dec = [] { const char* e = getenv("VNM_DEC"); return e && e[0] == '1'; }();
-    if (use_dec && vnm::spmm_dec_applies(*g, T)) {
-        const int rc = vnm::launch_spmm_dec(L, reinterpret_cast<cudaStream_t>(stream));
-        if (rc != vnm::kLaunchUnsupported) return from_launch(rc);  // else: no workspace -> other plans
-    }
+    if (small) return from_launch(vnm::launch_spmm_smallt(L, reinterpret_cast<cudaStream_t>(stream)));
     if (vnm::spmm_pair_applies(*g, T)) return from_launch(vnm::launch_spmm_pair(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -323,9 +319,10 @@ vnm_status vnm_spmm_workspace_init(void* ws, size_t bytes, vnm_stream_t stream) 
 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T) {
     if (check_geom(g) != VNM_OK || T < 0) return 0;
-    size_t dec = vnm::spmm_dec_applies(*g, T) ? vnm::spmm_dec_workspace_bytes(*g, T) : 0;
-    size_t other = vnm::spmm_pair_applies(*g, T) ? vnm::spmm_pair_workspace_bytes(*g, T) : vnm::spmm_workspace_bytes(*g, T);
-    return dec > other ? dec : other;
+    // the largest workspace any plan for (g, T) can use (the tickets / flags sit at offset 0 in every plan)
+    size_t b = vnm::spmm_smallt_workspace_bytes(*g, T);
+    const size_t o = vnm::spmm_pair_applies(*g, T) ? vnm::spmm_pair_workspace_bytes(*g, T) : vnm::spmm_workspace_bytes(*g, T);
+    return b > o ? b : o;
 }
 
 vnm_status vnm_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, float* norms, vnm_stream_t stream) {

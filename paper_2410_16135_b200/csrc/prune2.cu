@@ -510,7 +510,7 @@ static bool setup_problem(const PruneLaunch& L, Maps& tm, Prune2Args& a, cudaStr
     a.has_values = vals ? 1 : 0; a.has_tc = tc ? 1 : 0;
     a.M = g.M; a.rows_p = g.rows_p; a.nb = g.nb; a.nb_pad = g.nb_pad; a.ld_mask = g.ld_mask;
     a.has_score = has_score ? 1 : 0;
-    a.trace = getenv("VNM_PRUNE_TRACE") ? 1 : 0;
+    a.trace = VNM_ENV_INT("VNM_PRUNE_TRACE", 0) ? 1 : 0;
     a.n_mma = n_mma;
     a.n_stage_tc = (n_mma + 3) / 4;
     if (tc) {

@@ -388,7 +388,7 @@ int choose_ksplit(int ntiles, int n_stage) {
 }
 
 void dump_trace(cudaStream_t st) {
-    if (!getenv("VNM_SPMM_TRACE")) return;
+    if (!VNM_ENV_INT("VNM_SPMM_TRACE", 0)) return;
     {
         static unsigned long long h[7][512];
         cudaStreamSynchronize(st);
@@ -423,7 +423,7 @@ void plan_units(SpmmArgs& a, const SpmmLaunch& L, int NT) {
     a.ntt = (L.T + NT - 1) / NT;
     a.ntiles = a.nvb * a.ntt;
     const int n_stage = (a.nb_pad / 8 + kMmaPerStage - 1) / kMmaPerStage;
-    a.trace = getenv("VNM_SPMM_TRACE") ? atoi(getenv("VNM_SPMM_TRACE")) : 0;
+    a.trace = VNM_ENV_INT("VNM_SPMM_TRACE", 0);
     a.ks_n = 1;
     if (L.workspace) {
         const int ks = choose_ksplit(a.ntiles, n_stage);

@@ -470,7 +470,7 @@ int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t st) {
     a.grid = p.grid;
     a.stream_k = p.stream_k;
     a.nb_tok = L.T <= 16 ? 16 : 32;
-    a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
+    a.trace = VNM_ENV_INT("VNM_SPMM_TRACE", 0) ? 1 : 0;
     if (p.stream_k) {
         if (!L.workspace || L.workspace_bytes < p.ws_bytes) {  // no scratch: whole tiles only
             a.stream_k = 0;
@@ -508,7 +508,7 @@ int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t st) {
         !encode_2d(&tx, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols),
                    static_cast<uint64_t>(L.ldx) * 2, a.tp, kBlocksPerStage * g.M, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                    CU_TENSOR_MAP_SWIZZLE_NONE)) {
-        if (getenv("VNM_DEBUG")) fprintf(stderr, "vnm_spmm (pair plan): tensor-map encoding failed\n");
+        if (VNM_ENV_INT("VNM_DEBUG", 0)) fprintf(stderr, "vnm_spmm (pair plan): tensor-map encoding failed\n");
         return kLaunchCudaError;
     }
     cudaError_t e = cudaFuncSetAttribute(vnm_spmm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -528,7 +528,7 @@ int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t st) {
             fprintf(stderr, "  cta %3d start %6llu mma_done %6llu epi_done %6llu end %6llu ns\n", i, h[0][i] - t0,
                     h[1][i] - t0, h[2][i] - t0, h[3][i] - t0);
     }
-    if (e != cudaSuccess && getenv("VNM_DEBUG"))
+    if (e != cudaSuccess && VNM_ENV_INT("VNM_DEBUG", 0))
         fprintf(stderr, "vnm_spmm (pair plan): %s (smem %d, grid %d)\n", cudaGetErrorString(e), smem, a.grid);
     return e == cudaSuccess ? 0 : kLaunchCudaError;
 }

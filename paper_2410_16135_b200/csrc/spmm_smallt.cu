@@ -1,0 +1,442 @@
+// spmm_smallt.cu — the small-T plan of the V:N:M SpMM (decode-sized token counts, 1 <= T <= 32, any M, V >= 16),
+// SURVEY §8(a) rows a6-a8 and §8(d) config 4b; §3 "Acceleration of V:N:M sparsity" P:106-109, App. A
+// P:547-548 ("retrieve the retained weights and the corresponding tiles of B").
+//
+// At T <= 32 the product is a stream of the canonical packed weights — A_n (2 values per block and row), A_i2
+// (one 2:4 nibble per block and row) and A_i1 (4 column indices per block and V-block) — with a few MACs per
+// weight, so the kernel is a TMA stream with light tensor work on top, and it reads nothing but those arrays and
+// a dense slice of X^T:
+//   * unit of work = 128 rows x 32 column blocks (4 k-steps of logical K = 32): the A_n box [128 rows][64 values]
+//     (128-byte swizzle), the A_i2 box [128 rows][4 words], the A_i1 words of the unit's V-block(s) and the
+//     dense X^T slice of the 32 blocks [32 M channels][TP tokens] arrive by TMA in a ring of S slots (one
+//     producer thread); the X^T slice is L2-resident (every row group re-reads it) and shared by the unit's
+//     two V-blocks (V = 64);
+//   * warp-level sparse MMA (mma.sp::ordered_metadata m16n8k32, bf16 in, fp32 accumulate): A_n IS the
+//     2:4-compressed operand of the gathered product (the block's 2 kept values = one group of 4 gathered
+//     channels) and its A_i2 word is the operand's metadata; the A fragments come from the swizzled A_n box by
+//     ldmatrix (conflict-free); the B fragments are GATHERED by ldmatrix.trans itself: lane i supplies the
+//     shared-memory address of gathered K-row i of the k-step, i.e. X^T channel (block i/4, A_i1 position i%4)
+//     of the slice — no gather copy, no B tile, no metadata repacking;
+//   * 8 consumer warps: half h = w % 2 (64 rows = 4 m16 tiles = one V-block at V = 64), phase p = w / 2 (units
+//     p, p + 4, ... of the CTA's share);
+//   * persistent CTAs take equal contiguous shares of the (row group, stage) list (stream-K); at the end of a
+//     piece (the row group changes or the share ends) the 4 phases are added in phase order through shared
+//     memory; a row group cut between CTAs is finished by the LAST CTA to arrive (ticket), which adds the fp32
+//     pieces in CTA order — deterministic, no second kernel, no CTA ever waits for another.
+// Why not tcgen05 here: an M = 64/128 sparse tcgen05.mma costs >= 104 cycles whatever N <= 128
+// (profiles/r01_probes.md MB2) and needs the gathered B tile in shared memory plus the metadata repacked into
+// TMEM each stage — per-stage work the previous small-T plan measured at ~1 us per stage (0.24 of HBM); here the
+// tensor work per unit is 64 warp MMAs that hide under the stream.
+#include <cstdint>
+#include <cstdio>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "tmap.h"
+#include "vnm_internal.h"
+
+namespace vnm {
+namespace {
+
+constexpr int kRowsU = 128;        // rows per unit (two 64-row halves)
+constexpr int kKS = 4;             // k-steps (8 blocks = logical K 32) per unit
+constexpr int kBlkU = 8 * kKS;     // 32 column blocks per unit
+constexpr int kCons = 8;           // consumer warps
+constexpr int kPhases = kCons / 2;
+constexpr int kProd = kCons;       // producer warp index
+constexpr int kThreads = 32 * (kCons + 1);
+constexpr uint32_t kABytes = kRowsU * 128;   // A_n box [128 rows][64 bf16], SW128
+constexpr uint32_t kMBytes = kRowsU * 16;    // A_i2 box [128 rows][4 u32]
+constexpr uint32_t kCRow = kBlkU * 4;        // A_i1 words of one V-block and unit (128 B)
+constexpr uint32_t kTicketWords = 4096;      // fixed ticket region at the start of the workspace (16 KB)
+
+struct StArgs {
+    void* YT;
+    int64_t ldy;
+    float* ws;           // partials [n_rp][maxseg][128][TP] fp32 (after the ticket region)
+    uint32_t* tickets;   // [kTicketWords], zero at launch; every launch leaves them zero
+    int32_t T, y_bf16, rows, rows_p, V, M, n_ks, n_st, n_rp, units, grid, maxseg;
+    int32_t S;           // ring slots
+    int32_t rg_mode;     // 1: shares are whole row groups (no workspace: no piece is ever cut between CTAs)
+    int32_t c_rows;      // A_i1 rows (V-blocks) per unit: max(1, 128 / V)
+    int32_t x_rows, x_box, x_nbox;  // X^T slice rows (32 M), rows per TMA box (<= 256), boxes
+    uint32_t x_bytes;    // slice bytes in shared memory (x_rows * TP * 2, rounded to 1 KB)
+    uint32_t slot_bytes, tx_bytes;
+};
+
+__device__ __forceinline__ int unit_owner(const StArgs& a, int u) {  // CTA whose share contains unit u
+    return static_cast<int>((static_cast<long long>(u + 1) * a.grid - 1) / a.units);
+}
+__device__ __forceinline__ int share_begin(const StArgs& a, int b) {  // first unit of CTA b's share
+    if (a.rg_mode) return static_cast<int>(static_cast<long long>(b) * a.n_rp / a.grid) * a.n_st;
+    return static_cast<int>(static_cast<long long>(b) * a.units / a.grid);
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+// D (16 x 8, fp32) += A (16 x 32, 2:4-compressed bf16, metadata e) * B (32 x 8 bf16)
+__device__ __forceinline__ void mma_sp_16832(float (&d)[4], const uint32_t (&A)[4], const uint32_t (&B)[4], uint32_t e) {
+    asm volatile(
+        "mma.sp::ordered_metadata.sync.aligned.m16n8k32.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+        "{%8, %9, %10, %11}, {%0, %1, %2, %3}, %12, 0x0;"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(A[0]), "r"(A[1]), "r"(A[2]), "r"(A[3]), "r"(B[0]), "r"(B[1]), "r"(B[2]), "r"(B[3]), "r"(e));
+}
+
+// byte offset of 16-byte token chunk n of X^T slice row r: rows of TP*2 bytes, TMA swizzle none (TP = 8),
+// 32B (TP = 16) or 64B (TP = 32) — Swizzle<log2(TP/8),4,3>: chunk bits [4, ..) ^= row-address bits [7, ..)
+template <int TP>
+__device__ __forceinline__ uint32_t xoff(int r, int n) {
+    if constexpr (TP == 8) return 16u * r;
+    else if constexpr (TP == 16) return 32u * r + 16u * (n ^ ((r >> 2) & 1));
+    else return 64u * r + 16u * (n ^ ((r >> 1) & 3));
+}
+
+// NT8: token tiles of 8 computed (T <= 8 NT8); VSET: V-blocks per 64-row half (64 / V for V <= 64, else 1)
+template <int NT8, int VSET, bool kBf16>
+__global__ void __launch_bounds__(kThreads, 1)
+    vnm_spmm_smallt_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_m,
+                           const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_x,
+                           const StArgs a) {
+    constexpr int TP = NT8 == 1 ? 8 : (NT8 == 2 ? 16 : 32);  // tokens per X^T slice row in shared memory
+    extern __shared__ __align__(1024) uint8_t smem[];
+    // slot s: [A_n 16 KB][X^T slice x_bytes][A_i2 2 KB][A_i1 c_rows x 128 B]; then red [128][TP] fp32, barriers
+    float* red = reinterpret_cast<float*>(smem + a.S * a.slot_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + kRowsU * TP);
+    uint64_t* empty = full + a.S;
+    uint32_t& last_flag = *reinterpret_cast<uint32_t*>(empty + a.S);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int u0 = share_begin(a, blockIdx.x), u1 = share_begin(a, blockIdx.x + 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < a.S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 2);  // the two half warps of the phase that consumes the slot
+        }
+        fence_mbar_init();
+    }
+    if (warp == kProd && lane == 0) {
+        tma_prefetch_desc(&tm_a);
+        tma_prefetch_desc(&tm_m);
+        tma_prefetch_desc(&tm_c);
+        tma_prefetch_desc(&tm_x);
+    }
+    __syncthreads();
+    grid_dep_wait();    // the previous kernel's outputs (this layer's X^T, packed weights) are visible
+    grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
+
+    if (warp == kProd) {
+        // ------------------------------------------------------------ producer: one thread, one unit per slot
+        if (lane == 0) {
+            for (int u = u0, q = 0; u < u1; ++u, ++q) {
+                const int rp = u / a.n_st, st = u % a.n_st, s = q % a.S;
+                mbar_wait(&empty[s], ((q / a.S) & 1) ^ 1);
+                uint8_t* base = smem + s * a.slot_bytes;
+                mbar_arrive_expect_tx(&full[s], a.tx_bytes);
+                tma_load_2d(base, &tm_a, st * 2 * kBlkU, rp * kRowsU, &full[s]);
+                for (int b = 0; b < a.x_nbox; ++b)
+                    tma_load_2d(base + kABytes + b * a.x_box * TP * 2, &tm_x, 0, st * kBlkU * a.M + b * a.x_box, &full[s]);
+                tma_load_2d(base + kABytes + a.x_bytes, &tm_m, st * kKS, rp * kRowsU, &full[s]);
+                tma_load_2d(base + kABytes + a.x_bytes + kMBytes, &tm_c, st * kBlkU, (rp * kRowsU) / a.V, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const int h = warp & 1, p = warp >> 1;
+    const int g = lane >> 2, c = lane & 3;
+    const int hsh = 16 * (c & 1);  // metadata half of this thread (selector 0: threads c = 0, 1 of each group)
+    const int cons_tid = threadIdx.x;  // 0 .. 255
+    float acc[4][NT8][4];
+
+    for (int pu0 = u0; pu0 < u1;) {
+        const int rp = pu0 / a.n_st;
+        const int pu1 = min(u1, (rp + 1) * a.n_st);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int n = 0; n < NT8; ++n)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[mt][n][k] = 0.f;
+        const bool half_ok = rp * kRowsU + 64 * h < a.rows_p;
+        // this phase's units of the piece: u = u0 + q, q = p (mod 4)
+        int u = pu0 + ((p - (pu0 - u0)) % kPhases + kPhases) % kPhases;
+        for (; u < pu1; u += kPhases) {
+            const int q = u - u0, s = q % a.S;
+            mbar_wait(&full[s], (q / a.S) & 1);
+            if (half_ok) {
+                const int st = u % a.n_st;
+                const int nks = min(kKS, a.n_ks - st * kKS);
+                const uint32_t sA = smem_u32(smem + s * a.slot_bytes);
+                const uint32_t sX = sA + kABytes, sM = sX + a.x_bytes, sC = sM + kMBytes;
+                // A_i2 words of rows g, g + 8 of every m16 tile of this half (4 words = the unit's 4 k-steps)
+                uint32_t w0[4][4], w1[4][4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    const int r0 = 64 * h + 16 * mt + g;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(w0[mt][0]), "=r"(w0[mt][1]), "=r"(w0[mt][2]), "=r"(w0[mt][3])
+                                 : "r"(sM + 16 * r0));
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(w1[mt][0]), "=r"(w1[mt][1]), "=r"(w1[mt][2]), "=r"(w1[mt][3])
+                                 : "r"(sM + 16 * (r0 + 8)));
+                }
+                // ldmatrix roles: matrix j = lane / 8 (rows +8 for j odd, 16-byte chunk +1 for j >= 2), row lane % 8
+                const int jm = lane >> 3, rr = lane & 7;
+#pragma unroll
+                for (int ks = 0; ks < kKS; ++ks) {
+                    if (ks >= nks) break;
+                    // B: lane i addresses gathered K-row i of the k-step = block 8 ks + i / 4, A_i1 position i % 4
+                    uint32_t B[VSET][NT8][4];
+#pragma unroll
+                    for (int v = 0; v < VSET; ++v) {
+                        const int crow = a.c_rows == 1 ? 0 : h * VSET + v;
+                        const int blk = 8 * ks + (lane >> 2);
+                        uint32_t cw;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(sC + crow * kCRow + 4 * blk));
+                        const int xr = blk * a.M + static_cast<int>((cw >> (8 * (lane & 3))) & 0xFFu);
+#pragma unroll
+                        for (int n = 0; n < NT8; ++n) ldsm_x4_t(sX + xoff<TP>(xr, n), B[v][n]);
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) {
+                        const int row = 64 * h + 16 * mt + rr + 8 * (jm & 1);
+                        const int chunk = 2 * ks + (jm >> 1);
+                        uint32_t A[4];
+                        ldsm_x4(sA + 128 * row + 16 * ((chunk ^ row) & 7), A);
+                        const uint32_t e = ((w0[mt][ks] >> hsh) & 0xFFFFu) | (((w1[mt][ks] >> hsh) & 0xFFFFu) << 16);
+                        const int v = mt / (4 / VSET);
+#pragma unroll
+                        for (int n = 0; n < NT8; ++n) mma_sp_16832(acc[mt][n], A, B[v][n], e);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // ---- end of the piece: phases 0..3 added in order through red[128][TP]
+#pragma unroll 1
+        for (int r = 0; r < kPhases; ++r) {
+            if (p == r) {
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int n = 0; n < NT8; ++n)
+#pragma unroll
+                        for (int k2 = 0; k2 < 2; ++k2) {
+                            float2* d = reinterpret_cast<float2*>(red + (64 * h + 16 * mt + g + 8 * k2) * TP + 8 * n + 2 * c);
+                            float2 v = make_float2(acc[mt][n][2 * k2], acc[mt][n][2 * k2 + 1]);
+                            if (r > 0) {
+                                const float2 o = *d;
+                                v.x = o.x + v.x;
+                                v.y = o.y + v.y;
+                            }
+                            *d = v;
+                        }
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
+        }
+        const bool whole = pu0 == rp * a.n_st && pu1 == (rp + 1) * a.n_st;
+        const int row0 = rp * kRowsU;
+        // Y^T rows row0 .. +127, tokens [0, T): one 16-byte group (8 bf16 / 4 fp32 tokens) per thread and step
+        auto store_rows = [&](auto&& value) {
+            constexpr int kEl = kBf16 ? 8 : 4;
+            constexpr int kGroups = TP / kEl;  // groups per row
+            for (int i = cons_tid; i < kRowsU * kGroups; i += 32 * kCons) {
+                const int r = i / kGroups, t0 = (i % kGroups) * kEl;
+                const int grow = row0 + r;
+                if (grow >= a.rows || t0 >= a.T) continue;
+                float v[kEl];
+#pragma unroll
+                for (int e = 0; e < kEl; ++e) v[e] = value(r, t0 + e);
+                uint8_t* dst = static_cast<uint8_t*>(a.YT) + (static_cast<int64_t>(grow) * a.ldy + t0) * (kBf16 ? 2 : 4);
+                if (t0 + kEl <= a.T) {
+                    uint32_t w[4];
+                    if constexpr (kBf16) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+                            w[e] = *reinterpret_cast<uint32_t*>(&b2);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(v[e]);
+                    }
+                    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                                 "r"(w[3])
+                                 : "memory");
+                } else {
+                    for (int e = 0; e < a.T - t0; ++e) {
+                        if constexpr (kBf16)
+                            reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(v[e]);
+                        else
+                            reinterpret_cast<float*>(dst)[e] = v[e];
+                    }
+                }
+            }
+        };
+        if (whole) {
+            store_rows([&](int r, int t) { return red[r * TP + t]; });
+        } else {
+            // a cut row group: publish this CTA's piece; the last CTA to arrive adds the pieces in CTA order
+            const int own0 = unit_owner(a, rp * a.n_st);
+            const int nseg = unit_owner(a, rp * a.n_st + a.n_st - 1) - own0 + 1;
+            float* wsr = a.ws + static_cast<int64_t>(rp) * a.maxseg * kRowsU * TP;
+            float4* mine = reinterpret_cast<float4*>(wsr + static_cast<int64_t>(blockIdx.x - own0) * kRowsU * TP);
+            const float4* red4 = reinterpret_cast<const float4*>(red);
+            for (int i = cons_tid; i < kRowsU * TP / 4; i += 32 * kCons) __stcg(mine + i, red4[i]);
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
+            if (cons_tid == 0) last_flag = atomicAdd(&a.tickets[rp], 1u) == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
+            if (last_flag) {
+                __threadfence();
+                store_rows([&](int r, int t) {
+                    float v = 0.f;
+                    for (int j = 0; j < nseg; ++j) v += __ldcg(wsr + (static_cast<int64_t>(j) * kRowsU + r) * TP + t);
+                    return v;
+                });
+                if (cons_tid == 0) a.tickets[rp] = 0u;  // ready for the next launch (stream order)
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");  // red is reused by the next piece
+        pu0 = pu1;
+    }
+}
+
+struct StPlan {
+    int n_rp, n_ks, n_st, units, grid, maxseg, S, tp, c_rows, x_rows, x_box, x_nbox;
+    uint32_t x_bytes, slot_bytes;
+    size_t smem, ws_bytes;
+};
+
+StPlan make_plan(const vnm_geom& g, int32_t T) {
+    StPlan p{};
+    p.n_rp = (g.rows_p + kRowsU - 1) / kRowsU;
+    p.n_ks = g.nb_pad / 8;
+    p.n_st = (p.n_ks + kKS - 1) / kKS;
+    p.units = p.n_rp * p.n_st;
+    p.grid = p.units < num_sms() ? p.units : num_sms();
+    p.tp = T <= 8 ? 8 : (T <= 16 ? 16 : 32);
+    p.c_rows = g.V >= kRowsU ? 1 : kRowsU / g.V;
+    p.x_rows = kBlkU * g.M;
+    p.x_nbox = (p.x_rows + 255) / 256;
+    p.x_box = (p.x_rows + p.x_nbox - 1) / p.x_nbox;
+    p.x_box = (p.x_box + 7) / 8 * 8;  // whole 8-row swizzle atoms per box
+    p.x_bytes = static_cast<uint32_t>(p.x_nbox * p.x_box * p.tp * 2 + 1023) / 1024 * 1024;
+    p.slot_bytes = (kABytes + p.x_bytes + kMBytes + p.c_rows * kCRow + 1023) / 1024 * 1024;
+    const size_t fixed = static_cast<size_t>(kRowsU) * p.tp * 4 + 2 * 16 * 8 + 64;
+    p.S = static_cast<int>((kMaxSmem - fixed) / p.slot_bytes);
+    if (p.S > 16) p.S = 16;
+    p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
+    p.maxseg = 1;
+    for (int rp = 0; rp < p.n_rp; ++rp) {
+        const long long x0 = static_cast<long long>(rp) * p.n_st, x1 = x0 + p.n_st - 1;
+        const int o0 = static_cast<int>(((x0 + 1) * p.grid - 1) / p.units);
+        const int o1 = static_cast<int>(((x1 + 1) * p.grid - 1) / p.units);
+        if (o1 - o0 + 1 > p.maxseg) p.maxseg = o1 - o0 + 1;
+    }
+    p.ws_bytes = kTicketWords * 4 + static_cast<size_t>(p.n_rp) * p.maxseg * kRowsU * p.tp * 4;
+    return p;
+}
+
+template <int NT8, int VSET>
+int launch_nt(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUtensorMap* tm, cudaStream_t st) {
+    auto k = L.y_dtype == VNM_BF16 ? vnm_spmm_smallt_kernel<NT8, VSET, true> : vnm_spmm_smallt_kernel<NT8, VSET, false>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)) != cudaSuccess)
+        return kLaunchCudaError;
+    cudaError_t e = launch_pdl(true, k, dim3(p.grid), dim3(kThreads), p.smem, st, tm[0], tm[1], tm[2], tm[3], a);
+    count_launch();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : kLaunchCudaError;
+}
+
+template <int VSET>
+int launch_v(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUtensorMap* tm, cudaStream_t st) {
+    const int nt8 = (L.T + 7) / 8;
+    if (nt8 <= 1) return launch_nt<1, VSET>(L, p, a, tm, st);
+    if (nt8 == 2) return launch_nt<2, VSET>(L, p, a, tm, st);
+    if (nt8 == 3) return launch_nt<3, VSET>(L, p, a, tm, st);
+    return launch_nt<4, VSET>(L, p, a, tm, st);
+}
+
+}  // namespace
+
+bool spmm_smallt_applies(const vnm_geom& g, int32_t T) {
+    if (T < 1 || T > 32 || g.V < 16 || g.nb_pad == 0) return false;
+    const StPlan p = make_plan(g, T);
+    return p.S >= 2 && p.n_rp <= static_cast<int>(kTicketWords);
+}
+
+size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T) {
+    return spmm_smallt_applies(g, T) ? make_plan(g, T).ws_bytes : 0;
+}
+
+int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) {
+    const vnm_geom& g = L.P->g;
+    if (!spmm_smallt_applies(g, L.T)) return kLaunchUnsupported;
+    const StPlan p = make_plan(g, L.T);
+    StArgs a{};
+    // without a workspace (or a too small one) every CTA takes whole row groups: nothing is cut, no tickets
+    a.rg_mode = (!L.workspace || L.workspace_bytes < p.ws_bytes) ? 1 : 0;
+    StPlan q = p;
+    if (a.rg_mode) q.grid = p.n_rp < num_sms() ? p.n_rp : num_sms();
+    a.YT = L.YT;
+    a.ldy = L.ldy;
+    a.tickets = a.rg_mode ? nullptr : static_cast<uint32_t*>(L.workspace);
+    a.ws = a.rg_mode ? nullptr : reinterpret_cast<float*>(static_cast<uint8_t*>(L.workspace) + kTicketWords * 4);
+    a.T = L.T;
+    a.y_bf16 = L.y_dtype == VNM_BF16;
+    a.rows = g.rows;
+    a.rows_p = g.rows_p;
+    a.V = g.V;
+    a.M = g.M;
+    a.n_ks = p.n_ks;
+    a.n_st = p.n_st;
+    a.n_rp = p.n_rp;
+    a.units = p.units;
+    a.grid = q.grid;
+    a.maxseg = p.maxseg;
+    a.S = p.S;
+    a.c_rows = p.c_rows;
+    a.x_rows = p.x_rows;
+    a.x_box = p.x_box;
+    a.x_nbox = p.x_nbox;
+    a.x_bytes = p.x_bytes;
+    a.slot_bytes = p.slot_bytes;
+    a.tx_bytes = kABytes + static_cast<uint32_t>(p.x_nbox * p.x_box * p.tp * 2) + kMBytes + p.c_rows * kCRow;
+    CUtensorMap tm[4];
+    const CUtensorMapSwizzle xsw = p.tp == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                             : (p.tp == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+    // A_n [rows_p][ld_val] bf16; A_i2 [rows_p][ld_meta] u32 (k-steps nb_pad / 8 wide); A_i1 [rows_p / V][nb_pad]
+    // u32; X^T [cols][ldx] bf16 (T wide).  Boxes past an edge are zero-filled (pad k-steps, rows, tokens).
+    if (!encode_2d(&tm[0], L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
+                   static_cast<uint64_t>(g.ld_val) * 2, 64, kRowsU) ||
+        !encode_2d(&tm[1], L.P->meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
+                   static_cast<uint64_t>(g.ld_meta) * 4, kKS, kRowsU, CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                   CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_2d(&tm[2], L.P->col_idx, static_cast<uint64_t>(g.nb_pad), static_cast<uint64_t>(g.rows_p / g.V),
+                   static_cast<uint64_t>(g.nb_pad) * 4, kBlkU, static_cast<uint32_t>(p.c_rows),
+                   CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_2d(&tm[3], L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols),
+                   static_cast<uint64_t>(L.ldx) * 2, static_cast<uint32_t>(p.tp), static_cast<uint32_t>(p.x_box),
+                   CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw))
+        return kLaunchCudaError;
+    const int vset = g.V >= 64 ? 1 : 64 / g.V;
+    if (vset == 1) return launch_v<1>(L, q, a, tm, stream);
+    if (vset == 2) return launch_v<2>(L, q, a, tm, stream);
+    return launch_v<4>(L, q, a, tm, stream);
+}
+
+}  // namespace vnm

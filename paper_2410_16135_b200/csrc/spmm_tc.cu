@@ -331,10 +331,10 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
     const int grid = a.work < num_sms() ? a.work : num_sms();
-    a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
+    a.abl = VNM_ABLATION_FLAGS();
     // opt-in (VNM_TC_PF): the 1-CTA kernel alone gained 11 % on DeiT-B fc2-sized K, but whole steps got slower
     // (DeiT-B 0.519 -> 0.554 ms: profiles/r01f_experiments.md)
-    a.pf = getenv("VNM_TC_PF") ? atoi(getenv("VNM_TC_PF")) : 0;
+    a.pf = VNM_ENV_INT("VNM_TC_PF", 0);
     cudaError_t e = launch_pdl(false, k, dim3(grid), dim3(kThreads), smem, stream, ta, tb, ty, a);
     count_launch();
     return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
@@ -359,13 +359,14 @@ int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream) {
     // Plan (measured, profiles/r01_*): long K (many stages per tile) -> NT = 256, one accumulator (the
     // epilogue is amortised over the K loop); short K -> NT = 192 with double-buffered accumulators so the
     // epilogue overlaps the next tile.  RT = 2 (two row tiles sharing each X^T tile) measured no faster.
-    // VNM_TC_CFG="NT,RT" overrides (tuning experiments).
+    // VNM_TC_CFG_NT / VNM_TC_CFG_RT override (tuning experiments).
     // Tile order: the larger operand is the one to keep hot in L2 across the tiles resident at a time —
     // row-tile-major when the window-form weights outweigh X^T (Llama), token-tile-major otherwise (DeiT).
     a.row_major = static_cast<int64_t>(a.n_rt) * 128 * 16 * a.n_mma > static_cast<int64_t>(g.cols) * L.T ? 1 : 0;
     // (3 or fewer row tiles: 256-token tiles quantise evenly over the SMs, measured faster for DeiT proj)
     int nt = (a.n_stage >= 12 || a.n_rt <= 3) ? 256 : 192, rt = 1;
-    if (const char* e = getenv("VNM_TC_CFG")) sscanf(e, "%d,%d", &nt, &rt);
+    if (const int v = VNM_ENV_INT("VNM_TC_CFG_NT", 0)) nt = v;
+    if (const int v = VNM_ENV_INT("VNM_TC_CFG_RT", 0)) rt = v;
     if (nt == 256 && rt == 1) return launch_cfg<256, 1>(L, a, stream);
     if (nt == 128 && rt == 1) return launch_cfg<128, 1>(L, a, stream);
     if (nt == 128 && rt == 2) return launch_cfg<128, 2>(L, a, stream);

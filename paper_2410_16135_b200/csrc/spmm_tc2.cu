@@ -339,7 +339,7 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
     const uint32_t b_stage = (a.b_bytes + 1023) / 1024 * 1024;
     const uint32_t fixed = 1024 + 256;
     a.a_res = a.res_bytes + 3 * b_stage + y_bytes + fixed <= kMaxSmem ? 1 : 0;
-    if (const char* e = getenv("VNM_TC2_ARES")) a.a_res = a.a_res && atoi(e) != 0;
+    if (VNM_ENV_INT("VNM_TC2_ARES", 1) == 0) a.a_res = 0;
     if (a.a_res && num_sms() / 2 < a.n_rp) a.a_res = 0;  // every row pair needs a CTA pair of its own
     if (a.a_res) {
         a.stage_bytes = b_stage;
@@ -355,7 +355,7 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
     // the larger operand stays hot in L2 across the tiles resident at a time (see spmm_tc.cu)
     const int64_t w_bytes = static_cast<int64_t>(a.n_rt) * 128 * 16 * a.n_mma;
     a.row_major = w_bytes > static_cast<int64_t>(g.cols) * L.T ? 1 : 0;
-    if (const char* e = getenv("VNM_TC2_ORDER")) a.row_major = atoi(e);
+    if (const int v = VNM_ENV_INT("VNM_TC2_ORDER", -1); v >= 0) a.row_major = v;
 
     CUtensorMap ta, tb, te, ty;
     const int ld_tc = 16 * a.n_mma;
@@ -384,10 +384,10 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
     } else if (a.work < pairs) {
         pairs = a.work;
     }
-    a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
-    a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
+    a.trace = VNM_ENV_INT("VNM_SPMM_TRACE", 0) ? 1 : 0;
+    a.abl = VNM_ABLATION_FLAGS();
     // off by default: measured in whole steps it slowed DeiT-B 0.519 -> 0.554 ms (profiles/r01f_experiments.md)
-    a.pf = getenv("VNM_TC_PF") ? atoi(getenv("VNM_TC_PF")) : 0;
+    a.pf = VNM_ENV_INT("VNM_TC_PF", 0);
     cudaError_t e = launch_pdl(false, k, dim3(2 * pairs), dim3(C::kThreads), smem, stream, ta, tb, te, ty, a);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -426,7 +426,7 @@ int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
     // long K: 256-token tiles, one accumulator (the per-tile hand-off is amortised over many stages);
     // short K: 192-token tiles with two accumulators so the epilogue overlaps the next tile
     int nt = a.n_stage >= 12 ? 256 : 192;
-    if (const char* e = getenv("VNM_TC2_NT")) nt = atoi(e);
+    if (const int v = VNM_ENV_INT("VNM_TC2_NT", 0)) nt = v;
     return nt == 256 ? launch_nt<256>(L, a, stream) : launch_nt<192>(L, a, stream);
 }
 

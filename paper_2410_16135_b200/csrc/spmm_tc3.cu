@@ -421,7 +421,7 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
         if (tmem_ok && ab + 2u * (s * a.rows_stage + 8) * 128u + fixed <= kMaxSmem) S = s;
     }
     if (!S) return kLaunchUnsupported;
-    if (const char* e = getenv("VNM_TC3_S")) { const int v = atoi(e); if (v >= 3 && v < S) S = v; }
+    if (const int v = VNM_ENV_INT("VNM_TC3_S", 0); v >= 3 && v < S) S = v;
     a.S = S;
     a.ring_rows = static_cast<uint32_t>(S * a.rows_stage + 8);
     a.stage_tx = 2u * a.rows_stage * (64 + kW1) * 2u + (a.a_res ? 0u : 2u * (kABytes + kEBytes));
@@ -459,8 +459,8 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     auto k = bf ? vnm_spmm_tc3_kernel<NT, true> : vnm_spmm_tc3_kernel<NT, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return kLaunchCudaError;
-    a.trace = getenv("VNM_SPMM_TRACE") ? 1 : 0;
-    a.abl = getenv("VNM_ABL") ? atoi(getenv("VNM_ABL")) : 0;
+    a.trace = VNM_ENV_INT("VNM_SPMM_TRACE", 0) ? 1 : 0;
+    a.abl = VNM_ABLATION_FLAGS();
     a.Y = L.YT;
     a.ldy = L.ldy;
     a.rows = g.rows;
@@ -498,13 +498,13 @@ int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream) {
     const int res = mode < 0 ? 1 : mode;
     // resident A: 4 MMAs per stage (16 blocks), 2 when a 4-MMA stage would be large (M >= 7: >= 112 rows)
     a.ms = g.M >= 7 && res ? 2 : 4;
-    if (const char* e = getenv("VNM_TC3_MS")) a.ms = atoi(e) == 2 ? 2 : 4;
+    if (const int v = VNM_ENV_INT("VNM_TC3_MS", 0)) a.ms = v == 2 ? 2 : 4;
     a.n_st = (a.n_mma + a.ms - 1) / a.ms;
     a.rows_stage = a.ms * (g.M == 4 ? 32 : 4 * g.M);
     // NT = 256 (one accumulator) when T is a multiple of 256 and A streams (long K: the per-tile hand-off is
     // amortised), else NT = 224 (two accumulators)
     int nt = (mode == 0 && L.T % 256 == 0) ? 256 : 224;
-    if (const char* e = getenv("VNM_TC3_NT")) nt = atoi(e);
+    if (const int v = VNM_ENV_INT("VNM_TC3_NT", 0)) nt = v;
     const int want = mode < 0 ? -1 : res;
     int rc = nt == 256 ? launch_nt3<256>(L, a, want, stream) : launch_nt3<224>(L, a, want, stream);
     if (rc == kLaunchUnsupported && mode < 0 && a.ms != 4) {  // resident did not fit: stream, 4-MMA stages

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/vnm.h"
@@ -9,6 +10,20 @@
 namespace vnm {
 
 constexpr size_t kMaxSmem = 227 * 1024;
+
+// Tuning / tracing switches from the environment, read ONCE per call site and process (a function-local static
+// inside a unique lambda), so the hot path makes no getenv calls.  Timing ablations (VNM_ABL, which make the
+// results invalid) exist only in builds compiled with -DVNM_ABLATIONS.
+#define VNM_ENV_INT(name, dflt)                                                                     \
+    ([] {                                                                                           \
+        static const int v_ = [] { const char* e_ = getenv(name); return e_ ? atoi(e_) : (dflt); }(); \
+        return v_;                                                                                  \
+    }())
+#ifdef VNM_ABLATIONS
+#define VNM_ABLATION_FLAGS() VNM_ENV_INT("VNM_ABL", 0)
+#else
+#define VNM_ABLATION_FLAGS() 0
+#endif
 constexpr int kLaunchUnsupported = 1;
 constexpr int kLaunchCudaError = 2;
 
@@ -52,14 +67,14 @@ int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream);
 int launch_pack_tc(const vnm_packed& P, cudaStream_t stream);
 int launch_pack_nat24(const vnm_packed& P, cudaStream_t stream);  // M % 4 == 0, M > 8: natural 2:4 form
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
-// small-T plan (spmm_pair.cu): T <= 32, V = 64, M <= 8
+// small-T plan (spmm_smallt.cu): 1 <= T <= 32, V >= 16, any M; canonical A_n / A_i1 / A_i2 only
+bool spmm_smallt_applies(const vnm_geom& g, int32_t T);
+size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T);
+int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream);
+// previous small-T plan (spmm_pair.cu, VNM_SMALLT=0): T <= 32, V = 64, M <= 8
 bool spmm_pair_applies(const vnm_geom& g, int32_t T);
 size_t spmm_pair_workspace_bytes(const vnm_geom& g, int32_t T);
 int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t stream);
-// decode plan (spmm_dec.cu): T <= 16, V >= 64, warp-level mma.sp with A straight from global memory
-bool spmm_dec_applies(const vnm_geom& g, int32_t T);
-size_t spmm_dec_workspace_bytes(const vnm_geom& g, int32_t T);
-int launch_spmm_dec(const SpmmLaunch& L, cudaStream_t stream);
 
 // RIA importance (ria.cu)
 size_t ria_workspace_bytes(int32_t rows, int32_t cols);

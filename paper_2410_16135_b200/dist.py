@@ -46,13 +46,17 @@ def shard_packed(P: vnm.Packed, rank: int, world: int) -> tuple[vnm.Packed, int,
     gl = vnm.geometry(rows_local, g.cols, V, g.M)
     sub = vnm.Packed(gl, P.values[r0:r0 + gl.rows_p], P.col_idx[vb0:vb0 + gl.rows_p // V], P.meta[r0:r0 + gl.rows_p])
     if tc and gl.rows_p > 0:
-        # include/vnm.h window form: values_tc [rows_w][16 n_mma], meta_tc [rows_w/128][n_stage][128][4]
-        n_mma = g.nb_pad // (8 if g.M == 4 else 4)
-        ld_tc, n_stage = 16 * n_mma, (n_mma + 3) // 4
+        # include/vnm.h tensor-core form: values_tc [rows_w][ld_tc], meta_tc [rows_w/128][per-tile words]; both
+        # strides are taken from the library's own byte counts of the FULL geometry, so the window form (M <= 8)
+        # and the natural 2:4 form (M % 4 == 0, laid out over 4-channel groups) slice alike
+        nv, nm = vnm.tc_bytes(g)
+        rows_w_full = math.ceil(g.rows_p / 128) * 128
+        ld_tc = nv // 2 // rows_w_full
+        meta_tile = nm // 4 // (rows_w_full // 128)
         rows_w = math.ceil(gl.rows_p / 128) * 128
         sub.values_tc = P.values_tc[r0 * ld_tc:(r0 + rows_w) * ld_tc]
         t0 = r0 // 128
-        sub.meta_tc = P.meta_tc[t0 * n_stage * 512:(t0 + rows_w // 128) * n_stage * 512]
+        sub.meta_tc = P.meta_tc[t0 * meta_tile:(t0 + rows_w // 128) * meta_tile]
     return sub, r0, S * V
 
 

@@ -279,8 +279,20 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
     _require_cuda(XT, out, workspace)
     T = XT.shape[1] if T is None else T
     g = P.g
+    _ld(XT)
     if XT.shape[0] != g.cols:
         raise ValueError(f"XT has {XT.shape[0]} rows, the packed weight has {g.cols} input channels")
+    if not 0 <= T <= XT.shape[1]:
+        raise ValueError(f"T = {T} outside [0, {XT.shape[1]}] (the columns of XT)")
+    if out is not None:
+        # the kernels write rows [0, g.rows) x tokens [0, T) through out.stride(0): check the extent here
+        _ld(out)
+        if out.shape[0] < g.rows or out.shape[1] < T:
+            raise ValueError(f"out is {tuple(out.shape)}, needs at least ({g.rows}, {T})")
+        if out.device != XT.device:
+            raise ValueError("out and XT must be on the same device")
+    if workspace is not None and workspace.device != XT.device:
+        raise ValueError("workspace and XT must be on the same device")
     if out is None:
         ldy = (T + 7) // 8 * 8
         out = torch.empty((g.rows, ldy), dtype=out_dtype, device=XT.device)[:, :T] if ldy != T else \

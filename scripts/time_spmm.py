@@ -13,7 +13,8 @@ X = synth.activations_t(cols, T, seed=2)
 z = os.environ.get("VNM_TS_ZERO", "")  # power probe: zero activations and / or weights
 if "x" in z: X = X * 0
 if "w" in z: W = W * 0
-P = vnm.prune_compress(to_dev_bf16(W), 64, M, tc=tc)
+V = int(os.environ.get("VNM_TS_V", "64"))
+P = vnm.prune_compress(to_dev_bf16(W), V, M, tc=tc)
 Xd = to_dev_bf16(X)
 Y = torch.empty((rows, (T + 7) // 8 * 8), dtype=torch.bfloat16, device="cuda")
 ws = vnm.spmm_workspace(P.g, T, "cuda")
@@ -39,4 +40,4 @@ for _ in range(10):
     a.record(); g1.replay(); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3)
 ts.sort()
-print(f"spmm {rows}x{cols} M={M} T={T}{' tc' if tc else ''}: warm {warm:.2f} us  cold median {ts[len(ts)//2]:.2f} us")
+print(f"spmm {rows}x{cols} V={V} M={M} T={T}{' tc' if tc else ''}: warm {warm:.2f} us  cold median {ts[len(ts)//2]:.2f} us")

@@ -67,10 +67,13 @@ def test_status_codes_without_launch():
     bad = vnm.geometry(128, 64, 64, 8)
     bad.nb_pad = 7
     assert L.vnm_prune(fake, 64, None, 0, ctypes.byref(bad), fake, None) == vnm.VNM_ERR_SHAPE
-    # spmm: V other than 64 is not built yet
+    # spmm: V = 16 runs only in the small-T plan (T <= 32); V = 8 nowhere; both rejected before any launch
     g16 = vnm.geometry(128, 64, 16, 8)
     P = vnm.CPacked(g16, 1 << 20, 1 << 20, 1 << 20)
-    assert L.vnm_spmm(fake, 16, 16, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_ERR_UNSUPPORTED
+    assert L.vnm_spmm(fake, 128, 128, ctypes.byref(P), fake, 128, 0, None, 0, None) == vnm.VNM_ERR_UNSUPPORTED
+    g8 = vnm.geometry(128, 64, 8, 8)
+    P8 = vnm.CPacked(g8, 1 << 20, 1 << 20, 1 << 20)
+    assert L.vnm_spmm(fake, 16, 16, ctypes.byref(P8), fake, 16, 0, None, 0, None) == vnm.VNM_ERR_UNSUPPORTED
     P = vnm.CPacked(g, 1 << 20, 1 << 20, 1 << 20)
     assert L.vnm_spmm(fake, 16, 16, ctypes.byref(P), fake, 16, 7, None, 0, None) == vnm.VNM_ERR_ARG
     assert L.vnm_spmm(fake, 8, 16, ctypes.byref(P), fake, 16, 0, None, 0, None) == vnm.VNM_ERR_SHAPE

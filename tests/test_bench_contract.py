@@ -41,6 +41,26 @@ def test_reference_arm_rank0_only():
     assert json.loads(lines[0])["impl"] == "reference"
 
 
+def test_gpus_flag_launches_the_ranks():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under torch.distributed.run with 2 ranks (one per
+    GPU); the line reports n_gpus = 2 (rank 0 prints, rank 1 exits 0)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "toy", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0", "--ref-tokens", "16"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_world_size_mismatch_fails():
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "toy", "--gpus", "4",
+                        "--steps", "1", "--warmup", "0"], cwd=ROOT, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0"))
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
 @pytest.mark.gpu
 def test_gpu_arm_json():
     """The GPU arm on the toy workload: one JSON line with the roofline / e2e / clocks / launch-count keys."""

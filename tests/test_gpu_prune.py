@@ -259,3 +259,93 @@ def test_batched_more_than_eight():
             assert np.array_equal(a, b)
         assert torch.equal(P.values_tc.view(torch.int16), Q.values_tc.view(torch.int16))
         assert torch.equal(P.meta_tc, Q.meta_tc)
+
+
+def decode_window_form(P, rows, cols):
+    """Host decode of the tensor-core window form (include/vnm.h; M <= 8) back to a dense [rows_w][cols_p + 8]
+    weight: block b of a row is an 8-channel window starting at channel b*M holding two 2:4 groups (channels
+    0-3, 4-7), 2 values per group (values_tc[4b + 2 sub + i]); its nibbles sit in meta_tc's M = 128 lane
+    order (lane L: rows (L%8) + 16 (L/16) and + 8; K-group gi of MMA k -> bits 16 j + 4 (gi % 4) of lane
+    (L with h = gi / 4)).  For M = 4 the form is the plain 2:4 layout (8 blocks of 4 channels per MMA).
+    Window positions past the block (channel >= M) must hold zero values; every value lands exactly once."""
+    g = P.g
+    M = g.M
+    bpm = 8 if M == 4 else 4          # blocks per MMA
+    gpb = 1 if M == 4 else 2          # 2:4 groups per block
+    n_mma = g.nb_pad // bpm
+    n_stage = (n_mma + 3) // 4
+    rows_w = (g.rows_p + 127) // 128 * 128
+    vals = P.values_tc.view(torch.int16).cpu().numpy().view(np.uint16).reshape(rows_w, 16 * n_mma)
+    mt = P.meta_tc.cpu().numpy().view(np.uint32).reshape(rows_w // 128, n_stage, 128, 4)
+    dense = np.zeros((rows_w, g.cols_p + 8), np.uint16)
+    for r in range(rows_w):
+        t, rr = divmod(r, 128)
+        j = 0 if (rr % 16) < 8 else 1
+        for b in range(g.nb_pad):
+            for sub in range(gpb):
+                q = b * gpb + sub                 # 2:4 group index along the row (8 per MMA)
+                mi, gi = divmod(q, 8)
+                st, k = divmod(mi, 4)
+                lane = (rr % 8) + 16 * (rr // 16) + 8 * (gi // 4)
+                nib = (int(mt[t, st, lane, k]) >> (16 * j + 4 * (gi % 4))) & 0xF
+                for i, pos in enumerate((nib & 3, nib >> 2)):
+                    v = vals[r, 2 * q + i]
+                    ch = 4 * sub + pos
+                    if ch >= M or b >= g.nb:
+                        assert v & 0x7FFF == 0, (r, b, sub, ch)  # window overhang / pad block: zero value
+                        continue
+                    c = b * M + ch
+                    assert dense[r, c] == 0 or v & 0x7FFF == 0, (r, c)
+                    if v & 0x7FFF:
+                        dense[r, c] = v
+    return dense[:rows, :cols]
+
+
+@pytest.mark.parametrize("V", [32, 64, 128])
+@pytest.mark.parametrize("M", [4, 5, 6, 7, 8])
+@pytest.mark.parametrize("rows,cols,kind", [(200, 333, "outlier"), (128, 64, "int")])
+def test_window_form_decodes_to_oracle(V, M, rows, cols, kind):
+    """The window form written by the fused prune pass (single and batched) holds exactly the oracle's masked
+    W: decoded on the host, value for value."""
+    W = synth.weights(rows, cols, seed=rows + cols + M + V, kind=kind)
+    Wd = to_dev_bf16(W)
+    P = vnm.prune_compress(Wd, V, M, tc=True)
+    B = vnm.prune_compress_batched([Wd, Wd], V, M, tc=True)[1]
+    torch.cuda.synchronize()
+    Wm = oracle.apply_mask(W, oracle.prune(W, V, M), V, M)
+    zero = lambda a: np.where((a & 0x7FFF) == 0, 0, a)  # -0 and +0 both mean "no weight"
+    for Q in (P, B):
+        assert np.array_equal(zero(decode_window_form(Q, rows, cols)), zero(Wm))
+
+
+@pytest.mark.parametrize("V", [32, 64, 128])
+@pytest.mark.parametrize("M", [5, 6, 8])
+def test_prune2_wide_exponent(V, M):
+    """Wide-exponent weights (sign * 2^U(-24, 4) * U(1, 2); pin P13) through prune2.cu — the kernel the bench
+    runs (32 <= V <= 128, M <= 8) — single and batched: every byte vs the oracle, whose fp32 column L1 follows
+    the canonical stride-halving tree (Q3); a different summation order flips near-ties here."""
+    W = synth.weights(520, 1000, seed=V * 7 + M, kind="wide")
+    check(W, V, M)
+    W2 = synth.weights(300, 333, seed=V + M, kind="wide")
+    Ps, masks = vnm.prune_compress_batched([to_dev_bf16(W), to_dev_bf16(W2)], V, M, want_mask=True, tc=True)
+    torch.cuda.synchronize()
+    for Wx, P, mk in zip((W, W2), Ps, masks):
+        mask_ref, v_ref, c_ref, m_ref = oracle.prune_pack(Wx, V, M)
+        assert np.array_equal(u32(mk), mask_ref)
+        v, c, m = packed_np(P)
+        assert np.array_equal(v, v_ref) and np.array_equal(c, c_ref) and np.array_equal(m, m_ref)
+
+
+def test_batched_eight_entries_vs_oracle():
+    """The batched pass at its maximum of 8 weights in one launch (mixed shapes, one (V, M)): EVERY entry vs the
+    oracle, byte for byte (not only against single GPU calls)."""
+    shapes = [(1152, 384), (384, 384), (1536, 384), (384, 1536), (70, 23), (200, 333), (64, 4), (130, 1000)]
+    Ws = [synth.weights(r, c, seed=5 * r + c, kind=k) for (r, c), k in
+          zip(shapes, ["outlier", "normal", "wide", "int", "normal", "wide", "int", "outlier"])]
+    Ps, masks = vnm.prune_compress_batched([to_dev_bf16(W) for W in Ws], 64, 5, want_mask=True, tc=True)
+    torch.cuda.synchronize()
+    for W, P, mk in zip(Ws, Ps, masks):
+        mask_ref, v_ref, c_ref, m_ref = oracle.prune_pack(W, 64, 5)
+        assert np.array_equal(u32(mk), mask_ref)
+        v, c, m = packed_np(P)
+        assert np.array_equal(v, v_ref) and np.array_equal(c, c_ref) and np.array_equal(m, m_ref)

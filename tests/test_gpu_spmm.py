@@ -146,8 +146,8 @@ def test_llama_decode_full(T):
 @pytest.mark.parametrize("rows,cols,T,M", [(70, 23, 3, 5), (200, 333, 17, 7), (128, 1000, 32, 8), (64, 4, 1, 4),
                                            (130, 2048, 24, 6), (4096, 11008, 9, 5), (11008, 4096, 31, 4)])
 def test_slab_plan(rows, cols, T, M):
-    """The small-T plan (T <= 32, M <= 8): dense X^T slab per stage by TMA, gather in shared memory;
-    ragged rows / channels / tokens, split-K on the Llama shapes, every output compared."""
+    """The small-T plan (T <= 32): dense X^T slice per unit by TMA, the kept rows gathered by ldmatrix;
+    ragged rows / channels / tokens, stream-K splits on the Llama shapes, every output compared."""
     W, XT, Wm = make(rows, cols, 64, M, T, seed=rows + cols + T)
     Yref, Aref = oracle.gemm_ref(XT, Wm)
     assert_within(gpu_y(W, XT, 64, M, T), Yref, Aref)
@@ -227,30 +227,6 @@ def test_v128_without_window_form_is_unsupported():
 
 
 
-def test_decode_mma_sp_kernel_opt_in():
-    """The register-direct mma.sp decode kernel (spmm_dec.cu, opt-in VNM_DEC=1) against the oracle, in a child
-    process so the plan switch is seen at library load."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, oracle\n"
-        "from paper_2410_16135_b200 import synth, vnm\n"
-        "from tests.gpu_util import to_dev_bf16\n"
-        "for rows, cols, M, T in [(256, 1000, 5, 1), (192, 333, 8, 16), (4096, 4096, 5, 8), (128, 64, 7, 13)]:\n"
-        "    W = synth.weights(rows, cols, seed=rows + T); XT = synth.activations_t(cols, T, seed=cols + T)\n"
-        "    mask = oracle.prune(W, 64, M)\n"
-        "    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, mask, 64, M))\n"
-        "    P = vnm.prune_compress(to_dev_bf16(W), 64, M)\n"
-        "    Y = vnm.spmm(to_dev_bf16(XT), P, T=T).cpu().numpy().astype(np.float64)\n"
-        "    assert np.all(np.abs(Y - Yref) <= oracle.tolerance(Yref, Aref)), (rows, cols, M, T)\n"
-        "print('ok')\n")
-    import os
-    env = dict(os.environ, VNM_DEC="1")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
-
-
 def test_pair_resident_kernel_forced():
     """The CTA-pair resident-A kernel (spmm_tc3.cu) on every shape class it accepts — fp32 and bf16 Y^T, ragged
     rows / K / tokens (T % 8 != 0 exercises the element-wise tail stores), every window-form M, V = 32 / 128 —
@@ -307,8 +283,7 @@ def test_chained_small_t_layers_see_the_previous_output(graph):
     MLP), eagerly and replayed from a CUDA graph.  The small-T plan is launched with programmatic dependent
     launch; its griddepcontrol.wait (after the prologue) is what orders the second kernel's reads after the
     first's writes.  Y1's buffer is NaN-filled first, so a read of unwritten data shows as NaN / a mismatch.
-    (A build with the wait removed still passed this test — the race window is narrow — so it checks the
-    chained path, not the absence of the race.)"""
+    (The race itself is pinned by test_pdl_wait_orders_reads_after_a_delayed_producer.)"""
     T, M = 16, 5
     W1 = synth.weights(256, 512, seed=31)
     W2 = synth.weights(384, 256, seed=32)
@@ -343,3 +318,158 @@ def test_chained_small_t_layers_see_the_previous_output(graph):
     Wm2 = oracle.apply_mask(W2, oracle.prune(W2, 64, M), 64, M)
     Yref, Aref = oracle.gemm_ref(y1, Wm2)
     assert_within(Y2.cpu().numpy().astype(np.float64), Yref, Aref)
+
+
+# ---------------------------------------------------------------------------------------------- small-T plan
+@pytest.mark.parametrize("rows,cols,V,M,T", [
+    (256, 640, 128, 5, 16), (384, 1000, 128, 8, 1), (300, 2000, 128, 9, 7), (512, 1500, 128, 10, 16),
+    (200, 777, 128, 11, 24), (640, 3000, 128, 13, 32), (256, 640, 32, 5, 9), (130, 500, 32, 7, 16),
+    (200, 300, 16, 5, 5), (96, 257, 16, 8, 32), (512, 1024, 256, 5, 16), (600, 999, 256, 6, 3),
+    (192, 640, 64, 9, 16), (130, 1100, 64, 13, 8), (256, 4096, 64, 16, 16), (64, 100, 64, 32, 12),
+    (1000, 333, 64, 4, 17)])
+def test_smallt_any_v_any_m(rows, cols, V, M, T):
+    """The small-T plan reads only the canonical arrays (A_n / A_i1 / A_i2), so it serves every V >= 16 and
+    every M — incl. the paper's 128:2:9 / 10 / 11 / 13 points (tab:bs-sped, P:656-665) — at decode sizes;
+    ragged rows, channels and tokens, fp32 and bf16 Y^T, every output compared."""
+    W, XT, Wm = make(rows, cols, V, M, T, seed=rows + cols + V + M + T, wkind="outlier")
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, V, M, T), Yref, Aref)
+    assert_within(gpu_y(W, XT, V, M, T, out_dtype=torch.bfloat16), Yref, Aref, bf16=True)
+
+
+@pytest.mark.parametrize("V,M", [(128, 5), (128, 8), (128, 13), (64, 16)])
+@pytest.mark.parametrize("T", [1, 16])
+def test_llama_decode_any_vm_full(V, M, T):
+    """Llama up 11008 x 4096 at decode sizes for the paper's V = 128 points and 64:2:16, every output compared."""
+    rows, cols = 11008, 4096
+    W = synth.weights(rows, cols, seed=60 + T + M, kind="outlier")
+    XT = synth.activations_t(cols, T, seed=70 + T)
+    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, oracle.prune(W, V, M), V, M))
+    assert_within(gpu_y(W, XT, V, M, T, out_dtype=torch.bfloat16), Yref, Aref, bf16=True)
+
+
+def _spmm_raw(Xd, P, T, Y, ws, ws_bytes):
+    """vnm_spmm through the C ABI with an explicit (possibly NULL) workspace."""
+    import ctypes
+    cp = P.c()
+    st = vnm.lib().vnm_spmm(ctypes.c_void_p(Xd.data_ptr()), Xd.stride(0), T, ctypes.byref(cp),
+                            ctypes.c_void_p(Y.data_ptr()), Y.stride(0),
+                            vnm.VNM_BF16 if Y.dtype == torch.bfloat16 else vnm.VNM_F32,
+                            None if ws is None else ctypes.c_void_p(ws.data_ptr()), ws_bytes,
+                            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert st == 0, vnm.status_string(st)
+
+
+@pytest.mark.parametrize("rows,cols,M,T", [(11008, 4096, 5, 16), (4096, 11008, 5, 3), (300, 777, 9, 20)])
+def test_smallt_without_workspace(rows, cols, M, T):
+    """No workspace: the small-T plan gives every CTA whole row groups (nothing is cut between CTAs)."""
+    W, XT, Wm = make(rows, cols, 64, M, T, seed=rows + M + T)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    P = vnm.prune_compress(to_dev_bf16(W), 64, M)
+    Y = torch.empty((rows, (T + 7) // 8 * 8), dtype=torch.float32, device="cuda")[:, :T]
+    _spmm_raw(to_dev_bf16(XT), P, T, Y, None, 0)
+    torch.cuda.synchronize()
+    assert_within(Y.cpu().numpy().astype(np.float64), Yref, Aref)
+
+
+def test_workspace_reused_across_shapes():
+    """ONE workspace (zeroed once, sized for the largest call) serves calls of different geometry and T in any
+    order on a stream (include/vnm.h): the tickets sit at a fixed offset and every call leaves them zero, so
+    the partials one call leaves behind never look like tickets to the next."""
+    shapes = [(11008, 4096, 5, 32), (4096, 11008, 5, 16), (4096, 4096, 5, 8), (11008, 4096, 5, 1), (512, 3000, 11, 24)]
+    cases = []
+    for i, (rows, cols, M, T) in enumerate(shapes):
+        W, XT, Wm = make(rows, cols, 64, M, T, seed=100 + i)
+        Yref, Aref = oracle.gemm_ref(XT, Wm)
+        cases.append((vnm.prune_compress(to_dev_bf16(W), 64, M), to_dev_bf16(XT), T, Yref, Aref))
+    nws = max(vnm.spmm_workspace_bytes(P.g, T) for P, _, T, _, _ in cases)
+    ws = torch.empty(nws // 4 + 4, dtype=torch.float32, device="cuda")
+    assert vnm.lib().vnm_spmm_workspace_init(ctypes_ptr(ws), ws.numel() * 4, None) == 0
+    for rep in range(2):
+        for P, Xd, T, Yref, Aref in (cases if rep == 0 else cases[::-1]):
+            Y = torch.empty((P.g.rows, (T + 7) // 8 * 8), dtype=torch.float32, device="cuda")[:, :T]
+            _spmm_raw(Xd, P, T, Y, ws, ws.numel() * 4)
+            torch.cuda.synchronize()
+            assert_within(Y.cpu().numpy().astype(np.float64), Yref, Aref)
+
+
+def ctypes_ptr(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def test_previous_small_t_plan_forced():
+    """The previous small-T plan (spmm_pair.cu, tcgen05 with two V-blocks per M = 128 MMA), forced with
+    VNM_SMALLT=0 in a child process, on the shapes it accepts (V = 64, M <= 8, T <= 32)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, oracle\n"
+        "from paper_2410_16135_b200 import synth, vnm\n"
+        "from tests.gpu_util import to_dev_bf16\n"
+        "for rows, cols, M, T in [(256, 1000, 5, 1), (192, 333, 8, 16), (4096, 4096, 5, 8), (128, 64, 7, 13)]:\n"
+        "    W = synth.weights(rows, cols, seed=rows + T); XT = synth.activations_t(cols, T, seed=cols + T)\n"
+        "    mask = oracle.prune(W, 64, M)\n"
+        "    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, mask, 64, M))\n"
+        "    P = vnm.prune_compress(to_dev_bf16(W), 64, M)\n"
+        "    Y = vnm.spmm(to_dev_bf16(XT), P, T=T).cpu().numpy().astype(np.float64)\n"
+        "    assert np.all(np.abs(Y - Yref) <= oracle.tolerance(Yref, Aref)), (rows, cols, M, T)\n"
+        "print('ok')\n")
+    env = dict(os.environ, VNM_SMALLT="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_pdl_wait_orders_reads_after_a_delayed_producer():
+    """The small-T SpMM is launched with programmatic dependent launch and reads its X^T only after
+    griddepcontrol.wait.  Here its producer is a one-CTA kernel (test-only probe library) that releases its
+    dependents at once and writes X^T only after spinning ~0.5 ms, so the SpMM's CTAs run DURING the spin: a
+    missing or misplaced wait reads the NaN-filled buffer and fails this test every time, not by chance."""
+    import ctypes
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    probe = os.path.join(root, "tests", "probes", "libvnm_probe.so")
+    if not os.path.exists(probe):
+        pytest.skip("tests/probes/libvnm_probe.so not built")
+    PL = ctypes.CDLL(probe)
+    PL.vnm_probe_delayed_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_longlong,
+                                          ctypes.c_void_p]
+    rows, cols, M, T = 4096, 4096, 5, 16
+    W, XT, Wm = make(rows, cols, 64, M, T, seed=321)
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    P = vnm.prune_compress(to_dev_bf16(W), 64, M)
+    src = to_dev_bf16(XT)
+    assert src.stride(0) == T
+    X = torch.empty_like(src)
+    Y = torch.empty((rows, T), dtype=torch.float32, device="cuda")
+    ws = vnm.spmm_workspace(P.g, T, "cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        X.fill_(float("nan"))
+        Y.zero_()
+        assert PL.vnm_probe_delayed_copy(X.data_ptr(), src.data_ptr(), X.numel() * 2, 1_000_000,
+                                         stream.cuda_stream) == 0
+        vnm.spmm(X, P, T=T, out=Y, workspace=ws)
+        torch.cuda.synchronize()
+        assert not torch.isnan(Y).any()
+        assert_within(Y.cpu().numpy().astype(np.float64), Yref, Aref)
+
+
+def test_binding_validates_out_and_xt():
+    """vnm.spmm checks `out` / `XT` extents and strides before the call (an undersized or strided `out` would
+    otherwise become an out-of-bounds device write)."""
+    W = synth.weights(128, 64, seed=1)
+    P = vnm.prune_compress(to_dev_bf16(W), 64, 8)
+    X = to_dev_bf16(synth.activations_t(64, 16, seed=2))
+    with pytest.raises(ValueError):
+        vnm.spmm(X, P, T=16, out=torch.empty((127, 16), device="cuda"))
+    with pytest.raises(ValueError):
+        vnm.spmm(X, P, T=16, out=torch.empty((128, 8), device="cuda"))
+    with pytest.raises(ValueError):
+        vnm.spmm(X, P, T=16, out=torch.empty((16, 128), device="cuda").t())
+    with pytest.raises(ValueError):
+        vnm.spmm(X, P, T=17)
+    with pytest.raises(ValueError):
+        vnm.spmm(X.t().contiguous().t(), P, T=16)
