@@ -22,7 +22,7 @@ PROBES = os.path.join(HERE, "..", "tests", "probes")
 LIBS = {
     os.path.join(HERE, "libvnm.so"): (CSRC, ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "spmm_pair.cu", "pack_tc.cu",
                                            "spmm_tc.cu", "spmm_tc2.cu", "spmm_tc3.cu", "spmm_smallt.cu", "ria.cu", "permute.cu"]),
-    os.path.join(PROBES, "libvnm_probe.so"): (PROBES, ["probes.cu", "probes2.cu", "probes3.cu"]),
+    os.path.join(PROBES, "libvnm_probe.so"): (PROBES, ["probes.cu", "probes2.cu", "probes3.cu", "probes4.cu"]),
 }
 
 
@@ -35,12 +35,16 @@ def _stale(out: str, srcs: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> None:
-    """Each source is compiled to an object in build/ (in parallel, only when stale), then linked."""
+def build(force: bool = False, verbose: bool = False, ablations: bool = False) -> None:
+    """Each source is compiled to an object in build/ (in parallel, only when stale), then linked.
+    ablations=True builds libvnm_abl.so instead (-DVNM_ABLATIONS: the VNM_ABL timing switches; results invalid;
+    experiments only, loaded when VNM_LIB points at it)."""
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build_abl" if ablations else "build")
     os.makedirs(objdir, exist_ok=True)
-    for out, (srcdir, files) in LIBS.items():
+    libs = {os.path.join(HERE, "libvnm_abl.so"): LIBS[os.path.join(HERE, "libvnm.so")]} if ablations else LIBS
+    extra = ["-DVNM_ABLATIONS"] if ablations else []
+    for out, (srcdir, files) in libs.items():
         srcs = [os.path.join(srcdir, f) for f in files]
         if not force and not _stale(out, srcs):
             continue
@@ -50,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> None:
             if not force and not _stale(objs[i], [srcs[i]]):
                 return
             tmp = objs[i] + f".tmp{os.getpid()}"
-            cmd = [NVCC, *ARCH, *FLAGS, "-I", CSRC, "-c", "-o", tmp, srcs[i]]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", CSRC, "-c", "-o", tmp, srcs[i]]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.check_call(cmd)
@@ -67,4 +71,4 @@ def build(force: bool = False, verbose: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, ablations="--ablations" in sys.argv)

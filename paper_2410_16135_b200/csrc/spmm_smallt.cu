@@ -6,11 +6,15 @@
 // (one 2:4 nibble per block and row) and A_i1 (4 column indices per block and V-block) — with a few MACs per
 // weight, so the kernel is a TMA stream with light tensor work on top, and it reads nothing but those arrays and
 // a dense slice of X^T:
-//   * unit of work = 128 rows x 32 column blocks (4 k-steps of logical K = 32): the A_n box [128 rows][64 values]
-//     (128-byte swizzle), the A_i2 box [128 rows][4 words], the A_i1 words of the unit's V-block(s) and the
-//     dense X^T slice of the 32 blocks [32 M channels][TP tokens] arrive by TMA in a ring of S slots (one
-//     producer thread); the X^T slice is L2-resident (every row group re-reads it) and shared by the unit's
-//     two V-blocks (V = 64);
+//   * unit of work = 128 rows x 32 column blocks (4 k-steps of logical K = 32), staged in a ring of S slots by
+//     one producer warp: the A_n box [128 rows][64 values] (128-byte swizzle) by ONE TMA; the A_i2 words
+//     [128 rows][4], the A_i1 words of the unit's V-block(s) and the dense X^T slice of the 32 blocks
+//     [32 M channels][TP tokens] by 16-byte cp.async from all 32 lanes, completing on the same mbarrier
+//     (cp.async.mbarrier.arrive).  Measured (profiles/r02_decode.md): the TMA engine spends about the same time
+//     on every box row whatever its width, and the 16-B A_i2 rows / 32-B X^T rows of a unit were 2/3 of its
+//     rows — boxes of them capped a CTA at ~1 unit per 450 ns.  The X^T slice is L2-resident (every row group
+//     re-reads it), written swizzled (conflict-free for the gather below) and shared by the unit's two
+//     V-blocks (V = 64);
 //   * warp-level sparse MMA (mma.sp::ordered_metadata m16n8k32, bf16 in, fp32 accumulate): A_n IS the
 //     2:4-compressed operand of the gathered product (the block's 2 kept values = one group of 4 gathered
 //     channels) and its A_i2 word is the operand's metadata; the A fragments come from the swizzled A_n box by
@@ -48,11 +52,27 @@ constexpr int kPhases = kCons / 2;
 constexpr int kProd = kCons;       // producer warp index
 constexpr int kThreads = 32 * (kCons + 1);
 constexpr uint32_t kABytes = kRowsU * 128;   // A_n box [128 rows][64 bf16], SW128
-constexpr uint32_t kMBytes = kRowsU * 16;    // A_i2 box [128 rows][4 u32]
-constexpr uint32_t kCRow = kBlkU * 4;        // A_i1 words of one V-block and unit (128 B)
 constexpr uint32_t kTicketWords = 4096;      // fixed ticket region at the start of the workspace (16 KB)
+constexpr int kMBoxUnits = 8;                // units per A_i2 box: [128 rows][8 units x 4 words] = 128 B per row
+constexpr uint32_t kMBoxBytes = kRowsU * 128;
+constexpr int kMB = 3;                       // A_i2 box ring slots
+constexpr uint32_t kCRow = kBlkU * 4;        // A_i1 words of one V-block and unit (128 B)
+
+// VNM_SPMM_TRACE: %globaltimer per CTA — entry, after the prologue, first unit landed, consumers done, exit
+__device__ unsigned long long g_st_t[5][1024];
+__device__ unsigned long long g_st_u[160][32][4];  // VNM_SPMM_TRACE=2: per unit: slot free, landed, consumed, issued
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct StArgs {
+    const uint16_t* XT;
+    const uint32_t* meta;
+    const uint8_t* col_idx;
+    int64_t ldx;
+    int32_t cols, ld_meta, nb_pad, n_vb;
     void* YT;
     int64_t ldy;
     float* ws;           // partials [n_rp][maxseg][128][TP] fp32 (after the ticket region)
@@ -61,9 +81,17 @@ struct StArgs {
     int32_t S;           // ring slots
     int32_t rg_mode;     // 1: shares are whole row groups (no workspace: no piece is ever cut between CTAs)
     int32_t c_rows;      // A_i1 rows (V-blocks) per unit: max(1, 128 / V)
-    int32_t x_rows, x_box, x_nbox;  // X^T slice rows (32 M), rows per TMA box (<= 256), boxes
-    uint32_t x_bytes;    // slice bytes in shared memory (x_rows * TP * 2, rounded to 1 KB)
-    uint32_t slot_bytes, tx_bytes;
+    int32_t x_rows;      // X^T slice rows (32 M channels)
+    int32_t x_pack;      // > 1: X^T viewed as 128-byte lines of x_pack = 64 / ldx channels (SW128); 1: one row per channel
+    int32_t x_l8;        // ldx / 8 (16-byte chunks per channel in the packed view)
+    int32_t x_pack_log2;
+    int32_t x_box, x_nbox;        // rows of the view per TMA box (<= 256), boxes per slice
+    uint32_t x_box_bytes;         // shared-memory bytes per box
+    uint32_t x_bytes;    // slice bytes in shared memory (rounded to 1 KB)
+    uint32_t slot_bytes, tx_bytes, c_bytes;
+    int32_t trace;
+    int32_t abl;  // VNM_ABL timing ablations (-DVNM_ABLATIONS builds only; results invalid): 1 consumers skip the
+                  // MMA work, 2 no X^T slice loads, 8 no A_i2 / A_i1 loads
 };
 
 __device__ __forceinline__ int unit_owner(const StArgs& a, int u) {  // CTA whose share contains unit u
@@ -105,49 +133,85 @@ __device__ __forceinline__ uint32_t xoff(int r, int n) {
 // NT8: token tiles of 8 computed (T <= 8 NT8); VSET: V-blocks per 64-row half (64 / V for V <= 64, else 1)
 template <int NT8, int VSET, bool kBf16>
 __global__ void __launch_bounds__(kThreads, 1)
-    vnm_spmm_smallt_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_m,
-                           const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_x,
+    vnm_spmm_smallt_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_x,
+                           const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_c,
                            const StArgs a) {
     constexpr int TP = NT8 == 1 ? 8 : (NT8 == 2 ? 16 : 32);  // tokens per X^T slice row in shared memory
     extern __shared__ __align__(1024) uint8_t smem[];
-    // slot s: [A_n 16 KB][X^T slice x_bytes][A_i2 2 KB][A_i1 c_rows x 128 B]; then red [128][TP] fp32, barriers
-    float* red = reinterpret_cast<float*>(smem + a.S * a.slot_bytes);
+    // [A_i2 box ring: kMB x 16 KB][slot s: A_n 16 KB | X^T slice x_bytes | A_i1 c_rows x 128 B]
+    // [red [128][TP] fp32][barriers]
+    uint8_t* mbox = smem;
+    uint8_t* slots = smem + kMB * kMBoxBytes;
+    float* red = reinterpret_cast<float*>(slots + a.S * a.slot_bytes);
     uint64_t* full = reinterpret_cast<uint64_t*>(red + kRowsU * TP);
     uint64_t* empty = full + a.S;
-    uint32_t& last_flag = *reinterpret_cast<uint32_t*>(empty + a.S);
+    uint64_t* mfull = empty + a.S;
+    uint64_t* mempty = mfull + kMB;
+    uint32_t& last_flag = *reinterpret_cast<uint32_t*>(mempty + kMB);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int u0 = share_begin(a, blockIdx.x), u1 = share_begin(a, blockIdx.x + 1);
+    const bool tr = a.trace && blockIdx.x < 1024 && threadIdx.x == 0;
+    if (tr) g_st_t[0][blockIdx.x] = gtime();
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.S; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1);   // the producer's expect_tx arrival (+ the TMA bytes)
             mbar_init(&empty[s], 2);  // the two half warps of the phase that consumes the slot
+        }
+        for (int k = 0; k < kMB; ++k) {
+            mbar_init(&mfull[k], 1);
+            mbar_init(&mempty[k], kCons);  // every consumer warp releases every box once
         }
         fence_mbar_init();
     }
     if (warp == kProd && lane == 0) {
         tma_prefetch_desc(&tm_a);
+        tma_prefetch_desc(&tm_x);
         tma_prefetch_desc(&tm_m);
         tma_prefetch_desc(&tm_c);
-        tma_prefetch_desc(&tm_x);
     }
     __syncthreads();
     grid_dep_wait();    // the previous kernel's outputs (this layer's X^T, packed weights) are visible
     grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
+    if (tr) g_st_t[1][blockIdx.x] = gtime();
 
     if (warp == kProd) {
-        // ------------------------------------------------------------ producer: one thread, one unit per slot
+        // ------------------------------------------------------------ producer: lane 0 issues the TMAs (A_n box +
+        // X^T slice boxes).  (L2 prefetches of the A_i2 / A_i1 lines from the other lanes measured slower.)
         if (lane == 0) {
+            // A_i2 words: a few long TMA rows per row group instead of a 16-byte row per unit — boxes
+            // [128 rows][8 units x 4 words] (128-byte swizzle) from the first unit of each piece (row group of the
+            // share) on, in a ring of kMB boxes; box k is issued with the first unit that reads it
+            int k = 0, pend = u0;  // next box; first unit past the last issued box
+            int rp = u0 / a.n_st, st = u0 - rp * a.n_st, s = 0, par = 0;  // (incremental: no divisions per unit)
             for (int u = u0, q = 0; u < u1; ++u, ++q) {
-                const int rp = u / a.n_st, st = u % a.n_st, s = q % a.S;
-                mbar_wait(&empty[s], ((q / a.S) & 1) ^ 1);
-                uint8_t* base = smem + s * a.slot_bytes;
-                mbar_arrive_expect_tx(&full[s], a.tx_bytes);
+                if (u == pend) {
+                    const int pu1 = min(u1, (rp + 1) * a.n_st);
+                    const int ms = k % kMB;
+                    mbar_wait(&mempty[ms], ((k / kMB) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&mfull[ms], kMBoxBytes);
+                    tma_load_2d(mbox + ms * kMBoxBytes, &tm_m, kKS * st, rp * kRowsU, &mfull[ms]);
+                    pend = min(pu1, u + kMBoxUnits);
+                    ++k;
+                }
+                mbar_wait(&empty[s], par ^ 1);
+                if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][0] = gtime();
+                uint8_t* base = slots + s * a.slot_bytes;
+                mbar_arrive_expect_tx(&full[s], (a.abl & 2) ? kABytes + a.c_bytes : a.tx_bytes);
                 tma_load_2d(base, &tm_a, st * 2 * kBlkU, rp * kRowsU, &full[s]);
-                for (int b = 0; b < a.x_nbox; ++b)
-                    tma_load_2d(base + kABytes + b * a.x_box * TP * 2, &tm_x, 0, st * kBlkU * a.M + b * a.x_box, &full[s]);
-                tma_load_2d(base + kABytes + a.x_bytes, &tm_m, st * kKS, rp * kRowsU, &full[s]);
-                tma_load_2d(base + kABytes + a.x_bytes + kMBytes, &tm_c, st * kBlkU, (rp * kRowsU) / a.V, &full[s]);
+                const int y0 = (st * kBlkU * a.M) >> a.x_pack_log2;  // first row of the slice in the X^T view
+                for (int b = 0; b < ((a.abl & 2) ? 0 : a.x_nbox); ++b)
+                    tma_load_2d(base + kABytes + b * a.x_box_bytes, &tm_x, 0, y0 + b * a.x_box, &full[s]);
+                tma_load_2d(base + kABytes + a.x_bytes, &tm_c, st * kBlkU, (rp * kRowsU) / a.V, &full[s]);
+                if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][3] = gtime();
+                if (++s == a.S) {
+                    s = 0;
+                    par ^= 1;
+                }
+                if (++st == a.n_st) {
+                    st = 0;
+                    ++rp;
+                }
             }
         }
         return;
@@ -159,6 +223,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hsh = 16 * (c & 1);  // metadata half of this thread (selector 0: threads c = 0, 1 of each group)
     const int cons_tid = threadIdx.x;  // 0 .. 255
     float acc[4][NT8][4];
+    int k_piece = 0;  // first A_i2 box of the current piece (the producer's order)
+    int k_rel = 0;    // first box this warp has not released yet
+    // release boxes [k_rel, k_end) (each waited on first: a box is released only after it was (re)issued, so the
+    // arrivals of consecutive uses of a ring slot never mix)
+    auto release_to = [&](int k_end) {
+        for (; k_rel < k_end; ++k_rel) {
+            mbar_wait(&mfull[k_rel % kMB], (k_rel / kMB) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mempty[k_rel % kMB]);
+        }
+    };
 
     for (int pu0 = u0; pu0 < u1;) {
         const int rp = pu0 / a.n_st;
@@ -172,59 +247,95 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool half_ok = rp * kRowsU + 64 * h < a.rows_p;
         // this phase's units of the piece: u = u0 + q, q = p (mod 4)
         int u = pu0 + ((p - (pu0 - u0)) % kPhases + kPhases) % kPhases;
+        int s = (u - u0) % a.S, par = ((u - u0) / a.S) & 1;  // slot / phase parity, advanced without divisions
         for (; u < pu1; u += kPhases) {
-            const int q = u - u0, s = q % a.S;
-            mbar_wait(&full[s], (q / a.S) & 1);
-            if (half_ok) {
-                const int st = u % a.n_st;
-                const int nks = min(kKS, a.n_ks - st * kKS);
-                const uint32_t sA = smem_u32(smem + s * a.slot_bytes);
-                const uint32_t sX = sA + kABytes, sM = sX + a.x_bytes, sC = sM + kMBytes;
-                // A_i2 words of rows g, g + 8 of every m16 tile of this half (4 words = the unit's 4 k-steps)
-                uint32_t w0[4][4], w1[4][4];
+            const int q = u - u0;
+            const int kb = k_piece + (u - pu0) / kMBoxUnits, ub = (u - pu0) % kMBoxUnits;
+            release_to(kb);
+            mbar_wait(&mfull[kb % kMB], (kb / kMB) & 1);
+            mbar_wait(&full[s], par);
+            if (tr && q == 0) g_st_t[2][blockIdx.x] = gtime();
+            if (a.trace == 2 && lane == 0 && h == 0 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][1] = gtime();
+            if (half_ok && !(a.abl & 1)) {
+                const uint32_t sA = smem_u32(slots + s * a.slot_bytes);
+                const uint32_t sX = sA + kABytes, sC = sX + a.x_bytes;
+                const uint32_t sMb = smem_u32(mbox + (kb % kMB) * kMBoxBytes);
+                // A_i2 words of this unit for rows g, g + 8 of every m16 tile (4 words = the unit's 4 k-steps):
+                // row r of the box holds 8 units x 16 B, 16-byte chunk ub at ub ^ (r % 8) (SW128)
+                uint4 w0[4], w1[4];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) {
-                    const int r0 = 64 * h + 16 * mt + g;
+                    const int r0 = 64 * h + 16 * mt + g;  // (r0 + 8) % 8 == r0 % 8
+                    const uint32_t o = 16u * ((ub ^ r0) & 7);
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(w0[mt][0]), "=r"(w0[mt][1]), "=r"(w0[mt][2]), "=r"(w0[mt][3])
-                                 : "r"(sM + 16 * r0));
+                                 : "=r"(w0[mt].x), "=r"(w0[mt].y), "=r"(w0[mt].z), "=r"(w0[mt].w)
+                                 : "r"(sMb + 128u * r0 + o));
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(w1[mt][0]), "=r"(w1[mt][1]), "=r"(w1[mt][2]), "=r"(w1[mt][3])
-                                 : "r"(sM + 16 * (r0 + 8)));
+                                 : "=r"(w1[mt].x), "=r"(w1[mt].y), "=r"(w1[mt].z), "=r"(w1[mt].w)
+                                 : "r"(sMb + 128u * (r0 + 8) + o));
                 }
-                // ldmatrix roles: matrix j = lane / 8 (rows +8 for j odd, 16-byte chunk +1 for j >= 2), row lane % 8
+                // Manually scheduled (in-order issue; the asm statements keep program order): the A_i1 words of
+                // all k-steps first, the gathered B fragments one k-step ahead of their MMAs, the 4 A fragments of
+                // a k-step before its MMAs.  K-steps past n_ks are computed too: their A values are zero (TMA
+                // zero fill past ld_val) and their metadata the pad pattern, so they add exact zeros.
                 const int jm = lane >> 3, rr = lane & 7;
+                uint32_t cwv[kKS][VSET];
 #pragma unroll
-                for (int ks = 0; ks < kKS; ++ks) {
-                    if (ks >= nks) break;
-                    // B: lane i addresses gathered K-row i of the k-step = block 8 ks + i / 4, A_i1 position i % 4
-                    uint32_t B[VSET][NT8][4];
+                for (int ks = 0; ks < kKS; ++ks)
 #pragma unroll
                     for (int v = 0; v < VSET; ++v) {
                         const int crow = a.c_rows == 1 ? 0 : h * VSET + v;
-                        const int blk = 8 * ks + (lane >> 2);
-                        uint32_t cw;
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(sC + crow * kCRow + 4 * blk));
-                        const int xr = blk * a.M + static_cast<int>((cw >> (8 * (lane & 3))) & 0xFFu);
-#pragma unroll
-                        for (int n = 0; n < NT8; ++n) ldsm_x4_t(sX + xoff<TP>(xr, n), B[v][n]);
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cwv[ks][v]) : "r"(sC + crow * kCRow + 4 * (8 * ks + (lane >> 2))));
                     }
+                // B of k-step ks: lane i addresses gathered K-row i = block 8 ks + i / 4, A_i1 position i % 4
+                auto load_b = [&](int ks, uint32_t (&B)[VSET][NT8][4]) {
+#pragma unroll
+                    for (int v = 0; v < VSET; ++v) {
+                        const int xr = (8 * ks + (lane >> 2)) * a.M + static_cast<int>((cwv[ks][v] >> (8 * (lane & 3))) & 0xFFu);
+#pragma unroll
+                        for (int n = 0; n < NT8; ++n) {
+                            uint32_t off;
+                            if (a.x_pack > 1) {  // X^T viewed as 128-byte lines of x_pack channels (SW128)
+                                const int line = xr >> a.x_pack_log2;
+                                const int ch = (xr & (a.x_pack - 1)) * a.x_l8 + n;
+                                off = 128u * line + 16u * ((ch ^ line) & 7);
+                            } else {
+                                off = xoff<TP>(xr, n);
+                            }
+                            ldsm_x4_t(sX + off, B[v][n]);
+                        }
+                    }
+                };
+                uint32_t Bb[2][VSET][NT8][4];
+                load_b(0, Bb[0]);
+#pragma unroll
+                for (int ks = 0; ks < kKS; ++ks) {
+                    if (ks + 1 < kKS) load_b(ks + 1, Bb[(ks + 1) & 1]);
+                    uint32_t A[4][4];
 #pragma unroll
                     for (int mt = 0; mt < 4; ++mt) {
                         const int row = 64 * h + 16 * mt + rr + 8 * (jm & 1);
                         const int chunk = 2 * ks + (jm >> 1);
-                        uint32_t A[4];
-                        ldsm_x4(sA + 128 * row + 16 * ((chunk ^ row) & 7), A);
-                        const uint32_t e = ((w0[mt][ks] >> hsh) & 0xFFFFu) | (((w1[mt][ks] >> hsh) & 0xFFFFu) << 16);
+                        ldsm_x4(sA + 128 * row + 16 * ((chunk ^ row) & 7), A[mt]);
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) {
+                        const uint32_t x0 = ks == 0 ? w0[mt].x : ks == 1 ? w0[mt].y : ks == 2 ? w0[mt].z : w0[mt].w;
+                        const uint32_t x1 = ks == 0 ? w1[mt].x : ks == 1 ? w1[mt].y : ks == 2 ? w1[mt].z : w1[mt].w;
+                        const uint32_t e = ((x0 >> hsh) & 0xFFFFu) | (((x1 >> hsh) & 0xFFFFu) << 16);
                         const int v = mt / (4 / VSET);
 #pragma unroll
-                        for (int n = 0; n < NT8; ++n) mma_sp_16832(acc[mt][n], A, B[v][n], e);
+                        for (int n = 0; n < NT8; ++n) mma_sp_16832(acc[mt][n], A[mt], Bb[ks & 1][v][n], e);
                     }
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if (a.trace == 2 && lane == 0 && h == 0 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][2] = gtime();
+            for (s += kPhases; s >= a.S; s -= a.S) par ^= 1;
         }
+        k_piece += (pu1 - pu0 + kMBoxUnits - 1) / kMBoxUnits;
+        release_to(k_piece);  // the piece's boxes are done (also those this warp had no unit in)
         // ---- end of the piece: phases 0..3 added in order through red[128][TP]
 #pragma unroll 1
         for (int r = 0; r < kPhases; ++r) {
@@ -289,39 +400,72 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (whole) {
             store_rows([&](int r, int t) { return red[r * TP + t]; });
         } else {
-            // a cut row group: publish this CTA's piece; the last CTA to arrive adds the pieces in CTA order
+            // a cut row group: publish this CTA's piece; the last CTA to arrive adds the pieces in CTA order.
+            // Ordering (the CUTLASS semaphore pattern): the pieces' stores, bar.sync, ONE acq_rel atomic by
+            // thread 0 (release: cumulative over the CTA's stores through the barrier; acquire: the last arriver's
+            // reads below, ordered after it by the next barrier).
             const int own0 = unit_owner(a, rp * a.n_st);
             const int nseg = unit_owner(a, rp * a.n_st + a.n_st - 1) - own0 + 1;
+            const int me = static_cast<int>(blockIdx.x) - own0;
             float* wsr = a.ws + static_cast<int64_t>(rp) * a.maxseg * kRowsU * TP;
-            float4* mine = reinterpret_cast<float4*>(wsr + static_cast<int64_t>(blockIdx.x - own0) * kRowsU * TP);
-            const float4* red4 = reinterpret_cast<const float4*>(red);
-            for (int i = cons_tid; i < kRowsU * TP / 4; i += 32 * kCons) __stcg(mine + i, red4[i]);
-            __threadfence();
+            float4* red4 = reinterpret_cast<float4*>(red);
+            float4* mine = reinterpret_cast<float4*>(wsr + static_cast<int64_t>(me) * kRowsU * TP);
+            constexpr int kN4 = kRowsU * TP / 4;  // float4 groups per piece
+            for (int i = cons_tid; i < kN4; i += 32 * kCons) __stcg(mine + i, red4[i]);
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
-            if (cons_tid == 0) last_flag = atomicAdd(&a.tickets[rp], 1u) == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
+            if (cons_tid == 0) {
+                uint32_t old;
+                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.tickets + rp) : "memory");
+                last_flag = old == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
+            }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
             if (last_flag) {
-                __threadfence();
-                store_rows([&](int r, int t) {
-                    float v = 0.f;
-                    for (int j = 0; j < nseg; ++j) v += __ldcg(wsr + (static_cast<int64_t>(j) * kRowsU + r) * TP + t);
-                    return v;
-                });
+                // every piece of the row group, added in CTA order (j = 0 .. nseg-1; this CTA's own from shared
+                // memory): all loads of a group first, then the ordered sum
+                constexpr int kPer = (kN4 + 32 * kCons - 1) / (32 * kCons);
+                constexpr int kMaxSeg = 8;
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    const int i = cons_tid + k * 32 * kCons;
+                    if (i >= kN4) break;
+                    float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int j0 = 0; j0 < nseg; j0 += kMaxSeg) {
+                        float4 v[kMaxSeg];
+#pragma unroll
+                        for (int j = 0; j < kMaxSeg; ++j)
+                            if (j0 + j < nseg)
+                                v[j] = j0 + j == me ? red4[i]
+                                                    : __ldcg(reinterpret_cast<const float4*>(wsr + static_cast<int64_t>(j0 + j) * kRowsU * TP) + i);
+#pragma unroll
+                        for (int j = 0; j < kMaxSeg; ++j)
+                            if (j0 + j < nseg) {
+                                acc4.x += v[j].x;
+                                acc4.y += v[j].y;
+                                acc4.z += v[j].z;
+                                acc4.w += v[j].w;
+                            }
+                    }
+                    red4[i] = acc4;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
+                store_rows([&](int r, int t) { return red[r * TP + t]; });
                 if (cons_tid == 0) a.tickets[rp] = 0u;  // ready for the next launch (stream order)
             }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");  // red is reused by the next piece
         pu0 = pu1;
     }
+    if (tr) g_st_t[3][blockIdx.x] = gtime();
 }
 
 struct StPlan {
-    int n_rp, n_ks, n_st, units, grid, maxseg, S, tp, c_rows, x_rows, x_box, x_nbox;
-    uint32_t x_bytes, slot_bytes;
+    int n_rp, n_ks, n_st, units, grid, maxseg, S, tp, c_rows, x_rows, x_pack, x_box, x_nbox;
+    uint32_t x_box_bytes, x_bytes, slot_bytes;
     size_t smem, ws_bytes;
 };
 
-StPlan make_plan(const vnm_geom& g, int32_t T) {
+// ldx: X^T's leading dimension (0: assume ldx == TP, the dense case; only the X^T view / box shape depend on it)
+StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
     StPlan p{};
     p.n_rp = (g.rows_p + kRowsU - 1) / kRowsU;
     p.n_ks = g.nb_pad / 8;
@@ -331,12 +475,18 @@ StPlan make_plan(const vnm_geom& g, int32_t T) {
     p.tp = T <= 8 ? 8 : (T <= 16 ? 16 : 32);
     p.c_rows = g.V >= kRowsU ? 1 : kRowsU / g.V;
     p.x_rows = kBlkU * g.M;
-    p.x_nbox = (p.x_rows + 255) / 256;
-    p.x_box = (p.x_rows + p.x_nbox - 1) / p.x_nbox;
-    p.x_box = (p.x_box + 7) / 8 * 8;  // whole 8-row swizzle atoms per box
-    p.x_bytes = static_cast<uint32_t>(p.x_nbox * p.x_box * p.tp * 2 + 1023) / 1024 * 1024;
-    p.slot_bytes = (kABytes + p.x_bytes + kMBytes + p.c_rows * kCRow + 1023) / 1024 * 1024;
-    const size_t fixed = static_cast<size_t>(kRowsU) * p.tp * 4 + 2 * 16 * 8 + 64;
+    // X^T slice by TMA: with a dense X^T (ldx == TP) the slice rows are contiguous, so it is viewed as 128-byte
+    // lines of 64 / TP channels (4x fewer, 4x longer TMA rows at TP = 16; SW128); otherwise one row per channel
+    if (ldx == 0) ldx = p.tp;
+    p.x_pack = (ldx == p.tp && g.cols % (64 / p.tp) == 0) ? 64 / p.tp : 1;
+    const int vrows = p.x_rows / p.x_pack;                  // rows of the X^T view per slice
+    const uint32_t row_bytes = p.x_pack > 1 ? 128u : static_cast<uint32_t>(p.tp * 2);
+    p.x_nbox = (vrows + 255) / 256;
+    p.x_box = ((vrows + p.x_nbox - 1) / p.x_nbox + 7) / 8 * 8;  // whole 8-row swizzle atoms per box
+    p.x_box_bytes = static_cast<uint32_t>(p.x_box) * row_bytes;
+    p.x_bytes = (p.x_nbox * p.x_box_bytes + 1023) / 1024 * 1024;
+    p.slot_bytes = (kABytes + p.x_bytes + p.c_rows * kCRow + 1023) / 1024 * 1024;
+    const size_t fixed = static_cast<size_t>(kMB) * kMBoxBytes + static_cast<size_t>(kRowsU) * p.tp * 4 + (2 * 16 + 2 * kMB) * 8 + 64;
     p.S = static_cast<int>((kMaxSmem - fixed) / p.slot_bytes);
     if (p.S > 16) p.S = 16;
     p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
@@ -359,6 +509,36 @@ int launch_nt(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUten
     cudaError_t e = launch_pdl(true, k, dim3(p.grid), dim3(kThreads), p.smem, st, tm[0], tm[1], tm[2], tm[3], a);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess && a.trace) {
+        static unsigned long long h[5][1024];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_st_t, sizeof(h));
+        unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0}, mn[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+        const int n = p.grid < 1024 ? p.grid : 1024;
+        for (int i = 0; i < n; ++i) t0 = h[0][i] < t0 ? h[0][i] : t0;
+        for (int j = 0; j < 4; ++j)
+            for (int i = 0; i < n; ++i) {
+                const unsigned long long v = h[j][i] - t0;
+                mx[j] = v > mx[j] ? v : mx[j];
+                mn[j] = v < mn[j] ? v : mn[j];
+            }
+        fprintf(stderr, "smallt grid %d S %d units %d slot %u B: entry %llu..%llu  prologue %llu..%llu  first %llu..%llu  "
+                        "done %llu..%llu ns\n", p.grid, p.S, p.units, p.slot_bytes, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2],
+                mn[3], mx[3]);
+        if (a.trace == 2) {
+            static unsigned long long u[160][32][4];
+            cudaMemcpyFromSymbol(u, g_st_u, sizeof(u));
+            for (int i = 0; i < n && i < 160; ++i) {
+                const int nu = static_cast<int>(static_cast<long long>(i + 1) * p.units / p.grid -
+                                                static_cast<long long>(i) * p.units / p.grid);
+                fprintf(stderr, "cta %3d done %6llu:", i, h[3][i] - t0);
+                for (int q = 0; q < nu && q < 32; ++q)
+                    fprintf(stderr, " [%llu %llu %llu %llu]", (u[i][q][0] - t0) / 10, (u[i][q][3] - t0) / 10,
+                            (u[i][q][1] - t0) / 10, (u[i][q][2] - t0) / 10);
+                fprintf(stderr, "\n");
+            }
+        }
+    }
     return e == cudaSuccess ? 0 : kLaunchCudaError;
 }
 
@@ -386,7 +566,7 @@ size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T) {
 int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
     if (!spmm_smallt_applies(g, L.T)) return kLaunchUnsupported;
-    const StPlan p = make_plan(g, L.T);
+    const StPlan p = make_plan(g, L.T, L.ldx);
     StArgs a{};
     // without a workspace (or a too small one) every CTA takes whole row groups: nothing is cut, no tickets
     a.rg_mode = (!L.workspace || L.workspace_bytes < p.ws_bytes) ? 1 : 0;
@@ -411,27 +591,47 @@ int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) {
     a.S = p.S;
     a.c_rows = p.c_rows;
     a.x_rows = p.x_rows;
+    a.x_pack = p.x_pack;
+    a.x_l8 = static_cast<int32_t>(L.ldx / 8);
+    a.x_pack_log2 = p.x_pack == 8 ? 3 : p.x_pack == 4 ? 2 : p.x_pack == 2 ? 1 : 0;
     a.x_box = p.x_box;
     a.x_nbox = p.x_nbox;
+    a.x_box_bytes = p.x_box_bytes;
     a.x_bytes = p.x_bytes;
     a.slot_bytes = p.slot_bytes;
-    a.tx_bytes = kABytes + static_cast<uint32_t>(p.x_nbox * p.x_box * p.tp * 2) + kMBytes + p.c_rows * kCRow;
+    a.c_bytes = p.c_rows * kCRow;
+    a.tx_bytes = kABytes + static_cast<uint32_t>(p.x_nbox) * p.x_box_bytes + a.c_bytes;
+    a.XT = L.XT;
+    a.meta = L.P->meta;
+    a.col_idx = L.P->col_idx;
+    a.ldx = L.ldx;
+    a.cols = g.cols;
+    a.ld_meta = g.ld_meta;
+    a.nb_pad = g.nb_pad;
+    a.n_vb = g.rows_p / g.V;
+    a.trace = VNM_ENV_INT("VNM_SPMM_TRACE", 0);
+    a.abl = VNM_ABLATION_FLAGS();
+    // A_n [rows_p][ld_val] bf16, boxes [128 rows][64 values]; X^T as lines of x_pack channels [cols / x_pack][64]
+    // (SW128) or [cols][T] (boxes TP wide, 32B / 64B swizzle).  Past an edge boxes are zero-filled (rows past
+    // rows_p, pad k-steps, channels past cols, tokens past T).
     CUtensorMap tm[4];
-    const CUtensorMapSwizzle xsw = p.tp == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
-                                             : (p.tp == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
-    // A_n [rows_p][ld_val] bf16; A_i2 [rows_p][ld_meta] u32 (k-steps nb_pad / 8 wide); A_i1 [rows_p / V][nb_pad]
-    // u32; X^T [cols][ldx] bf16 (T wide).  Boxes past an edge are zero-filled (pad k-steps, rows, tokens).
-    if (!encode_2d(&tm[0], L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
-                   static_cast<uint64_t>(g.ld_val) * 2, 64, kRowsU) ||
-        !encode_2d(&tm[1], L.P->meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
-                   static_cast<uint64_t>(g.ld_meta) * 4, kKS, kRowsU, CU_TENSOR_MAP_DATA_TYPE_UINT32,
-                   CU_TENSOR_MAP_SWIZZLE_NONE) ||
-        !encode_2d(&tm[2], L.P->col_idx, static_cast<uint64_t>(g.nb_pad), static_cast<uint64_t>(g.rows_p / g.V),
-                   static_cast<uint64_t>(g.nb_pad) * 4, kBlkU, static_cast<uint32_t>(p.c_rows),
-                   CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-        !encode_2d(&tm[3], L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols),
-                   static_cast<uint64_t>(L.ldx) * 2, static_cast<uint32_t>(p.tp), static_cast<uint32_t>(p.x_box),
-                   CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw))
+    const CUtensorMapSwizzle xsw = p.x_pack > 1 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : (p.tp == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                               : (p.tp == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B));
+    const bool okx = p.x_pack > 1
+        ? encode_2d(&tm[1], L.XT, 64, static_cast<uint64_t>(g.cols / p.x_pack), 128, 64, static_cast<uint32_t>(p.x_box),
+                    CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw)
+        : encode_2d(&tm[1], L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
+                    static_cast<uint32_t>(p.tp), static_cast<uint32_t>(p.x_box), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw);
+    // A_i2 [rows_p][ld_meta] u32, boxes [128 rows][32 words] (SW128; past n_ks: zero, never read); A_i1 as u32
+    // [rows_p / V][nb_pad], boxes [c_rows][32 words]
+    if (!okx || !encode_2d(&tm[0], L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
+                           static_cast<uint64_t>(g.ld_val) * 2, 64, kRowsU) ||
+        !encode_2d(&tm[2], L.P->meta, static_cast<uint64_t>(g.ld_meta), static_cast<uint64_t>(g.rows_p),
+                   static_cast<uint64_t>(g.ld_meta) * 4, 32, kRowsU, CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_2d(&tm[3], L.P->col_idx, static_cast<uint64_t>(g.nb_pad), static_cast<uint64_t>(g.rows_p / g.V),
+                   static_cast<uint64_t>(g.nb_pad) * 4, kBlkU, static_cast<uint32_t>(p.c_rows), CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                   CU_TENSOR_MAP_SWIZZLE_NONE))
         return kLaunchCudaError;
     const int vset = g.V >= 64 ? 1 : 64 / g.V;
     if (vset == 1) return launch_v<1>(L, q, a, tm, stream);

@@ -18,7 +18,8 @@ from dataclasses import dataclass
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvnm.so")
+# VNM_LIB: an alternative build of the same library (experiments, e.g. the -DVNM_ABLATIONS libvnm_abl.so)
+LIB_PATH = os.environ.get("VNM_LIB") or os.path.join(HERE, "libvnm.so")
 
 VNM_OK, VNM_ERR_ARG, VNM_ERR_SHAPE, VNM_ERR_ALIGN, VNM_ERR_UNSUPPORTED, VNM_ERR_CUDA = 0, -1, -2, -3, -4, -5
 VNM_F32, VNM_BF16 = 0, 1

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_spmm.py -m gpu -x -q --timeout 600 -k "smallt or slab or decode or workspace or pdl or chained or toy or token_tails" > gpurun_out/r02k_tests.log 2>&1; echo "tests exit $?"; tail -3 gpurun_out/r02k_tests.log
+VNM_SPMM_TRACE=2 timeout 120 python scripts/trace_spmm.py 11008 4096 5 16 > gpurun_out/r02k_trace.txt 2>&1; grep -A4 "call 3" gpurun_out/r02k_trace.txt | cut -c1-400
+for s in "11008 4096 5 16" "4096 11008 5 16" "4096 4096 5 16" "11008 4096 5 1" "11008 4096 5 32"; do
+  timeout 120 python scripts/time_spmm.py $s
+done
+C="python scripts/time_spmm.py 11008 4096 5 16"
+timeout 120 $C > /dev/null && timeout 600 ncu --set full --clock-control none --import-source on -k regex:vnm_spmm_smallt -s 25 -c 1 -o gpurun_out/r02k_prof_smallt_up $C > gpurun_out/r02k_ncu.log 2>&1; echo "ncu exit $?"

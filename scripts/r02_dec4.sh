@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_spmm.py -m gpu -x -q --timeout 600 -k "smallt or slab or decode or workspace or pdl or chained or toy or token_tails" > gpurun_out/r02e_tests.log 2>&1; echo "tests exit $?"; tail -5 gpurun_out/r02e_tests.log
+VNM_SPMM_TRACE=2 timeout 120 python scripts/trace_spmm.py 11008 4096 5 16 > gpurun_out/r02e_trace_up.txt 2>&1; echo "trace $?"
+grep -A3 "call 3" gpurun_out/r02e_trace_up.txt | cut -c1-300
+for s in "11008 4096 5 16" "4096 11008 5 16" "4096 4096 5 16" "11008 4096 5 1" "11008 4096 5 32"; do
+  timeout 120 python scripts/time_spmm.py $s
+done

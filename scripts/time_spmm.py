@@ -34,9 +34,18 @@ g1 = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g1):
     f()
 fl = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+rd = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+import time
+t_end = time.perf_counter() + 0.5  # clocks up under this load before measuring
+while time.perf_counter() < t_end:
+    g.replay()
+torch.cuda.synchronize()
+a.record(); g.replay(); b.record(); torch.cuda.synchronize()
+warm = a.elapsed_time(b) / 20 * 1e3
 ts = []
 for _ in range(10):
     fl.zero_()
+    rd.sum()
     a.record(); g1.replay(); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3)
 ts.sort()
