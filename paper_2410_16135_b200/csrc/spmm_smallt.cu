@@ -50,7 +50,8 @@ constexpr int kBlkU = 8 * kKS;     // 32 column blocks per unit
 constexpr int kCons = 8;           // consumer warps
 constexpr int kPhases = kCons / 2;
 constexpr int kProd = kCons;       // producer warp index
-constexpr int kThreads = 32 * (kCons + 1);
+constexpr int kFix = kCons + 1;    // fix-up warp: finishes every piece but the share's last, off the consumers' path
+constexpr int kThreads = 32 * (kCons + 2);
 constexpr uint32_t kABytes = kRowsU * 128;   // A_n box [128 rows][64 bf16], SW128
 constexpr uint32_t kTicketWords = 4096;      // fixed ticket region at the start of the workspace (16 KB)
 constexpr int kMBoxUnits = 8;                // units per A_i2 box: [128 rows][8 units x 4 words] = 128 B per row
@@ -130,6 +131,133 @@ __device__ __forceinline__ uint32_t xoff(int r, int n) {
     else return 64u * r + 16u * (n ^ ((r >> 1) & 3));
 }
 
+// Finish piece [pu0, pu1) of row group rp whose sum is in redb [128][TP] fp32: a whole row group goes straight to
+// Y^T; a row group cut between CTAs is published to the workspace and the LAST CTA to arrive adds the pieces in CTA
+// order (deterministic) — the CUTLASS semaphore pattern: the pieces' stores, a barrier, ONE acq_rel atomic by
+// thread 0 (release: cumulative over the group's stores through the barrier; acquire: the reads that follow the
+// next barrier).  t_early: the ticket read (acquire) when the share's last piece began, or ~0u (the fix-up warp's
+// pieces: straight to publishing).
+// Called by the 256 consumer threads (cons: named barrier 1) for the share's last piece, and by the fix-up warp
+// (__syncwarp) for the others.
+template <int TP, bool kBf16, int kNthr>
+__device__ __forceinline__ void finish_piece(const StArgs& a, int rp, int pu0, int pu1, float* redb, int tid,
+                                             uint32_t t_early, uint32_t& flag) {
+    auto sync = [&] {
+        if constexpr (kNthr == 32) __syncwarp();
+        else asm volatile("bar.sync 1, %0;" ::"n"(kNthr) : "memory");
+    };
+    constexpr int kN4 = kRowsU * TP / 4;  // float4 groups of a piece
+    const int row0 = rp * kRowsU;
+    float4* red4 = reinterpret_cast<float4*>(redb);
+    const bool whole = pu0 == rp * a.n_st && pu1 == (rp + 1) * a.n_st;
+    if (!whole) {
+        const int own0 = unit_owner(a, rp * a.n_st);
+        const int nseg = unit_owner(a, rp * a.n_st + a.n_st - 1) - own0 + 1;
+        const int me = static_cast<int>(blockIdx.x) - own0;
+        float* wsr = a.ws + static_cast<int64_t>(rp) * a.maxseg * kRowsU * TP;
+        // are all the other pieces in already (the ticket read when the piece began, else read once more now)?
+        // then this CTA is the last one and finishes without publishing its own piece; otherwise publish + count
+        if (tid == 0) {
+            uint32_t t = t_early;
+            if (t != ~0u && t != static_cast<uint32_t>(nseg - 1))
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(a.tickets + rp) : "memory");
+            flag = t == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
+        }
+        sync();
+        if (!flag) {
+            float4* mine = reinterpret_cast<float4*>(wsr + static_cast<int64_t>(me) * kRowsU * TP);
+            for (int i = tid; i < kN4; i += kNthr) __stcg(mine + i, red4[i]);
+            sync();
+            if (tid == 0) {
+                uint32_t old;
+                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.tickets + rp) : "memory");
+                flag = old == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
+            }
+            sync();
+            if (!flag) return;  // an other CTA finishes the row group
+        }
+        // the last one: every piece, in the canonical order p_0 + (p_1 + (... + p_{nseg-1})) (this CTA's own from
+        // shared memory)
+        constexpr int kU = kN4 / kNthr < 2 ? (kN4 / kNthr > 0 ? kN4 / kNthr : 1) : 2;
+        constexpr int kJ = 4;  // pieces whose loads are all issued before the fold (one round trip)
+        for (int i0 = tid; i0 < kN4; i0 += kNthr * kU) {
+            float4 sum[kU];
+            if (nseg <= kJ) {
+                float4 v[kJ][kU];
+#pragma unroll
+                for (int j = 0; j < kJ; ++j)
+#pragma unroll
+                    for (int k = 0; k < kU; ++k) {
+                        const int i = i0 + k * kNthr;
+                        if (j < nseg && i < kN4)
+                            v[j][k] = j == me ? red4[i]
+                                              : __ldcg(reinterpret_cast<const float4*>(wsr + static_cast<int64_t>(j) * kRowsU * TP) + i);
+                    }
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    sum[k] = v[kJ - 1][k];
+#pragma unroll
+                    for (int j = kJ - 1; j >= 0; --j) {
+                        if (j == nseg - 1) sum[k] = v[j][k];
+                        else if (j < nseg - 1)
+                            sum[k] = make_float4(v[j][k].x + sum[k].x, v[j][k].y + sum[k].y, v[j][k].z + sum[k].z,
+                                                 v[j][k].w + sum[k].w);
+                    }
+                }
+            } else {
+                for (int j = nseg - 1; j >= 0; --j) {
+                    const float4* src = reinterpret_cast<const float4*>(wsr + static_cast<int64_t>(j) * kRowsU * TP);
+#pragma unroll
+                    for (int k = 0; k < kU; ++k) {
+                        const int i = i0 + k * kNthr;
+                        if (i < kN4) {
+                            const float4 v = j == me ? red4[i] : __ldcg(src + i);
+                            sum[k] = j == nseg - 1 ? v : make_float4(v.x + sum[k].x, v.y + sum[k].y, v.z + sum[k].z, v.w + sum[k].w);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kU; ++k)
+                if (i0 + k * kNthr < kN4) red4[i0 + k * kNthr] = sum[k];
+        }
+        sync();
+        if (tid == 0) a.tickets[rp] = 0u;  // ready for the next launch (stream order)
+    }
+    // Y^T rows row0 .. +127, tokens [0, T): one 16-byte group (8 bf16 / 4 fp32 tokens) per thread and step
+    constexpr int kEl = kBf16 ? 8 : 4;
+    constexpr int kGroups = TP / kEl;
+    for (int i = tid; i < kRowsU * kGroups; i += kNthr) {
+        const int r = i / kGroups, t0 = (i % kGroups) * kEl;
+        const int grow = row0 + r;
+        if (grow >= a.rows || t0 >= a.T) continue;
+        const float* v = redb + r * TP + t0;
+        uint8_t* dst = static_cast<uint8_t*>(a.YT) + (static_cast<int64_t>(grow) * a.ldy + t0) * (kBf16 ? 2 : 4);
+        if (t0 + kEl <= a.T) {
+            uint32_t w[4];
+            if constexpr (kBf16) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+                    w[e] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(v[e]);
+            }
+            asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                         : "memory");
+        } else {
+            for (int e = 0; e < a.T - t0; ++e) {
+                if constexpr (kBf16)
+                    reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(v[e]);
+                else
+                    reinterpret_cast<float*>(dst)[e] = v[e];
+            }
+        }
+    }
+}
+
 // NT8: token tiles of 8 computed (T <= 8 NT8); VSET: V-blocks per 64-row half (64 / V for V <= 64, else 1)
 template <int NT8, int VSET, bool kBf16>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -139,15 +267,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int TP = NT8 == 1 ? 8 : (NT8 == 2 ? 16 : 32);  // tokens per X^T slice row in shared memory
     extern __shared__ __align__(1024) uint8_t smem[];
     // [A_i2 box ring: kMB x 16 KB][slot s: A_n 16 KB | X^T slice x_bytes | A_i1 c_rows x 128 B]
-    // [red [128][TP] fp32][barriers]
+    // [red: 2 x [128][TP] fp32 (piece sums, double-buffered)][barriers]
     uint8_t* mbox = smem;
     uint8_t* slots = smem + kMB * kMBoxBytes;
     float* red = reinterpret_cast<float*>(slots + a.S * a.slot_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(red + kRowsU * TP);
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kRowsU * TP);
     uint64_t* empty = full + a.S;
     uint64_t* mfull = empty + a.S;
     uint64_t* mempty = mfull + kMB;
-    uint32_t& last_flag = *reinterpret_cast<uint32_t*>(mempty + kMB);
+    uint64_t* pfull = mempty + kMB;   // [2] piece j's sum is in red[j % 2] (consumers -> fix-up warp)
+    uint64_t* pempty = pfull + 2;     // [2] red[j % 2] is free again (fix-up warp -> consumers)
+    uint32_t* flags = reinterpret_cast<uint32_t*>(pempty + 2);  // broadcast words: [0] consumers, [1] fix-up warp
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int u0 = share_begin(a, blockIdx.x), u1 = share_begin(a, blockIdx.x + 1);
@@ -162,6 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&mfull[k], 1);
             mbar_init(&mempty[k], kCons);  // every consumer warp releases every box once
         }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&pfull[k], 1);
+            mbar_init(&pempty[k], 1);
+        }
+
         fence_mbar_init();
     }
     if (warp == kProd && lane == 0) {
@@ -217,6 +352,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         return;
     }
 
+    if (warp == kFix) {
+        // ------------------------------------------------------------ fix-up warp: every piece but the last
+        int jp = 0;
+        for (int pu0 = u0; pu0 < u1; ++jp) {
+            const int rp = pu0 / a.n_st, pu1 = min(u1, (rp + 1) * a.n_st);
+            if (pu1 == u1) break;  // the share's last piece: the consumers finish it
+            mbar_wait(&pfull[jp & 1], (jp >> 1) & 1);
+            finish_piece<TP, kBf16, 32>(a, rp, pu0, pu1, red + (jp & 1) * (kRowsU * TP), lane, ~0u, flags[1]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pempty[jp & 1]);
+            pu0 = pu1;
+        }
+        return;
+    }
+
     // ---------------------------------------------------------------- consumers
     const int h = warp & 1, p = warp >> 1;
     const int g = lane >> 2, c = lane & 3;
@@ -235,9 +385,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
 
+    int jp = 0;  // piece index (the fix-up warp's numbering)
     for (int pu0 = u0; pu0 < u1;) {
         const int rp = pu0 / a.n_st;
         const int pu1 = min(u1, (rp + 1) * a.n_st);
+        // the share's last piece of a cut row group: read its ticket now (acquire); used when the piece is done
+        uint32_t t_early = ~0u;
+        if (pu1 == u1 && !(pu0 == rp * a.n_st && pu1 == (rp + 1) * a.n_st) && cons_tid == 0 && !a.rg_mode)
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t_early) : "l"(a.tickets + rp) : "memory");
+
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -336,7 +492,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         k_piece += (pu1 - pu0 + kMBoxUnits - 1) / kMBoxUnits;
         release_to(k_piece);  // the piece's boxes are done (also those this warp had no unit in)
-        // ---- end of the piece: phases 0..3 added in order through red[128][TP]
+        // ---- end of the piece: phases 0..3 added in order into red[j % 2]; every piece but the share's last goes
+        // to the fix-up warp (the consumers move on at once), the last one is finished here
+        const bool last_piece = pu1 == u1;
+        float* redb = red + (jp & 1) * (kRowsU * TP);
+        if (cons_tid == 0) mbar_wait(&pempty[jp & 1], ((jp >> 1) & 1) ^ 1);  // its use two pieces ago is done
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
 #pragma unroll 1
         for (int r = 0; r < kPhases; ++r) {
             if (p == r) {
@@ -346,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int n = 0; n < NT8; ++n)
 #pragma unroll
                         for (int k2 = 0; k2 < 2; ++k2) {
-                            float2* d = reinterpret_cast<float2*>(red + (64 * h + 16 * mt + g + 8 * k2) * TP + 8 * n + 2 * c);
+                            float2* d = reinterpret_cast<float2*>(redb + (64 * h + 16 * mt + g + 8 * k2) * TP + 8 * n + 2 * c);
                             float2 v = make_float2(acc[mt][n][2 * k2], acc[mt][n][2 * k2 + 1]);
                             if (r > 0) {
                                 const float2 o = *d;
@@ -358,101 +519,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
         }
-        const bool whole = pu0 == rp * a.n_st && pu1 == (rp + 1) * a.n_st;
-        const int row0 = rp * kRowsU;
-        // Y^T rows row0 .. +127, tokens [0, T): one 16-byte group (8 bf16 / 4 fp32 tokens) per thread and step
-        auto store_rows = [&](auto&& value) {
-            constexpr int kEl = kBf16 ? 8 : 4;
-            constexpr int kGroups = TP / kEl;  // groups per row
-            for (int i = cons_tid; i < kRowsU * kGroups; i += 32 * kCons) {
-                const int r = i / kGroups, t0 = (i % kGroups) * kEl;
-                const int grow = row0 + r;
-                if (grow >= a.rows || t0 >= a.T) continue;
-                float v[kEl];
-#pragma unroll
-                for (int e = 0; e < kEl; ++e) v[e] = value(r, t0 + e);
-                uint8_t* dst = static_cast<uint8_t*>(a.YT) + (static_cast<int64_t>(grow) * a.ldy + t0) * (kBf16 ? 2 : 4);
-                if (t0 + kEl <= a.T) {
-                    uint32_t w[4];
-                    if constexpr (kBf16) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-                            w[e] = *reinterpret_cast<uint32_t*>(&b2);
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(v[e]);
-                    }
-                    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-                                 "r"(w[3])
-                                 : "memory");
-                } else {
-                    for (int e = 0; e < a.T - t0; ++e) {
-                        if constexpr (kBf16)
-                            reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(v[e]);
-                        else
-                            reinterpret_cast<float*>(dst)[e] = v[e];
-                    }
-                }
-            }
-        };
-        if (whole) {
-            store_rows([&](int r, int t) { return red[r * TP + t]; });
+        if (!last_piece) {
+            if (cons_tid == 0) mbar_arrive(&pfull[jp & 1]);
         } else {
-            // a cut row group: publish this CTA's piece; the last CTA to arrive adds the pieces in CTA order.
-            // Ordering (the CUTLASS semaphore pattern): the pieces' stores, bar.sync, ONE acq_rel atomic by
-            // thread 0 (release: cumulative over the CTA's stores through the barrier; acquire: the last arriver's
-            // reads below, ordered after it by the next barrier).
-            const int own0 = unit_owner(a, rp * a.n_st);
-            const int nseg = unit_owner(a, rp * a.n_st + a.n_st - 1) - own0 + 1;
-            const int me = static_cast<int>(blockIdx.x) - own0;
-            float* wsr = a.ws + static_cast<int64_t>(rp) * a.maxseg * kRowsU * TP;
-            float4* red4 = reinterpret_cast<float4*>(red);
-            float4* mine = reinterpret_cast<float4*>(wsr + static_cast<int64_t>(me) * kRowsU * TP);
-            constexpr int kN4 = kRowsU * TP / 4;  // float4 groups per piece
-            for (int i = cons_tid; i < kN4; i += 32 * kCons) __stcg(mine + i, red4[i]);
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
-            if (cons_tid == 0) {
-                uint32_t old;
-                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.tickets + rp) : "memory");
-                last_flag = old == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
-            }
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
-            if (last_flag) {
-                // every piece of the row group, added in CTA order (j = 0 .. nseg-1; this CTA's own from shared
-                // memory): all loads of a group first, then the ordered sum
-                constexpr int kPer = (kN4 + 32 * kCons - 1) / (32 * kCons);
-                constexpr int kMaxSeg = 8;
-#pragma unroll
-                for (int k = 0; k < kPer; ++k) {
-                    const int i = cons_tid + k * 32 * kCons;
-                    if (i >= kN4) break;
-                    float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (int j0 = 0; j0 < nseg; j0 += kMaxSeg) {
-                        float4 v[kMaxSeg];
-#pragma unroll
-                        for (int j = 0; j < kMaxSeg; ++j)
-                            if (j0 + j < nseg)
-                                v[j] = j0 + j == me ? red4[i]
-                                                    : __ldcg(reinterpret_cast<const float4*>(wsr + static_cast<int64_t>(j0 + j) * kRowsU * TP) + i);
-#pragma unroll
-                        for (int j = 0; j < kMaxSeg; ++j)
-                            if (j0 + j < nseg) {
-                                acc4.x += v[j].x;
-                                acc4.y += v[j].y;
-                                acc4.z += v[j].z;
-                                acc4.w += v[j].w;
-                            }
-                    }
-                    red4[i] = acc4;
-                }
-                asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
-                store_rows([&](int r, int t) { return red[r * TP + t]; });
-                if (cons_tid == 0) a.tickets[rp] = 0u;  // ready for the next launch (stream order)
-            }
+            finish_piece<TP, kBf16, 32 * kCons>(a, rp, pu0, pu1, redb, cons_tid, t_early, flags[0]);
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");  // red is reused by the next piece
+        ++jp;
         pu0 = pu1;
     }
     if (tr) g_st_t[3][blockIdx.x] = gtime();
@@ -486,7 +558,8 @@ StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
     p.x_box_bytes = static_cast<uint32_t>(p.x_box) * row_bytes;
     p.x_bytes = (p.x_nbox * p.x_box_bytes + 1023) / 1024 * 1024;
     p.slot_bytes = (kABytes + p.x_bytes + p.c_rows * kCRow + 1023) / 1024 * 1024;
-    const size_t fixed = static_cast<size_t>(kMB) * kMBoxBytes + static_cast<size_t>(kRowsU) * p.tp * 4 + (2 * 16 + 2 * kMB) * 8 + 64;
+    const size_t fixed = static_cast<size_t>(kMB) * kMBoxBytes + 2 * static_cast<size_t>(kRowsU) * p.tp * 4 +
+                         (2 * 16 + 2 * kMB + 4) * 8 + 64;
     p.S = static_cast<int>((kMaxSmem - fixed) / p.slot_bytes);
     if (p.S > 16) p.S = 16;
     p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
