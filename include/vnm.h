@@ -9,7 +9,8 @@
  *
  * Conventions (all calls):
  *   - Every data pointer is a DEVICE pointer owned by the caller (e.g. a torch tensor); the library
- *     allocates no device memory and keeps no state besides a host-side cache of TMA descriptors.
+ *     allocates no device memory and keeps no device state (TMA descriptors are encoded on the host per call,
+ *     passed as kernel parameters).
  *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
  *   - Argument / shape / alignment errors are detected on the host and returned before any launch.
  *     Data-dependent errors (a mask that violates the V:N:M pattern) are written to `d_status`.
@@ -144,20 +145,25 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
  *   YT  [P->g.rows][ldy]  fp32 (y_dtype VNM_F32) or bf16 (VNM_BF16, round-to-nearest-even), 16-B aligned,
  *       ldy % 8 == 0, ldy >= T; only rows < g.rows and columns < T are written.
  * bf16 x bf16 products, fp32 accumulation on the sparse tensor cores (tcgen05.mma.sp).
- * Supported: V == 64 (any M), and any 32 <= V <= 128 (e.g. the paper's 128:2:M) when the
- * tensor-core form is present (M <= 8, or M % 4 == 0); VNM_ERR_UNSUPPORTED otherwise.
- * Plans: tensor-core form present and T > 64 (or V != 64) -> a window-form kernel (dense X^T tiles by TMA):
+ * Supported: 1 <= T <= 32 with V >= 16 and any M; V = 64, 128, 256 with any M at any T (e.g. the paper's 128:2:M,
+ * SURVEY §8(f) NEXT-1); 32 <= V <= 128 at any T when the tensor-core form is present (M <= 8, or M % 4 == 0);
+ * VNM_ERR_UNSUPPORTED otherwise.
+ * Plans: tensor-core form present and T > 64 (or V != 64 beyond the small-T range) -> a window-form kernel (dense
+ * X^T tiles by TMA; a Y^T row of T tokens that is not a multiple of 16 bytes takes the pair kernel whose stores are
+ * element-wise at the tail, so nothing past column T is ever written):
  * CTA pairs with the row pair's A resident for short K (tcgen05.mma.sp.cta_group::2, M = 256), CTA pairs
  * streaming A, or single CTAs (M = 128) — chosen by shape from measurements;
- * V = 64, T <= 32, M <= 8 -> small-T kernel (two V-blocks per
- * M = 128 sparse MMA, split-K); otherwise the gather kernel (M = 64 sparse MMAs on the 4 kept X^T rows of each
- * block, 16-byte cp.async gathers).
- * workspace: optional device scratch (16-B aligned) used by the small-T split-K plan; pass NULL/0 to
- * let the library choose a plan without it (vnm_spmm_workspace_bytes gives the size it can use).  Its
- * completion flags must be zero when a call starts: zero it once with vnm_spmm_workspace_init (or allocate
- * it zero-filled); every completed vnm_spmm call leaves it zeroed again, so one initialisation serves all
- * later calls ordered on the stream (no per-call memset).  Re-initialise after a failed launch; use one
- * workspace per concurrently running call.                                                            */
+ * 1 <= T <= 32, V >= 16, any M -> the small-T kernel (canonical A_n / A_i1 / A_i2 streamed by TMA, warp-level sparse
+ * MMAs whose B fragments are gathered from a dense X^T slice by ldmatrix, stream-K over (128-row group, 32-block
+ * stage) units); otherwise (V = 64) the gather kernel (M = 64 sparse MMAs on the 4 kept X^T rows of each block,
+ * 16-byte cp.async gathers).
+ * workspace: optional device scratch (16-B aligned) for the split-K plans; pass NULL/0 to let the library run
+ * without it (the small-T plan then gives every CTA whole row groups).  vnm_spmm_workspace_bytes(g, T) is the
+ * size a call can use.  Layout: a fixed 16 KB region of completion tickets at offset 0, fp32 partials after it.
+ * The tickets must be zero when a call starts: zero the workspace once with vnm_spmm_workspace_init (or allocate
+ * it zero-filled); every completed call leaves the tickets zero again (the partials are not cleared and need not
+ * be), so ONE workspace sized for the largest (g, T) serves all later calls of any geometry ordered on the stream
+ * (no per-call memset).  Re-initialise after a failed launch; use one workspace per concurrently running call. */
 vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed* P, void* YT, int64_t ldy,
                     vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
 

@@ -268,16 +268,15 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     // tensor-core form: 32 <= V <= 128 with M <= 8 (window form) or M % 4 == 0 (natural 2:4 form; the kernels
     // see its M = 4 view); small-T plan (T <= 32): any V >= 16, any M, canonical arrays; gather plan: V = 64
     const bool tc_form = P->values_tc && P->meta_tc && tc_geom(g);
-    static const int smallt_env = VNM_ENV_INT("VNM_SMALLT", 1);  // 0: the previous small-T plan (comparisons)
-    const bool small = smallt_env && vnm::spmm_smallt_applies(*g, T);
-    if (g->V != 64 && !tc_form && !small) return VNM_ERR_UNSUPPORTED;
+    const bool small = vnm::spmm_smallt_applies(*g, T);
+    if (g->V < 64 && !tc_form && !small) return VNM_ERR_UNSUPPORTED;  // gather plan: V = 64, 128, 256
     if (T == 0 || g->rows == 0) return VNM_OK;
     if (!YT) return VNM_ERR_ARG;
     if (g->cols > 0 && !XT) return VNM_ERR_ARG;
     if ((XT && !aligned16(XT)) || !aligned16(YT) || (ldx % 8) != 0 || (ldy % 8) != 0) return VNM_ERR_ALIGN;
     if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
     vnm::SpmmLaunch L{P, XT, ldx, T, YT, ldy, y_dtype, workspace, workspace ? workspace_bytes : 0};
-    const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || (!small && g->V != 64));
+    const bool tc = tc_form && g->nb_pad > 0 && (T > kTcMinTokens || (!small && g->V < 64));
     if (tc && (!aligned16(P->values_tc) || !aligned16(P->meta_tc))) return VNM_ERR_ALIGN;
     vnm_packed Pv;
     if (tc && nat24(g)) {  // the natural 2:4 form runs as the M = 4 layout over 4-channel groups
@@ -297,7 +296,16 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         // row tiles at large T (DeiT-S qkv / fc1: profiles/r01c_probes.md); slower for M = 8 and 3-row-tile
         // layers, where the single-CTA kernel stays.
         const int n_mma = g->nb_pad / (g->M == 4 ? 8 : 4);
-        const bool tc3 = force ? force >= 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192);
+        // The single-CTA / pair kernels store Y^T with TMA, whose stores are whole 16-byte chunks: a row of Y^T that
+        // is not a multiple of 16 bytes (T % 8 bf16 / T % 4 fp32) would get up to 7 tokens past T written.  Those
+        // shapes take the resident / streamed pair kernel (st.global with element-wise tails; tests/test_gpu_bounds.py).
+        const bool ragged = (static_cast<int64_t>(T) * (y_dtype == VNM_BF16 ? 2 : 4)) % 16 != 0;
+        const bool tc3 = ragged || (force ? force >= 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192));
+        if (ragged) {
+            const int rc = vnm::launch_spmm_tc3(L, -1, reinterpret_cast<cudaStream_t>(stream));
+            if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
+            return VNM_ERR_UNSUPPORTED;
+        }
         if (tc3) {  // VNM_TC_PLAN=4: the same kernel with A streamed
             const int rc = vnm::launch_spmm_tc3(L, force == 4 ? 0 : (force == 3 ? -1 : 1), reinterpret_cast<cudaStream_t>(stream));
             if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
@@ -307,7 +315,6 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
     }
     if (small) return from_launch(vnm::launch_spmm_smallt(L, reinterpret_cast<cudaStream_t>(stream)));
-    if (vnm::spmm_pair_applies(*g, T)) return from_launch(vnm::launch_spmm_pair(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -320,8 +327,7 @@ vnm_status vnm_spmm_workspace_init(void* ws, size_t bytes, vnm_stream_t stream) 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T) {
     if (check_geom(g) != VNM_OK || T < 0) return 0;
     // the largest workspace any plan for (g, T) can use (the tickets / flags sit at offset 0 in every plan)
-    size_t b = vnm::spmm_smallt_workspace_bytes(*g, T);
-    const size_t o = vnm::spmm_pair_applies(*g, T) ? vnm::spmm_pair_workspace_bytes(*g, T) : vnm::spmm_workspace_bytes(*g, T);
+    const size_t b = vnm::spmm_smallt_workspace_bytes(*g, T), o = vnm::spmm_workspace_bytes(*g, T);
     return b > o ? b : o;
 }
 

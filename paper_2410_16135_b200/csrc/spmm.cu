@@ -59,6 +59,7 @@ struct SpmmArgs {
     int32_t T;
     int32_t y_bf16;
     int32_t rows, M, nb_pad, ld_meta, nvb, ntt, ntiles;
+    int32_t vdiv;  // V / 64: 64-row tiles per V-block (they share the block's A_i1 row)
     // split-K (small T): unit u = (tile u / ks_n, K-slice u % ks_n of sps stages); partial sums go to
     // ws[k][row][t] (fp32) and a second kernel adds the ks_n slices in order (deterministic)
     int32_t ks_n, sps, nunits;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = blockIdx.x; u < a.nunits; u += gridDim.x) {
             const int tile = u / a.ks_n, k0 = (u % a.ks_n) * a.sps, k1 = min(k0 + a.sps, n_stage);
             const int vb = tile % a.nvb, n0 = (tile / a.nvb) * NT;
-            const uint32_t* ci_vb = reinterpret_cast<const uint32_t*>(a.col_idx) + static_cast<int64_t>(vb) * a.nb_pad;
+            const uint32_t* ci_vb = reinterpret_cast<const uint32_t*>(a.col_idx) + static_cast<int64_t>(vb / a.vdiv) * a.nb_pad;
             const int tt_tok = min(a.T - n0, NT);
             const int cu = (tt_tok + 7) / 8;                    // 16-byte chunks per row holding tokens < T
             const int lg = cu <= 1 ? 0 : 32 - __clz(cu - 1);  // log2(gsz)
@@ -451,7 +452,7 @@ int launch_reduce(const SpmmArgs& a, int T, cudaStream_t st) {
 }  // namespace
 
 size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T) {
-    if (g.V != kV || T <= 0 || T > 64 || g.nb_pad == 0) return 0;  // split-K serves the small-T (gather) plan
+    if (g.V < kV || T <= 0 || T > 64 || g.nb_pad == 0) return 0;  // split-K serves the small-T (gather) plan
     const int n_stage = (g.nb_pad / 8 + kMmaPerStage - 1) / kMmaPerStage;
     const int ks = choose_ksplit(g.rows_p / kV, n_stage);
     return ks > 1 ? static_cast<size_t>(ks) * g.rows * T * 4 : 0;
@@ -459,7 +460,9 @@ size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T) {
 
 int launch_spmm(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
-    if (g.V != kV) return kLaunchUnsupported;
+    // V = 64: one V-block per 64-row tile; V = 128 / 256 (e.g. the paper's 128:2:M for M that has no tensor-core
+    // form): 2 / 4 tiles share a V-block's column indices (each gathers them: correct, not faster)
+    if (g.V < kV || g.V % kV) return kLaunchUnsupported;
     if (g.nb_pad == 0) {  // K == 0: Y = 0
         const size_t es = L.y_dtype == VNM_BF16 ? 2 : 4;
         return cudaMemset2DAsync(L.YT, static_cast<size_t>(L.ldy) * es, 0, static_cast<size_t>(L.T) * es, g.rows,
@@ -492,6 +495,7 @@ int launch_spmm(const SpmmLaunch& L, cudaStream_t stream) {
     a.nb_pad = g.nb_pad;
     a.ld_meta = g.ld_meta;
     a.nvb = g.rows_p / kV;
+    a.vdiv = g.V / kV;
     a.ntt = 0;
     a.ntiles = 0;
     if (L.T > 128) return launch_nt<256>(L, ta, tm, a, stream);

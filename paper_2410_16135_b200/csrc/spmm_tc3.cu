@@ -66,7 +66,7 @@ struct Tc3Args {
                   // loads at all, 16 no A / metadata loads (streaming), 32 no X^T loads
 };
 
-__device__ unsigned long long g_tc3_t[8][160];
+__device__ unsigned long long g_tc3_t[9][160];
 
 // tile i of this pair; false past the end.  Resident A: every pair owns one row pair and the row pair's token
 // tiles are dealt round-robin over its pairs.  Streaming: tiles row-pair-major over all pairs (consecutive
@@ -219,7 +219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t idesc1 = idesc_bf16(256, NT, true, 1, true);
             const uint64_t b_step = (a.M == 4 ? 32u : 4u * a.M) * 128u >> 4;  // B descriptor advance per MMA
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
-            unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
+            unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0, c_full0 = 0;
             for (; tile3(a, cid, tl, rp, tt); ++tl) {
                 if (a.a_res && tl == 0) {  // resident metadata -> TMEM columns kMetaCol + 4c (both CTAs)
                     mbar_wait(res_full, 0);
@@ -239,6 +239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(&full[s], (q / S) & 1);
                     if (a.peek && st + 1 < a.n_st) mbar_wait(&full[(q + 1) % S], ((q + 1) / S) & 1);  // overhang
                     c_full += clock64() - c0;
+                    if (st == 0) c_full0 += clock64() - c0;
                     tc_fence_after();
                     const int mi0 = st * a.ms;
                     const int left = a.n_mma - mi0;
@@ -265,6 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 g_tc3_t[1][blockIdx.x] = c_emp;
                 g_tc3_t[2][blockIdx.x] = clock64() - c_all;
                 g_tc3_t[7][blockIdx.x] = tl;
+                g_tc3_t[8][blockIdx.x] = c_full0;
             }
         }
     } else if (warp >= 4) {
@@ -468,14 +470,15 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && a.trace) {
-        static unsigned long long h[8][160];
+        static unsigned long long h[9][160];
         cudaStreamSynchronize(stream);
         cudaMemcpyFromSymbol(h, g_tc3_t, sizeof(h));
         fprintf(stderr, "tc3 NT=%d: grid %d a_res %d S %d ms %d n_st %d n_mma %d smem %zu\n", NT, 2 * pairs, a.a_res,
                 a.S, a.ms, a.n_st, a.n_mma, smem);
         for (int i = 0; i < 2 * pairs; i += 10)
-            fprintf(stderr, "  cta %3d tiles %llu | mma: wait_full %7llu wait_empty %7llu total %8llu | prod wait %8llu | "
-                            "epi wait %8llu busy %8llu\n", i, h[7][i], h[0][i], h[1][i], h[2][i], h[3][i], h[4][i], h[5][i]);
+            fprintf(stderr, "  cta %3d tiles %llu | mma: wait_full %7llu (stage 0: %7llu) wait_empty %7llu total %8llu | "
+                            "prod wait %8llu | epi wait %8llu busy %8llu\n", i, h[7][i], h[0][i], h[8][i], h[1][i], h[2][i],
+                    h[3][i], h[4][i], h[5][i]);
     }
     return e == cudaSuccess ? 0 : kLaunchCudaError;
 }

@@ -71,10 +71,6 @@ size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 bool spmm_smallt_applies(const vnm_geom& g, int32_t T);
 size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T);
 int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream);
-// previous small-T plan (spmm_pair.cu, VNM_SMALLT=0): T <= 32, V = 64, M <= 8
-bool spmm_pair_applies(const vnm_geom& g, int32_t T);
-size_t spmm_pair_workspace_bytes(const vnm_geom& g, int32_t T);
-int launch_spmm_pair(const SpmmLaunch& L, cudaStream_t stream);
 
 // RIA importance (ria.cu)
 size_t ria_workspace_bytes(int32_t rows, int32_t cols);

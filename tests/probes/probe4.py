@@ -27,3 +27,17 @@ for cg in (1, 2):
                 print(r, flush=True)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(res, open(os.path.join(ROOT, "gpurun_out", "probe4_mma.json"), "w"), indent=1)
+
+# ---- the tc3 stage pattern (4 MMAs + commit per stage, window SBO, ring of B slots)
+L.vnm_probe_bench_stage_pair.argtypes = [ctypes.c_uint32] * 6 + [ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+pairs = sms // 2
+res2 = []
+for n, sbo, step, rows, ring, commit in [(224, 640, 2560, 80, 6, 4), (224, 640, 2560, 80, 6, 5)]:
+    cyc = torch.zeros(pairs, dtype=torch.int64, device="cuda")
+    st = L.vnm_probe_bench_stage_pair(n, sbo, step, rows, ring, 2000, commit, pairs, cyc.data_ptr())
+    c = cyc.float() / (2000 * 4)
+    r = dict(n=n, sbo=sbo, b_step=step, stage_rows=rows, ring=ring, commit=commit, status=st,
+             cyc_per_mma_med=round(float(c.median()), 1), cyc_per_mma_max=round(float(c.max()), 1))
+    res2.append(r)
+    print(r, flush=True)
+json.dump(res + res2, open(os.path.join(ROOT, "gpurun_out", "probe4_mma.json"), "w"), indent=1)

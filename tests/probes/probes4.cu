@@ -220,3 +220,121 @@ extern "C" int vnm_probe_stream_units(const uint16_t* A, int32_t rows, int32_t c
     *ns = h[1] - h[0];
     return 0;
 }
+
+// ---- the window-form pair kernel's MMA issue pattern (spmm_tc3.cu), operands resident: per "stage" one
+// mma_sp_stage<2> (4 sparse MMAs, B K-group stride sbo, B advanced by b_step per MMA, metadata column pair e / e+2)
+// and a tcgen05.commit (multicast to both CTAs) on a per-slot mbarrier, slots cycling through `ring` B regions
+// (start offsets stage_rows * 128 B apart, not 1024-aligned when stage_rows % 8 != 0); no waits on the commits.
+namespace vnm {
+namespace {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    bench_stage_pair_kernel(uint32_t n, uint32_t sbo, uint32_t b_step, uint32_t stage_rows, uint32_t ring,
+                            uint32_t stages, int commit, unsigned long long* cycles) {
+    // commit == 2: the tc3 producer / MMA handshake: a producer thread waits empty[s] and arrives on full[s] (no
+    // loads), the MMA warp waits full[s] before each stage and commits to empty[s] (both CTAs)
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar[8], fullb[8], tfull[2], tempty[2];
+    __shared__ __align__(8) uint64_t done;
+    __shared__ uint32_t tmem_base;
+    const uint32_t tid = threadIdx.x, warp = tid / 32;
+    const uint32_t rank = cluster_ctarank();
+    for (uint32_t i = tid; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    fence_proxy_async_smem();
+    if (tid == 0) {
+        for (int i = 0; i < 8; ++i) {
+            mbar_init(&bar[i], 1);
+            mbar_init(&fullb[i], 1);
+        }
+        mbar_init(&done, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 2 * 8);  // 8 "epilogue" warps x 2 CTAs
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_pair(&tmem_base, 512);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tb = tmem_base;
+    if (warp < 4) {
+        for (int c = 480; c < 512; c += 4)
+            tmem_st_32x32b_x4(tb + ((warp * 32) << 16) + c, 0x44444444u, 0x44444444u, 0x44444444u, 0x44444444u);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    if (warp == 1 && rank == 0) {
+        const uint32_t idesc0 = idesc_bf16(256, n, true, 0, true), idesc1 = idesc_bf16(256, n, true, 1, true);
+        const uint64_t a0 = sdesc(smem_u32(smem), 16, 1024, kLayoutSW128);
+        const unsigned long long t0 = clock64();
+        for (uint32_t q = 0; q < stages; ++q) {
+            const uint32_t s = q % ring;
+            if (commit >= 4 && q % 5 == 0) {  // tile start: its accumulator is free (two tiles ago drained)
+                const uint32_t tl = q / 5;
+                mbar_wait(&tempty[tl & 1], ((tl >> 1) & 1) ^ 1);
+                tc_fence_after();
+            }
+            if (commit >= 2) {
+                mbar_wait(&fullb[s], (q / ring) & 1);
+                if (commit == 5 && q % 5 != 4) mbar_wait(&fullb[(q + 1) % ring], ((q + 1) / ring) & 1);  // tc3's peek
+                tc_fence_after();
+            }
+            const uint64_t bd = sdesc(smem_u32(smem + 81920 + s * stage_rows * 128), 16384, sbo, kLayoutSW128);
+            const uint64_t ad = a0 + ((q % 5) * 16384 >> 4);
+            mma_sp_stage<2>(tb + (q / 5 % 2) * 224 * (n <= 224), ad, bd, b_step >> 4, tb + 480 + 4 * (q % 5), idesc0, idesc1,
+                            q % 5 ? 1u : 0u, 4);
+            if (commit) mma_commit_pair_elect(&bar[s], 0x3);
+            if (commit >= 4 && q % 5 == 4) mma_commit_pair_elect(&tfull[(q / 5) & 1], 0x3);
+        }
+        mma_commit_pair_elect(&done, 0x3);
+        if ((threadIdx.x & 31) == 0) mbar_wait(&done, 0);
+        __syncwarp();
+        const unsigned long long t1 = clock64();
+        if (tid == 32) cycles[blockIdx.x / 2] = t1 - t0;
+    } else if (warp >= 2 && commit >= 4) {
+        // commit == 4: 8 "epilogue" warps per CTA take every tile's accumulator (tmem_full) and release it at once
+        for (uint32_t tl = 0; tl < stages / 5; ++tl) {
+            mbar_wait(&tfull[tl & 1], (tl >> 1) & 1);
+            tc_fence_before();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                if (rank == 0) mbar_arrive(&tempty[tl & 1]);
+                else mbar_arrive_remote(&tempty[tl & 1], 0);
+            }
+        }
+    } else if (warp >= 2 && commit >= 3) {
+        // commit == 3: 8 extra warps spin-wait (mbarrier try_wait loop) on a barrier that completes only at the end,
+        // like the window kernels' epilogue warps waiting for an accumulator
+        mbar_wait(&done, 0);
+    } else if (warp == 0 && commit >= 2 && (threadIdx.x & 31) == 0 && rank == 0) {
+        if (commit == 6) {  // a short stall before each arrival (the producer's TMA issue)
+        }
+        for (uint32_t q = 0; q < stages; ++q) {
+            const uint32_t s = q % ring;
+            mbar_wait(&bar[s], ((q / ring) & 1) ^ 1);
+            mbar_arrive(&fullb[s]);
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_pair(tb, 512);
+    }
+}
+}  // namespace
+}  // namespace vnm
+
+extern "C" int vnm_probe_bench_stage_pair(uint32_t n, uint32_t sbo, uint32_t b_step, uint32_t stage_rows, uint32_t ring,
+                                          uint32_t stages, int commit, int pairs, unsigned long long* cycles) {
+    using namespace vnm;
+    const size_t smem = 200 * 1024;
+    if (cudaFuncSetAttribute(bench_stage_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return 2;
+    bench_stage_pair_kernel<<<2 * pairs, commit >= 3 ? 320 : 128, smem>>>(n, sbo, b_step, stage_rows, ring, stages, commit, cycles);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}

@@ -219,12 +219,23 @@ def test_window_plan_any_v(V, rows, cols, T, M):
     assert_within(gpu_y(W, XT, V, M, T, tc=True), Yref, Aref)
 
 
-def test_v128_without_window_form_is_unsupported():
+def test_v32_without_window_form_is_unsupported():
+    """V = 32 past the small-T range needs the tensor-core form (the gather plan tiles 64-row V-blocks)."""
     W = synth.weights(256, 256, seed=3)
-    P = vnm.prune_compress(to_dev_bf16(W), 128, 5)
+    P = vnm.prune_compress(to_dev_bf16(W), 32, 5)
     with pytest.raises(RuntimeError):
         vnm.spmm(to_dev_bf16(synth.activations_t(256, 128, seed=4)), P, T=128)
 
+
+@pytest.mark.parametrize("V,M", [(128, 9), (128, 10), (128, 11), (128, 13), (128, 5), (256, 7)])
+@pytest.mark.parametrize("rows,cols,T", [(384, 1500, 100), (300, 777, 257)])
+def test_gather_plan_v128_any_m(V, M, rows, cols, T):
+    """NEXT-1: the paper's 128:2:9 / 10 / 11 / 13 points (tab:bs-sped), which have no tensor-core form,
+    at prefill-sized T through the gather plan (64-row tiles sharing their V-block's A_i1 row); V = 256 too."""
+    W, XT, Wm = make(rows, cols, V, M, T, seed=V + M + rows + T, wkind="outlier")
+    Yref, Aref = oracle.gemm_ref(XT, Wm)
+    assert_within(gpu_y(W, XT, V, M, T), Yref, Aref)
+    assert_within(gpu_y(W, XT, V, M, T, out_dtype=torch.bfloat16), Yref, Aref, bf16=True)
 
 
 def test_pair_resident_kernel_forced():
@@ -396,30 +407,6 @@ def test_workspace_reused_across_shapes():
 def ctypes_ptr(t):
     import ctypes
     return ctypes.c_void_p(t.data_ptr())
-
-
-def test_previous_small_t_plan_forced():
-    """The previous small-T plan (spmm_pair.cu, tcgen05 with two V-blocks per M = 128 MMA), forced with
-    VNM_SMALLT=0 in a child process, on the shapes it accepts (V = 64, M <= 8, T <= 32)."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, oracle\n"
-        "from paper_2410_16135_b200 import synth, vnm\n"
-        "from tests.gpu_util import to_dev_bf16\n"
-        "for rows, cols, M, T in [(256, 1000, 5, 1), (192, 333, 8, 16), (4096, 4096, 5, 8), (128, 64, 7, 13)]:\n"
-        "    W = synth.weights(rows, cols, seed=rows + T); XT = synth.activations_t(cols, T, seed=cols + T)\n"
-        "    mask = oracle.prune(W, 64, M)\n"
-        "    Yref, Aref = oracle.gemm_ref(XT, oracle.apply_mask(W, mask, 64, M))\n"
-        "    P = vnm.prune_compress(to_dev_bf16(W), 64, M)\n"
-        "    Y = vnm.spmm(to_dev_bf16(XT), P, T=T).cpu().numpy().astype(np.float64)\n"
-        "    assert np.all(np.abs(Y - Yref) <= oracle.tolerance(Yref, Aref)), (rows, cols, M, T)\n"
-        "print('ok')\n")
-    env = dict(os.environ, VNM_SMALLT="0")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 def test_pdl_wait_orders_reads_after_a_delayed_producer():
