@@ -41,7 +41,11 @@ namespace {
 constexpr uint32_t kABytes = 128 * 128;  // one 4-MMA chunk of A: 128 rows x 64 bf16 (SW128)
 constexpr uint32_t kEBytes = 128 * 16;   // one 4-MMA chunk of metadata: 128 lanes x 4 words
 constexpr uint32_t kYSlot = 32 * 64;     // epilogue transpose slot: 32 rows x 64 B (half a 128-byte row chunk)
-constexpr int kEpi = 8;                  // epilogue warps
+#ifndef VNM_TC3_EPI
+#define VNM_TC3_EPI 8
+#endif
+constexpr int kEpi = VNM_TC3_EPI;        // epilogue warps (a multiple of 4: kEpi / 4 per TMEM lane quadrant)
+constexpr int kEq = kEpi / 4;
 constexpr int kThreads = 128 + 32 * kEpi;  // warps 0 + 2 TMA, 1 MMA, 3 idle, 4.. epilogue
 
 struct Tc3Args {
@@ -56,7 +60,10 @@ struct Tc3Args {
     int32_t a_res;       // 1: A + metadata resident; 0: streamed per stage
     int32_t rp_per;      // resident: pairs per row pair;  streaming: total pairs
     int32_t peek;        // windows cross stage boundaries (5 <= M <= 7: an 8-channel window is wider than a block)
-    uint32_t ring_rows;  // S * rows_stage + 8 (shadow): rows per token-chunk region
+    int32_t ovh;         // 1: every slot also holds the next stage's first 8 rows (loaded twice; no cross-stage
+                         // wait, no shadow); 0: K-ring with the MMA waiting for the next stage too
+    int32_t slot_rows;   // rows per slot: rows_stage (+ 8 with ovh and peek)
+    uint32_t ring_rows;  // S * slot_rows (+ 8 shadow rows without ovh): rows per token-chunk region
     uint32_t stage_tx, shadow_tx;  // expect_tx bytes for both CTAs (X^T; + A / metadata when streaming)
     void* Y;
     int64_t ldy;
@@ -95,7 +102,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr uint32_t kMetaCol = kNacc * NT;      // metadata columns after the accumulators
     constexpr int kCw = kBf16 ? 64 : 32;           // tokens per 128-byte row of a transpose slot
     constexpr int kNch = (NT + kCw - 1) / kCw;     // epilogue chunks per tile
-    constexpr int kCpw = (kNch + 1) / 2;           // chunks per epilogue warp (2 warps per lane quadrant)
+    constexpr int kCpw = (kNch + kEq - 1) / kEq;   // chunks per epilogue warp (kEq warps per lane quadrant)
     static_assert(kW1 > 0 && kW1 <= 64 && kW1 % 16 == 0, "token split");
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = a.S;
@@ -187,7 +194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     // (box 1's bytes may land before box 0's thread registers the stage's expect_tx: the
                     // phase still needs that arrival, and the transaction count is signed)
                     if (pb == 0) {
-                        uint32_t tx = a.stage_tx + (s == 0 ? a.shadow_tx : 0u);
+                        uint32_t tx = a.stage_tx + (s == 0 && !a.ovh ? a.shadow_tx : 0u);
                         if (a.abl & 16) tx -= 2u * (kABytes + kEBytes);                  // ablation: no A / E loads
                         if (a.abl & 32) tx = a.a_res ? 0u : 2u * (kABytes + kEBytes);    // ablation: no X^T loads
                         if (leader) {
@@ -201,9 +208,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     if (a.abl & 32) continue;
                     const int y = st * a.rows_stage;
-                    uint8_t* dst = ring + static_cast<uint32_t>(s * a.rows_stage) * 128u + pb * region;
+                    uint8_t* dst = ring + static_cast<uint32_t>(s * a.slot_rows) * 128u + pb * region;
                     tma_load_2d_pair(dst, pb ? &tmap_b1 : &tmap_b0, x0 + 64 * pb, y, &full[s]);
-                    if (s == 0 && a.peek) {  // the shadow after the last slot: a copy of slot 0's first 8 rows
+                    if (s == 0 && a.peek && !a.ovh) {  // the shadow after the last slot: a copy of slot 0's first 8 rows
                         uint8_t* sh = ring + static_cast<uint32_t>(S * a.rows_stage) * 128u + pb * region;
                         tma_load_2d_pair(sh, pb ? &tmap_s1 : &tmap_s0, x0 + 64 * pb, y, &full[s]);
                     }
@@ -237,7 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int s = q % S;
                     c0 = clock64();
                     mbar_wait(&full[s], (q / S) & 1);
-                    if (a.peek && st + 1 < a.n_st) mbar_wait(&full[(q + 1) % S], ((q + 1) / S) & 1);  // overhang
+                    if (a.peek && !a.ovh && st + 1 < a.n_st) mbar_wait(&full[(q + 1) % S], ((q + 1) / S) & 1);  // overhang
                     c_full += clock64() - c0;
                     if (st == 0) c_full0 += clock64() - c0;
                     tc_fence_after();
@@ -245,7 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int left = a.n_mma - mi0;
                     const uint32_t n = static_cast<uint32_t>(left < a.ms ? left : a.ms);
                     const uint64_t bd =
-                        sdesc(smem_u32(ring + static_cast<uint32_t>(s * a.rows_stage) * 128u), region, sbo, kLayoutSW128);
+                        sdesc(smem_u32(ring + static_cast<uint32_t>(s * a.slot_rows) * 128u), region, sbo, kLayoutSW128);
                     uint64_t ad;
                     uint32_t e;
                     if (a.a_res) {
@@ -370,15 +377,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 uint32_t w[kCpw][32];
 #pragma unroll
                 for (int j = 0; j < kCpw; ++j)
-                    if (half + 2 * j < kNch) drain(taddr, half + 2 * j, w[j]);
+                    if (half + kEq * j < kNch) drain(taddr, half + kEq * j, w[j]);
                 release(acc);
 #pragma unroll
                 for (int j = 0; j < kCpw; ++j)
-                    if (half + 2 * j < kNch) store(rt, half + 2 * j, w[j]);
+                    if (half + kEq * j < kNch) store(rt, half + kEq * j, w[j]);
             } else {
-                const int last = ((kNch - 1 - half) / 2) * 2 + half;  // this warp's last chunk
+                const int last = half < kNch ? ((kNch - 1 - half) / kEq) * kEq + half : -1;  // this warp's last chunk
+                if (last < 0) release(acc);  // no chunk for this warp in this tile
 #pragma unroll 1
-                for (int c = half; c < kNch; c += 2) {
+                for (int c = half; c < kNch; c += kEq) {
                     uint32_t w[32];
                     drain(taddr, c, w);
                     if (c == last) release(acc);
@@ -412,7 +420,7 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     const bool alias = a.n_chunk * kEBytes <= kEpi * kYSlot;  // resident metadata staged in the epilogue slots
     const uint32_t res = static_cast<uint32_t>(a.n_chunk) * kABytes + (alias ? 0u : ebytes(a.n_chunk));
     a.a_res = want_res != 0 && pairs_all >= a.n_rp && kNacc * NT + 4 * a.n_chunk <= 512 &&
-              res + 2u * (4 * a.rows_stage + 8) * 128u + fixed <= kMaxSmem;
+              res + 2u * (4 * a.slot_rows + 8) * 128u + fixed <= kMaxSmem;
     if (want_res == 1 && !a.a_res) return kLaunchUnsupported;
     if (!a.a_res && a.ms != 4) return kLaunchUnsupported;  // streamed A arrives in 4-MMA chunks
     // ring slots: as many as fit (bytes in flight hide the load latency), at least 3
@@ -420,13 +428,13 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     for (int s = 8; s >= 3 && !S; --s) {
         const uint32_t ab = a.a_res ? res : static_cast<uint32_t>(s) * kABytes + ebytes(s);
         const bool tmem_ok = kNacc * NT + 4 * (a.a_res ? a.n_chunk : s) <= 512;
-        if (tmem_ok && ab + 2u * (s * a.rows_stage + 8) * 128u + fixed <= kMaxSmem) S = s;
+        if (tmem_ok && ab + 2u * (s * a.slot_rows + 8) * 128u + fixed <= kMaxSmem) S = s;
     }
     if (!S) return kLaunchUnsupported;
     if (const int v = VNM_ENV_INT("VNM_TC3_S", 0); v >= 3 && v < S) S = v;
     a.S = S;
-    a.ring_rows = static_cast<uint32_t>(S * a.rows_stage + 8);
-    a.stage_tx = 2u * a.rows_stage * (64 + kW1) * 2u + (a.a_res ? 0u : 2u * (kABytes + kEBytes));
+    a.ring_rows = static_cast<uint32_t>(S * a.slot_rows + (a.ovh ? 0 : 8));
+    a.stage_tx = 2u * a.slot_rows * (64 + kW1) * 2u + (a.a_res ? 0u : 2u * (kABytes + kEBytes));
     a.shadow_tx = a.peek ? 2u * 8u * (64 + kW1) * 2u : 0u;
     int pairs;
     if (a.a_res) {  // every pair owns one row pair; the token tiles of a row pair are dealt round-robin
@@ -448,9 +456,9 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
         return kLaunchCudaError;
     const uint64_t xr = static_cast<uint64_t>(L.ldx) * 2;
     if (!encode_2d(&tb0, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), xr, 64,
-                   static_cast<uint32_t>(a.rows_stage)) ||
+                   static_cast<uint32_t>(a.slot_rows)) ||
         !encode_2d(&tb1, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), xr, kW1,
-                   static_cast<uint32_t>(a.rows_stage)) ||
+                   static_cast<uint32_t>(a.slot_rows)) ||
         !encode_2d(&ts0, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), xr, 64, 8) ||
         !encode_2d(&ts1, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), xr, kW1, 8))
         return kLaunchCudaError;
@@ -498,23 +506,30 @@ int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream) {
     a.n_rt = (g.rows_p + 127) / 128;
     a.n_rp = (a.n_rt + 1) / 2;
     a.peek = g.M >= 5 && g.M <= 7;
+    a.ovh = VNM_ENV_INT("VNM_TC3_OVH", 1) ? 1 : 0;
     const int res = mode < 0 ? 1 : mode;
     // resident A: 4 MMAs per stage (16 blocks), 2 when a 4-MMA stage would be large (M >= 7: >= 112 rows)
     a.ms = g.M >= 7 && res ? 2 : 4;
     if (const int v = VNM_ENV_INT("VNM_TC3_MS", 0)) a.ms = v == 2 ? 2 : 4;
     a.n_st = (a.n_mma + a.ms - 1) / a.ms;
     a.rows_stage = a.ms * (g.M == 4 ? 32 : 4 * g.M);
+    a.slot_rows = a.rows_stage + (a.ovh && a.peek ? 8 : 0);
     // NT = 256 (one accumulator) when T is a multiple of 256 and A streams (long K: the per-tile hand-off is
     // amortised), else NT = 224 (two accumulators)
     int nt = (mode == 0 && L.T % 256 == 0) ? 256 : 224;
     if (const int v = VNM_ENV_INT("VNM_TC3_NT", 0)) nt = v;
     const int want = mode < 0 ? -1 : res;
-    int rc = nt == 256 ? launch_nt3<256>(L, a, want, stream) : launch_nt3<224>(L, a, want, stream);
+    auto launch = [&](int w) {
+        return nt == 256 ? launch_nt3<256>(L, a, w, stream) : nt == 192 ? launch_nt3<192>(L, a, w, stream)
+                                                                    : launch_nt3<224>(L, a, w, stream);
+    };
+    int rc = launch(want);
     if (rc == kLaunchUnsupported && mode < 0 && a.ms != 4) {  // resident did not fit: stream, 4-MMA stages
         a.ms = 4;
         a.n_st = (a.n_mma + 3) / 4;
         a.rows_stage = 4 * (g.M == 4 ? 32 : 4 * g.M);
-        rc = nt == 256 ? launch_nt3<256>(L, a, 0, stream) : launch_nt3<224>(L, a, 0, stream);
+        a.slot_rows = a.rows_stage + (a.ovh && a.peek ? 8 : 0);
+        rc = launch(0);
     }
     return rc;
 }
