@@ -69,6 +69,7 @@ def lib():
             L.vnmo_act_norms.argtypes = [P, i64, i32, i32, P]
             L.vnmo_ria.argtypes = [P, i64, i32, i32, P, ctypes.c_double, P, i64, P]
             L.vnmo_permute_gain.argtypes = [P, i64, i32, i32, i32, i32, P]
+            L.vnmo_permute_gain_out.argtypes = [P, i64, i32, i32, i32, i32, P]
             _lib = L
     return _lib
 
@@ -251,4 +252,19 @@ def permute_gain(score: np.ndarray, V: int, M: int) -> np.ndarray:
     st = lib().vnmo_permute_gain(_p(score), cols, rows, cols, V, M, _p(cost))
     if st:
         raise ValueError(f"vnmo_permute_gain status {st}")
+    return cost
+
+
+def permute_gain_out(score: np.ndarray, V: int, M: int) -> np.ndarray:
+    """LSA cost of the OUTPUT-channel permutation step (Eq. 8 `eq:admm2`, P:211-213; P:198; SURVEY NEXT-3;
+    DESIGN.md Q23): cost[i][g*V + s] = retained score row i contributes in slot s of V-row stripe g (other rows
+    frozen, the stripe re-pruned by S_{V:N:M}).  score fp32 [rows][cols]; returns fp64 [rows_p][rows_p]."""
+    score = np.ascontiguousarray(score, dtype=np.float32)
+    rows, cols = score.shape
+    g = geometry(rows, cols, V, M)
+    R = g["rows_p"]
+    cost = np.zeros((R, R), np.float64)
+    st = lib().vnmo_permute_gain_out(_p(score), cols, rows, cols, V, M, _p(cost))
+    if st:
+        raise ValueError(f"vnmo_permute_gain_out status {st}")
     return cost

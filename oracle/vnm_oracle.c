@@ -474,3 +474,64 @@ int vnmo_permute_gain(const float* score, int64_t lds, int32_t rows, int32_t col
     free(E);
     return VNMO_OK;
 }
+
+/* ------------------------------------------------------------------------------------------------------------
+ * Output-channel permutation gain (Eq. (8) `eq:admm2`, §4.2: P_o^{k+1} =
+ * argmax_{P_o} sum RIA(S_{V:N:M}(P_o W P_i^k)), "approximately modeled as the traditional linear sum assignment
+ * problem"; "V:N:M sparsity allows both input and output CP to affect the retained norm";
+ * SPEC solve_output_perm S:382-389; reading Q23).
+ *
+ * cost[i][g*V + s] = the retained score that ROW i contributes when it replaces the occupant of slot s of V-row
+ * stripe g (every other row frozen) and the stripe is re-pruned by S_{V:N:M}: in every column block b the stripe's
+ * 4 columns of largest L1 (fp32, the canonical stride-halving tree over the stripe's V rows with row i at position
+ * s; ties -> smaller column) are kept, then row i keeps the 2 largest e among them (ties -> smaller position);
+ * the contribution is the sum over blocks (ascending) of those 2 kept e (ascending column) in fp64.  With every
+ * row in its own slot the costs add up to the retained score of the actual pruning.
+ * score fp32 [rows][lds] (e = |score|, zero-padded to rows_p x cols_p); cost fp64 [rows_p][rows_p].
+ * ------------------------------------------------------------------------------------------------------------ */
+int vnmo_permute_gain_out(const float* score, int64_t lds, int32_t rows, int32_t cols, int32_t V, int32_t M,
+                          double* cost) {
+    vnmo_geom g;
+    int st = vnmo_geometry(rows, cols, V, M, &g);
+    if (st) return st;
+    if (!score || !cost || M > 64) return VNMO_ERR_ARG;
+    float* E = importance_padded(NULL, 0, score, lds, &g);
+    if (!E) return VNMO_ERR_ARG;
+    const int32_t K = g.cols_p, R = g.rows_p;
+    int32_t P = 1;
+    while (P < V) P <<= 1;
+#pragma omp parallel for schedule(dynamic)
+    for (int32_t i = 0; i < R; ++i) {
+        float* s = (float*)malloc(sizeof(float) * (size_t)P);
+        float* blk = (float*)malloc(sizeof(float) * (size_t)V * (size_t)M);  /* the hypothetical stripe block [V][M] */
+        float L[64];
+        for (int32_t gs = 0; gs < R; ++gs) {
+            const int32_t vb = gs / V, sl = gs % V;
+            double acc = 0.0;
+            for (int32_t b = 0; b < g.nb; ++b) {
+                for (int32_t r = 0; r < V; ++r)
+                    for (int32_t c = 0; c < M; ++c)
+                        blk[r * M + c] = E[(int64_t)(r == sl ? i : vb * V + r) * K + (int64_t)b * M + c];
+                for (int32_t c = 0; c < M; ++c) {  /* O3: the stride-halving tree of the block's column */
+                    for (int32_t r = 0; r < P; ++r) s[r] = r < V ? blk[r * M + c] : 0.0f;
+                    for (int32_t stride = P / 2; stride >= 1; stride /= 2)
+                        for (int32_t r = 0; r < stride; ++r) s[r] = s[r] + s[r + stride];
+                    L[c] = s[0];
+                }
+                uint8_t kept[4];
+                top4_columns(L, M, kept);
+                float e4[4];
+                for (int q = 0; q < 4; ++q) e4[q] = blk[sl * M + kept[q]];
+                uint8_t lo, hi;
+                top2_positions(e4, &lo, &hi);
+                acc += (double)e4[lo];
+                acc += (double)e4[hi];
+            }
+            cost[(int64_t)i * R + gs] = acc;
+        }
+        free(s);
+        free(blk);
+    }
+    free(E);
+    return VNMO_OK;
+}
