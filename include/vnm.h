@@ -198,11 +198,23 @@ vnm_status vnm_ria_score(const uint16_t* W, int64_t ldw, int32_t rows, int32_t c
  *   of e_j = |score[.][j]| over the rows that keep slot s (reading Q22).  With the identity
  *   assignment the costs add up to the retained score of the pruned matrix.
  *   score fp32 [g->rows][lds] (4-B aligned), cost fp32 [g->cols_p][ldc], ldc >= cols_p (caller-owned);
- *   workspace >= vnm_permute_gain_workspace_bytes(g), 16-B aligned.  V <= 64 and M <= 8
- *   (VNM_ERR_UNSUPPORTED otherwise).  Deterministic (fp32 sums in stripe order).                         */
+ *   workspace >= vnm_permute_gain_workspace_bytes(g), 16-B aligned.  V <= 128, any M (VNM_ERR_UNSUPPORTED for
+ *   V = 256).  Deterministic (fp32 sums in stripe order).                                              */
 size_t vnm_permute_gain_workspace_bytes(const vnm_geom* g);
 vnm_status vnm_permute_gain(const float* score, int64_t lds, const vnm_geom* g, float* cost, int64_t ldc,
                             void* workspace, size_t workspace_bytes, vnm_stream_t stream);
+
+/* ---- The OUTPUT-channel half of the V:N:M-specific channel permutation: the LSA cost of
+ * Eq. (8) `eq:admm2` (§4.2; "V:N:M sparsity allows both input and output CP to affect the
+ * retained norm").
+ *   cost[i][g*V + s] = the retained score ROW i contributes when it replaces the occupant of slot s of V-row
+ *   stripe g (every other row frozen) and the stripe is re-pruned by S_{V:N:M} (same tie rules and fp32
+ *   L1 tree as vnm_prune): in each column block row i keeps its 2 largest |score| among the stripe's 4 kept columns
+ *   (reading Q23).  With the identity assignment the costs add up to the retained score.
+ *   score fp32 [g->rows][lds] (4-B aligned), cost fp32 [g->rows_p][ldc], ldc >= rows_p (caller-owned).  V <= 128,
+ *   any M (VNM_ERR_UNSUPPORTED for V = 256).  Deterministic (fp32 sums in column-block order).               */
+vnm_status vnm_permute_gain_out(const float* score, int64_t lds, const vnm_geom* g, float* cost, int64_t ldc,
+                                vnm_stream_t stream);
 
 /* Human-readable text of a status (static storage).                                                   */
 const char* vnm_status_string(vnm_status s);

@@ -21,7 +21,7 @@ PROBES = os.path.join(HERE, "..", "tests", "probes")
 # output path -> (source directory, sources)
 LIBS = {
     os.path.join(HERE, "libvnm.so"): (CSRC, ["api.cpp", "prune.cu", "prune2.cu", "spmm.cu", "pack_tc.cu",
-                                           "spmm_tc.cu", "spmm_tc2.cu", "spmm_tc3.cu", "spmm_smallt.cu", "ria.cu", "permute.cu"]),
+                                           "spmm_tc.cu", "spmm_tc2.cu", "spmm_tc3.cu", "spmm_smallt.cu", "ria.cu", "permute.cu", "permute_out.cu"]),
     os.path.join(PROBES, "libvnm_probe.so"): (PROBES, ["probes.cu", "probes2.cu", "probes3.cu", "probes4.cu"]),
 }
 

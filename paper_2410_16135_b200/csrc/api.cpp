@@ -366,7 +366,7 @@ vnm_status vnm_permute_gain(const float* score, int64_t lds, const vnm_geom* g, 
                             void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
     vnm_status s = check_geom(g);
     if (s) return s;
-    if (g->V > 64 || g->M > 8) return VNM_ERR_UNSUPPORTED;
+    if (g->V > 128) return VNM_ERR_UNSUPPORTED;
     if (lds < g->cols || ldc < g->cols_p) return VNM_ERR_SHAPE;
     if (g->rows == 0 || g->cols == 0) return VNM_OK;
     if (!score || !cost || !workspace) return VNM_ERR_ARG;
@@ -374,6 +374,18 @@ vnm_status vnm_permute_gain(const float* score, int64_t lds, const vnm_geom* g, 
     if ((reinterpret_cast<uintptr_t>(score) & 3u) || (reinterpret_cast<uintptr_t>(cost) & 3u) || !aligned16(workspace))
         return VNM_ERR_ALIGN;
     return from_launch(vnm::launch_permute_gain(score, lds, *g, cost, ldc, workspace, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+vnm_status vnm_permute_gain_out(const float* score, int64_t lds, const vnm_geom* g, float* cost, int64_t ldc,
+                                vnm_stream_t stream) {
+    vnm_status s = check_geom(g);
+    if (s) return s;
+    if (g->V > 128) return VNM_ERR_UNSUPPORTED;
+    if (lds < g->cols || ldc < g->rows_p) return VNM_ERR_SHAPE;
+    if (g->rows == 0 || g->cols == 0) return VNM_OK;
+    if (!score || !cost) return VNM_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(score) & 3u) || (reinterpret_cast<uintptr_t>(cost) & 3u)) return VNM_ERR_ALIGN;
+    return from_launch(vnm::launch_permute_gain_out(score, lds, *g, cost, ldc, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 const char* vnm_status_string(vnm_status s) {

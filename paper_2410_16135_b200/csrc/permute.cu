@@ -53,29 +53,31 @@ __global__ void __launch_bounds__(256) colsum_tree_kernel(const float* score, in
 // key order of both decisions: larger value first, then the smaller block position
 __device__ __forceinline__ bool beats(float va, int pa, float vb, int pb) { return va > vb || (va == vb && pa < pb); }
 
-template <int V>
+// MMAX: block width bound (8, 16, 32); KBC: column blocks per CTA (4 for M <= 8, else 1 to bound shared memory)
+template <int V, int MMAX, int KBC>
 __global__ void __launch_bounds__(256) permute_gain_kernel(const float* score, int64_t lds, int32_t rows, int32_t cols,
                                                            int32_t M, int32_t cols_p, int32_t nb, int32_t nvb,
                                                            const float* colL1, float* cost, int64_t ldc) {
-    __shared__ float sL4[kBC][8];                // 4th-best L1 of the others (per block, slot)
-    __shared__ int sC4[kBC][8];                  // ... its position (-1: M = 4, always kept)
-    __shared__ float sThrE[kBC][8][V];           // 2nd-best e of the top-3 others, per row
-    __shared__ int8_t sThrC[kBC][8][V];          // ... its position
-    __shared__ int8_t sTop3[kBC][8][3];          // the 3 best others (positions)
+    constexpr int kBC = KBC;
+    __shared__ float sL4[kBC][MMAX];             // 4th-best L1 of the others (per block, slot)
+    __shared__ int sC4[kBC][MMAX];               // ... its position (-1: M = 4, always kept)
+    __shared__ float sThrE[kBC][MMAX][V];        // 2nd-best e of the top-3 others, per row
+    __shared__ int8_t sThrC[kBC][MMAX][V];       // ... its position
+    __shared__ int8_t sTop3[kBC][MMAX][3];       // the 3 best others (positions)
     const int b0 = blockIdx.x * kBC, j = blockIdx.y * kCand + threadIdx.x;
     const int nbl = min(kBC, nb - b0);
-    float acc[kBC][8];
+    float acc[kBC][MMAX];
 #pragma unroll
     for (int b = 0; b < kBC; ++b)
 #pragma unroll
-        for (int s = 0; s < 8; ++s) acc[b][s] = 0.f;
+        for (int s = 0; s < MMAX; ++s) acc[b][s] = 0.f;
 
     for (int vb = 0; vb < nvb; ++vb) {
         const float* Lrow = colL1 + static_cast<int64_t>(vb) * cols_p;
         // ---- per (block, slot): rank the other M-1 columns by (L1 desc, position asc)
         __syncthreads();
-        if (threadIdx.x < kBC * 8) {
-            const int b = threadIdx.x / 8, s = threadIdx.x % 8;
+        if (threadIdx.x < kBC * MMAX) {
+            const int b = threadIdx.x / MMAX, s = threadIdx.x % MMAX;
             if (b < nbl && s < M) {
                 float tv[4] = {-1.f, -1.f, -1.f, -1.f};
                 int ti[4] = {-1, -1, -1, -1};
@@ -97,8 +99,8 @@ __global__ void __launch_bounds__(256) permute_gain_kernel(const float* score, i
         }
         __syncthreads();
         // ---- per (block, slot, row): the 2nd best of the top-3 others by (e desc, position asc)
-        for (int idx = threadIdx.x; idx < kBC * 8 * V; idx += 256) {
-            const int b = idx / (8 * V), s = (idx / V) % 8, r = idx % V;
+        for (int idx = threadIdx.x; idx < kBC * MMAX * V; idx += 256) {
+            const int b = idx / (MMAX * V), s = (idx / V) % MMAX, r = idx % V;
             if (b >= nbl || s >= M) continue;
             const int gr = vb * V + r;
             int ti[3];
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(256) permute_gain_kernel(const float* score, i
 #pragma unroll
         for (int b = 0; b < kBC; ++b)
 #pragma unroll
-            for (int s = 0; s < 8; ++s) {
+            for (int s = 0; s < MMAX; ++s) {
                 const int c4 = sC4[b][s];
                 // slot s must exist and be kept in this stripe (compile-time b, s: acc stays in registers)
                 if (b < nbl && s < M && (c4 < 0 || beats(Lj, s, sL4[b][s], c4))) {
@@ -144,20 +146,28 @@ __global__ void __launch_bounds__(256) permute_gain_kernel(const float* score, i
 #pragma unroll
     for (int b = 0; b < kBC; ++b)
 #pragma unroll
-        for (int s = 0; s < 8; ++s)
+        for (int s = 0; s < MMAX; ++s)
             if (b < nbl && s < M) cost[static_cast<int64_t>(j) * ldc + (b0 + b) * M + s] = acc[b][s];
+}
+
+template <int V, int MMAX, int KBC>
+int launch_vm(const float* score, int64_t lds, const vnm_geom& g, float* cost, int64_t ldc, float* colL1,
+              cudaStream_t st) {
+    const int nvb = g.rows_p / V;
+    colsum_tree_kernel<V><<<dim3((g.cols_p + 255) / 256, nvb), 256, 0, st>>>(score, lds, g.rows, g.cols, g.cols_p, colL1);
+    count_launch();
+    permute_gain_kernel<V, MMAX, KBC><<<dim3((g.nb + KBC - 1) / KBC, (g.cols_p + kCand - 1) / kCand), 256, 0, st>>>(
+        score, lds, g.rows, g.cols, g.M, g.cols_p, g.nb, nvb, colL1, cost, ldc);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
 }
 
 template <int V>
 int launch_v(const float* score, int64_t lds, const vnm_geom& g, float* cost, int64_t ldc, float* colL1,
              cudaStream_t st) {
-    const int nvb = g.rows_p / V;
-    colsum_tree_kernel<V><<<dim3((g.cols_p + 255) / 256, nvb), 256, 0, st>>>(score, lds, g.rows, g.cols, g.cols_p, colL1);
-    count_launch();
-    permute_gain_kernel<V><<<dim3((g.nb + kBC - 1) / kBC, (g.cols_p + kCand - 1) / kCand), 256, 0, st>>>(
-        score, lds, g.rows, g.cols, g.M, g.cols_p, g.nb, nvb, colL1, cost, ldc);
-    count_launch();
-    return cudaGetLastError() == cudaSuccess ? 0 : kLaunchCudaError;
+    if (g.M <= 8) return launch_vm<V, 8, (V <= 64 ? kBC : 1)>(score, lds, g, cost, ldc, colL1, st);
+    if (g.M <= 16) return launch_vm<V, 16, 1>(score, lds, g, cost, ldc, colL1, st);
+    return launch_vm<V, 32, 1>(score, lds, g, cost, ldc, colL1, st);
 }
 
 }  // namespace
@@ -168,7 +178,6 @@ size_t permute_gain_workspace_bytes(const vnm_geom& g) {
 
 int launch_permute_gain(const float* score, int64_t lds, const vnm_geom& g, float* cost, int64_t ldc, void* ws,
                         cudaStream_t st) {
-    if (g.M > 8) return kLaunchUnsupported;
     float* colL1 = static_cast<float*>(ws);
     switch (g.V) {
         case 1: return launch_v<1>(score, lds, g, cost, ldc, colL1, st);
@@ -178,6 +187,7 @@ int launch_permute_gain(const float* score, int64_t lds, const vnm_geom& g, floa
         case 16: return launch_v<16>(score, lds, g, cost, ldc, colL1, st);
         case 32: return launch_v<32>(score, lds, g, cost, ldc, colL1, st);
         case 64: return launch_v<64>(score, lds, g, cost, ldc, colL1, st);
+        case 128: return launch_v<128>(score, lds, g, cost, ldc, colL1, st);
         default: return kLaunchUnsupported;
     }
 }

@@ -82,5 +82,7 @@ int launch_act_norms(const uint16_t* XT, int64_t ldx, int32_t cols, int32_t T, f
 size_t permute_gain_workspace_bytes(const vnm_geom& g);
 int launch_permute_gain(const float* score, int64_t lds, const vnm_geom& g, float* cost, int64_t ldc, void* ws,
                         cudaStream_t st);
+int launch_permute_gain_out(const float* score, int64_t lds, const vnm_geom& g, float* cost, int64_t ldc,
+                            cudaStream_t st);  // permute_out.cu
 
 }  // namespace vnm

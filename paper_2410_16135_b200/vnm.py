@@ -50,7 +50,8 @@ _lib = None
 EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress",
            "vnm_prune_compress_batched", "vnm_pack_tc",
            "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_spmm_workspace_init", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
-           "vnm_permute_gain_workspace_bytes", "vnm_permute_gain", "vnm_status_string", "vnm_launch_count"]
+           "vnm_permute_gain_workspace_bytes", "vnm_permute_gain", "vnm_permute_gain_out", "vnm_status_string",
+           "vnm_launch_count"]
 
 
 def lib():
@@ -94,6 +95,8 @@ def lib():
             L.vnm_permute_gain_workspace_bytes.restype = sz
             L.vnm_permute_gain.argtypes = [P, i64, GP, P, i64, P, sz, P]
             L.vnm_permute_gain.restype = ctypes.c_int
+            L.vnm_permute_gain_out.argtypes = [P, i64, GP, P, i64, P]
+            L.vnm_permute_gain_out.restype = ctypes.c_int
             L.vnm_status_string.argtypes = [ctypes.c_int]
             L.vnm_status_string.restype = ctypes.c_char_p
             L.vnm_launch_count.argtypes = []
@@ -366,4 +369,18 @@ def permute_gain(score: torch.Tensor, V: int, M: int) -> torch.Tensor:
     ws = torch.empty(max(nws, 16) // 4 + 4, dtype=torch.float32, device=score.device)
     _check(lib().vnm_permute_gain(_ptr(score), _ld(score), ctypes.byref(g), _ptr(cost), cost.stride(0), _ptr(ws),
                                   ws.numel() * 4, _stream(score.device)), "vnm_permute_gain")
+    return cost
+
+
+def permute_gain_out(score: torch.Tensor, V: int, M: int) -> torch.Tensor:
+    """LSA cost matrix of the OUTPUT-channel permutation step (Eq. 8 `eq:admm2`):
+    fp32 [rows_p][rows_p], cost[i][g*V + s] = retained score row i contributes in slot s of V-row stripe g."""
+    _require_cuda(score)
+    if score.dtype != torch.float32:
+        raise TypeError("score must be fp32")
+    rows, cols = score.shape
+    g = geometry(rows, cols, V, M)
+    cost = torch.empty((g.rows_p, g.rows_p), dtype=torch.float32, device=score.device)
+    _check(lib().vnm_permute_gain_out(_ptr(score), _ld(score), ctypes.byref(g), _ptr(cost), cost.stride(0),
+                                      _stream(score.device)), "vnm_permute_gain_out")
     return cost

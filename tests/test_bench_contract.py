@@ -33,9 +33,18 @@ def test_reference_arm_json(workload):
     assert d["metric"] == json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 
 
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def test_reference_arm_rank0_only():
     lines = run(["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
-                 "--master-port", "29533", "bench.py", "--impl", "reference", "--workload", "toy", "--gpus", "2",
+                 "--master-port", str(free_port()), "bench.py", "--impl", "reference", "--workload", "toy", "--gpus", "2",
                  "--steps", "1", "--warmup", "0", "--ref-tokens", "16"])
     assert len(lines) == 1
     assert json.loads(lines[0])["impl"] == "reference"
