@@ -56,7 +56,10 @@ constexpr uint32_t kABytes = kRowsU * 128;   // A_n box [128 rows][64 bf16], SW1
 constexpr uint32_t kTicketWords = 4096;      // fixed ticket region at the start of the workspace (16 KB)
 constexpr int kMBoxUnits = 8;                // units per A_i2 box: [128 rows][8 units x 4 words] = 128 B per row
 constexpr uint32_t kMBoxBytes = kRowsU * 128;
-constexpr int kMB = 3;                       // A_i2 box ring slots
+#ifndef VNM_ST_MB
+#define VNM_ST_MB 3
+#endif
+constexpr int kMB = VNM_ST_MB;                       // A_i2 box ring slots
 constexpr uint32_t kCRow = kBlkU * 4;        // A_i1 words of one V-block and unit (128 B)
 
 // VNM_SPMM_TRACE: %globaltimer per CTA — entry, after the prologue, first unit landed, consumers done, exit
@@ -562,6 +565,11 @@ StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
                          (2 * 16 + 2 * kMB + 4) * 8 + 64;
     p.S = static_cast<int>((kMaxSmem - fixed) / p.slot_bytes);
     if (p.S > 16) p.S = 16;
+    // S a multiple of the phase count: slot s is then only ever read by the warps of phase s % kPhases, which wait
+    // on its uses in order.  (Otherwise use j + 2 of a slot can belong to a phase that never waited on use j + 1,
+    // and its parity wait passes while use j + 1's TMA is still in flight: a parity wait cannot tell phase j from
+    // phase j + 2.  Seen as a rare illegal-instruction trap on the producer's next arrive, S = 9.)
+    p.S -= p.S % kPhases;
     p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
     p.maxseg = 1;
     for (int rp = 0; rp < p.n_rp; ++rp) {
@@ -629,7 +637,7 @@ int launch_v(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUtens
 bool spmm_smallt_applies(const vnm_geom& g, int32_t T) {
     if (T < 1 || T > 32 || g.V < 16 || g.nb_pad == 0) return false;
     const StPlan p = make_plan(g, T);
-    return p.S >= 2 && p.n_rp <= static_cast<int>(kTicketWords);
+    return p.S >= kPhases && p.n_rp <= static_cast<int>(kTicketWords);
 }
 
 size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T) {
