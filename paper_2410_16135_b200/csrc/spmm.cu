@@ -428,9 +428,9 @@ void plan_units(SpmmArgs& a, const SpmmLaunch& L, int NT) {
     a.ks_n = 1;
     if (L.workspace) {
         const int ks = choose_ksplit(a.ntiles, n_stage);
-        if (ks > 1 && L.workspace_bytes >= static_cast<size_t>(ks) * a.rows * L.T * 4) {
+        if (ks > 1 && L.workspace_bytes >= kWsTicketBytes + static_cast<size_t>(ks) * a.rows * L.T * 4) {
             a.ks_n = ks;
-            a.ws = static_cast<float*>(L.workspace);
+            a.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(L.workspace) + kWsTicketBytes);  // after the tickets
         }
     }
     a.sps = (n_stage + a.ks_n - 1) / a.ks_n;
@@ -455,7 +455,7 @@ size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T) {
     if (g.V < kV || T <= 0 || T > 64 || g.nb_pad == 0) return 0;  // split-K serves the small-T (gather) plan
     const int n_stage = (g.nb_pad / 8 + kMmaPerStage - 1) / kMmaPerStage;
     const int ks = choose_ksplit(g.rows_p / kV, n_stage);
-    return ks > 1 ? static_cast<size_t>(ks) * g.rows * T * 4 : 0;
+    return ks > 1 ? kWsTicketBytes + static_cast<size_t>(ks) * g.rows * T * 4 : 0;
 }
 
 int launch_spmm(const SpmmLaunch& L, cudaStream_t stream) {

@@ -22,7 +22,8 @@
 //     shared-memory address of gathered K-row i of the k-step, i.e. X^T channel (block i/4, A_i1 position i%4)
 //     of the slice — no gather copy, no B tile, no metadata repacking;
 //   * 8 consumer warps: half h = w % 2 (64 rows = 4 m16 tiles = one V-block at V = 64), phase p = w / 2 (units
-//     p, p + 4, ... of the CTA's share);
+//     p, p + 4, ... of the CTA's share); the slot ring size S is a multiple of the phases in use (4, or S itself
+//     when only 2-3 slots fit), so every slot is read by one phase only, whose warps wait on its uses in order;
 //   * persistent CTAs take equal contiguous shares of the (row group, stage) list (stream-K); at the end of a
 //     piece (the row group changes or the share ends) the 4 phases are added in phase order through shared
 //     memory; a row group cut between CTAs is finished by the LAST CTA to arrive (ticket), which adds the fp32
@@ -53,7 +54,7 @@ constexpr int kProd = kCons;       // producer warp index
 constexpr int kFix = kCons + 1;    // fix-up warp: finishes every piece but the share's last, off the consumers' path
 constexpr int kThreads = 32 * (kCons + 2);
 constexpr uint32_t kABytes = kRowsU * 128;   // A_n box [128 rows][64 bf16], SW128
-constexpr uint32_t kTicketWords = 4096;      // fixed ticket region at the start of the workspace (16 KB)
+constexpr uint32_t kTicketWords = kWsTicketBytes / 4;  // fixed ticket region at the start of the workspace
 constexpr int kMBoxUnits = 8;                // units per A_i2 box: [128 rows][8 units x 4 words] = 128 B per row
 constexpr uint32_t kMBoxBytes = kRowsU * 128;
 #ifndef VNM_ST_MB
@@ -83,6 +84,7 @@ struct StArgs {
     uint32_t* tickets;   // [kTicketWords], zero at launch; every launch leaves them zero
     int32_t T, y_bf16, rows, rows_p, V, M, n_ks, n_st, n_rp, units, grid, maxseg;
     int32_t S;           // ring slots
+    int32_t nph;         // consumer phases in use: 4, or S when S < 4 (S is a multiple of nph)
     int32_t rg_mode;     // 1: shares are whole row groups (no workspace: no piece is ever cut between CTAs)
     int32_t c_rows;      // A_i1 rows (V-blocks) per unit: max(1, 128 / V)
     int32_t x_rows;      // X^T slice rows (32 M channels)
@@ -404,10 +406,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[mt][n][k] = 0.f;
         const bool half_ok = rp * kRowsU + 64 * h < a.rows_p;
-        // this phase's units of the piece: u = u0 + q, q = p (mod 4)
-        int u = pu0 + ((p - (pu0 - u0)) % kPhases + kPhases) % kPhases;
+        // this phase's units of the piece: u = u0 + q, q = p (mod nph); phases p >= nph have none
+        const int nph = a.nph;
+        int u = p < nph ? pu0 + ((p - (pu0 - u0)) % nph + nph) % nph : pu1;
         int s = (u - u0) % a.S, par = ((u - u0) / a.S) & 1;  // slot / phase parity, advanced without divisions
-        for (; u < pu1; u += kPhases) {
+        for (; u < pu1; u += nph) {
             const int q = u - u0;
             const int kb = k_piece + (u - pu0) / kMBoxUnits, ub = (u - pu0) % kMBoxUnits;
             release_to(kb);
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
             if (a.trace == 2 && lane == 0 && h == 0 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][2] = gtime();
-            for (s += kPhases; s >= a.S; s -= a.S) par ^= 1;
+            for (s += nph; s >= a.S; s -= a.S) par ^= 1;
         }
         k_piece += (pu1 - pu0 + kMBoxUnits - 1) / kMBoxUnits;
         release_to(k_piece);  // the piece's boxes are done (also those this warp had no unit in)
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cons_tid == 0) mbar_wait(&pempty[jp & 1], ((jp >> 1) & 1) ^ 1);  // its use two pieces ago is done
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kCons) : "memory");
 #pragma unroll 1
-        for (int r = 0; r < kPhases; ++r) {
+        for (int r = 0; r < a.nph; ++r) {
             if (p == r) {
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 struct StPlan {
-    int n_rp, n_ks, n_st, units, grid, maxseg, S, tp, c_rows, x_rows, x_pack, x_box, x_nbox;
+    int n_rp, n_ks, n_st, units, grid, maxseg, S, nph, tp, c_rows, x_rows, x_pack, x_box, x_nbox;
     uint32_t x_box_bytes, x_bytes, slot_bytes;
     size_t smem, ws_bytes;
 };
@@ -565,11 +568,12 @@ StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
                          (2 * 16 + 2 * kMB + 4) * 8 + 64;
     p.S = static_cast<int>((kMaxSmem - fixed) / p.slot_bytes);
     if (p.S > 16) p.S = 16;
-    // S a multiple of the phase count: slot s is then only ever read by the warps of phase s % kPhases, which wait
+    // S a multiple of the phase count nph: slot s is then only ever read by the warps of phase s % nph, which wait
     // on its uses in order.  (Otherwise use j + 2 of a slot can belong to a phase that never waited on use j + 1,
     // and its parity wait passes while use j + 1's TMA is still in flight: a parity wait cannot tell phase j from
     // phase j + 2.  Seen as a rare illegal-instruction trap on the producer's next arrive, S = 9.)
-    p.S -= p.S % kPhases;
+    p.nph = p.S >= kPhases ? kPhases : p.S;  // (S < 4: only S phases take units; S = 2, 3 at large M x T)
+    p.S -= p.S % (p.nph > 0 ? p.nph : 1);
     p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
     p.maxseg = 1;
     for (int rp = 0; rp < p.n_rp; ++rp) {
@@ -637,7 +641,7 @@ int launch_v(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUtens
 bool spmm_smallt_applies(const vnm_geom& g, int32_t T) {
     if (T < 1 || T > 32 || g.V < 16 || g.nb_pad == 0) return false;
     const StPlan p = make_plan(g, T);
-    return p.S >= kPhases && p.n_rp <= static_cast<int>(kTicketWords);
+    return p.S >= 2 && p.n_rp <= static_cast<int>(kTicketWords);
 }
 
 size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T) {
@@ -670,6 +674,7 @@ int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) {
     a.grid = q.grid;
     a.maxseg = p.maxseg;
     a.S = p.S;
+    a.nph = p.nph;
     a.c_rows = p.c_rows;
     a.x_rows = p.x_rows;
     a.x_pack = p.x_pack;

@@ -10,6 +10,9 @@
 namespace vnm {
 
 constexpr size_t kMaxSmem = 227 * 1024;
+// every vnm_spmm workspace starts with this ticket region (small-T plan: zero between calls); plans that keep
+// other scratch there (split-K partials) place it after the region, so one workspace serves every plan
+constexpr size_t kWsTicketBytes = 16 * 1024;
 
 // Tuning / tracing switches from the environment, read ONCE per call site and process (a function-local static
 // inside a unique lambda), so the hot path makes no getenv calls.  Timing ablations (VNM_ABL, which make the
