@@ -58,7 +58,7 @@ constexpr uint32_t kTicketWords = kWsTicketBytes / 4;  // fixed ticket region at
 constexpr int kMBoxUnits = 8;                // units per A_i2 box: [128 rows][8 units x 4 words] = 128 B per row
 constexpr uint32_t kMBoxBytes = kRowsU * 128;
 #ifndef VNM_ST_MB
-#define VNM_ST_MB 3
+#define VNM_ST_MB 2
 #endif
 constexpr int kMB = VNM_ST_MB;                       // A_i2 box ring slots
 constexpr uint32_t kCRow = kBlkU * 4;        // A_i1 words of one V-block and unit (128 B)
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int k = 0; k < kMB; ++k) {
             mbar_init(&mfull[k], 1);
-            mbar_init(&mempty[k], kCons);  // every consumer warp releases every box once
+            mbar_init(&mempty[k], 2 * a.nph);  // every consumer warp of a phase in use releases every box once
         }
         for (int k = 0; k < 2; ++k) {
             mbar_init(&pfull[k], 1);
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (s += nph; s >= a.S; s -= a.S) par ^= 1;
         }
         k_piece += (pu1 - pu0 + kMBoxUnits - 1) / kMBoxUnits;
-        release_to(k_piece);  // the piece's boxes are done (also those this warp had no unit in)
+        if (p < a.nph) release_to(k_piece);  // the piece's boxes are done (also those this warp had no unit in)
         // ---- end of the piece: phases 0..3 added in order into red[j % 2]; every piece but the share's last goes
         // to the fix-up warp (the consumers move on at once), the last one is finished here
         const bool last_piece = pu1 == u1;
@@ -572,8 +572,18 @@ StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
     // on its uses in order.  (Otherwise use j + 2 of a slot can belong to a phase that never waited on use j + 1,
     // and its parity wait passes while use j + 1's TMA is still in flight: a parity wait cannot tell phase j from
     // phase j + 2.  Seen as a rare illegal-instruction trap on the producer's next arrive, S = 9.)
-    p.nph = p.S >= kPhases ? kPhases : p.S;  // (S < 4: only S phases take units; S = 2, 3 at large M x T)
-    p.S -= p.S % (p.nph > 0 ? p.nph : 1);
+    // The phases in use (4, 3 or 2) are chosen for the deepest ring (the consumers are not the bottleneck: a unit
+    // keeps a warp ~0.4 us busy against the producer's ~0.5 us per unit, profiles/r02c_trace_up.txt).
+    {
+        int best_s = 0, best_n = 1;
+        for (int n = kPhases; n >= 2; --n)
+            if (p.S - p.S % n > best_s) {
+                best_s = p.S - p.S % n;
+                best_n = n;
+            }
+        p.nph = best_n;
+        p.S = best_s;
+    }
     p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
     p.maxseg = 1;
     for (int rp = 0; rp < p.n_rp; ++rp) {

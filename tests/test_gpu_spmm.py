@@ -371,9 +371,12 @@ def _spmm_raw(Xd, P, T, Y, ws, ws_bytes):
     assert st == 0, vnm.status_string(st)
 
 
-@pytest.mark.parametrize("rows,cols,M,T", [(11008, 4096, 5, 16), (4096, 11008, 5, 3), (300, 777, 9, 20)])
+@pytest.mark.parametrize("rows,cols,M,T", [(11008, 4096, 5, 16), (4096, 11008, 5, 3), (300, 777, 9, 20),
+                                           (1024, 11008, 13, 32), (512, 11008, 8, 16)])
 def test_smallt_without_workspace(rows, cols, M, T):
-    """No workspace: the small-T plan gives every CTA whole row groups (nothing is cut between CTAs)."""
+    """No workspace: the small-T plan gives every CTA whole row groups (nothing is cut between CTAs).  The M = 13 /
+    M = 8, T = 16 cases run a 3- / 6-slot ring with 3 phases in use over 27- / 43-unit pieces (4 / 6 A_i2 boxes:
+    the idle phase's warps must not hold a box)."""
     W, XT, Wm = make(rows, cols, 64, M, T, seed=rows + M + T)
     Yref, Aref = oracle.gemm_ref(XT, Wm)
     P = vnm.prune_compress(to_dev_bf16(W), 64, M)
