@@ -40,6 +40,12 @@ WORKLOADS = {
                           layers=[("q", 4096, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]),
     "llama_decode": dict(V=64, M=5, T=16, cfg=4,
                          layers=[("q", 4096, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]),
+    # every linear layer of one Llama2-7B transformer block at decode; layers whose inputs do not depend on each
+    # other's outputs run as one grouped launch (vnm_spmm_batched): [q k v] [o] [gate up] [down]
+    "llama_block_decode": dict(V=64, M=5, T=16, cfg=4,
+                               layers=[("q", 4096, 4096), ("k", 4096, 4096), ("v", 4096, 4096), ("o", 4096, 4096),
+                                       ("gate", 11008, 4096), ("up", 11008, 4096), ("down", 4096, 11008)],
+                               groups=[[0, 1, 2], [3], [4, 5], [6]]),
 }
 for _m in (4, 5, 6, 7, 8, 16):
     WORKLOADS[f"llama_mlp_m{_m}"] = dict(V=64, M=_m, T=2048, cfg=5, layers=[("up", 11008, 4096), ("down", 4096, 11008)])
@@ -223,6 +229,24 @@ def run_gpu(args):
 
     for l in layers:  # split-K scratch (small T), allocated once outside the timed region
         l["ws"] = vnm.spmm_workspace(l["P"].g, T, dev)  # zero-initialised once; vnm_spmm leaves it zeroed
+    # launch groups: independent layers as one vnm_spmm_batched call (workloads with "groups"; token mode)
+    groups = wl.get("groups") if not out_mode else None
+    groups = groups or [[i] for i in range(len(layers))]
+    gargs = []
+    for gr in groups:
+        if len(gr) == 1:
+            gargs.append(None)
+            continue
+        ls = [layers[i] for i in gr]
+        wsg = vnm.spmm_batched_workspace([l["P"].g for l in ls], T, dev)
+        cpg = [l["P"].c() for l in ls]
+        k = len(ls)
+        gargs.append(dict(n=k, cp=cpg, ws=wsg,
+                          X=(ctypes.c_void_p * k)(*[l["X"].data_ptr() for l in ls]),
+                          ldx=(ctypes.c_int64 * k)(*[l["X"].stride(0) for l in ls]),
+                          P=(ctypes.c_void_p * k)(*[ctypes.cast(ctypes.pointer(c), ctypes.c_void_p) for c in cpg]),
+                          Y=(ctypes.c_void_p * k)(*[l["Y"].data_ptr() for l in ls]),
+                          ldy=(ctypes.c_int64 * k)(*[l["Y"].stride(0) for l in ls])))
 
     def spmm(l):
         cp = l["P"].c()
@@ -232,6 +256,19 @@ def run_gpu(args):
                         ctypes.c_void_p(ws.data_ptr()) if ws is not None else None,
                         ws.numel() * 4 if ws is not None else 0,
                         ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+        assert st == 0, vnm.status_string(st)
+
+    def spmm_group(gi):
+        """The layers of group gi: one vnm_spmm call, or one vnm_spmm_batched call (independent layers)."""
+        a = gargs[gi]
+        if a is None:
+            spmm(layers[groups[gi][0]])
+            return
+        ws = a["ws"]
+        st = L.vnm_spmm_batched(a["n"], a["X"], a["ldx"], T, a["P"], a["Y"], a["ldy"], vnm.VNM_BF16,
+                                ctypes.c_void_p(ws.data_ptr()) if ws is not None else None,
+                                ws.numel() * 4 if ws is not None else 0,
+                                ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
         assert st == 0, vnm.status_string(st)
 
     def gather(l):
@@ -248,12 +285,16 @@ def run_gpu(args):
         prune_all()
         if ev_mid is not None:
             ev_mid.record()
-        for i, l in enumerate(layers):
-            if ev is not None:
-                ev[i][1].record()
+        if ev is None:
+            for gi in range(len(groups)):
+                spmm_group(gi)
+                for i in groups[gi]:
+                    gather(layers[i])
+            return
+        for i, l in enumerate(layers):  # detail pass: every layer alone, an event pair around each launch
+            ev[i][1].record()
             spmm(l)
-            if ev is not None:
-                ev[i][2].record()
+            ev[i][2].record()
             gather(l)
 
     # e2e: host->device copies on one stream, compute on the main stream, device->host on a third, chained by
@@ -273,14 +314,17 @@ def run_gpu(args):
         stream.wait_event(ev_w)
         prune_all()
         s_d2h.wait_stream(stream)
-        for i, l in enumerate(layers):
-            stream.wait_event(ev_x[i])
-            spmm(l)
-            gather(l)
-            ev_y[i].record(stream)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev_y[i])
-                l["Yh"].copy_(l["Y"].view(torch.int16), non_blocking=True)
+        for gi, gr in enumerate(groups):
+            for i in gr:
+                stream.wait_event(ev_x[i])
+            spmm_group(gi)
+            for i in gr:
+                l = layers[i]
+                gather(l)
+                ev_y[i].record(stream)
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_y[i])
+                    l["Yh"].copy_(l["Y"].view(torch.int16), non_blocking=True)
         stream.wait_stream(s_d2h)
         stream.wait_stream(s_h2d)
 
@@ -310,6 +354,16 @@ def run_gpu(args):
     graph_detail = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph_detail):
         step(ev)
+    grouped = any(len(gr) > 1 for gr in groups)
+    if grouped:  # per-group times of the grouped launches (detail)
+        evg = [(EX(), EX()) for _ in groups]
+        graph_groups = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_groups):
+            prune_all()
+            for gi in range(len(groups)):
+                evg[gi][0].record()
+                spmm_group(gi)
+                evg[gi][1].record()
     # ---- warm-up
     for _ in range(args.warmup):
         graph.replay()
@@ -345,6 +399,14 @@ def run_gpu(args):
         pc_ms[0].append(ev[0][0].elapsed_time(ev[0][1]))
         for i in range(len(layers)):
             sp_ms[i].append(ev[i][1].elapsed_time(ev[i][2]))
+    grp_ms = [[] for _ in groups]
+    if grouped:
+        for _ in range(args.steps):
+            flush_l2()
+            graph_groups.replay()
+            torch.cuda.synchronize(dev)
+            for gi in range(len(groups)):
+                grp_ms[gi].append(evg[gi][0].elapsed_time(evg[gi][1]))
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -385,9 +447,10 @@ def run_gpu(args):
             traffic = None
     roofline = {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
                 "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_note": traffic_note,
-                "kernel": "vnm_spmm (tcgen05.mma.sp window-form / small-T kernels, per-layer launches); time = the "
-                          "SpMM section of each timed step (one event after the prune pass -> step end, inter-kernel "
-                          "gaps included)",
+                "kernel": ("vnm_spmm (tcgen05.mma.sp window-form / small-T kernels, " +
+                           ("independent layers grouped into vnm_spmm_batched launches" if grouped else "per-layer launches") +
+                           "); time = the SpMM section of each timed step (one event after the prune pass -> step end, "
+                           "inter-kernel gaps included)"),
                 "peak_source": "MEASURED_PEAKS.json" if not pk.get("fallback") else "fallback",
                 "spmm_share_of_step": round(sp_t / (ms_per_step * 1e-3), 4)}
 
@@ -435,6 +498,17 @@ def run_gpu(args):
     detail["prune_compress_batched_us"] = round(pc_t * 1e6, 2)  # one vnm_prune_compress_batched launch, all layers
     detail["prune_gbs"] = round(sum(l["n"]["prune_bytes"] for l in layers) / pc_t / 1e9, 1)
     detail["step_ms_min"] = round(min(step_ms), 4)
+    if grouped:  # the timed step's launches: groups of independent layers (one vnm_spmm_batched call each)
+        detail["groups"] = []
+        for gi, gr in enumerate(groups):
+            t_g = statistics.mean(grp_ms[gi]) * 1e-3
+            b_g = sum(layers[i]["n"]["packed_bytes"] + layers[i]["n"]["xt_bytes"] + layers[i]["n"]["yt_bytes"] for i in gr)
+            detail["groups"].append({"layers": "+".join(layers[i]["name"] for i in gr), "spmm_us": round(t_g * 1e6, 2),
+                                     "spmm_gbs": round(b_g / t_g / 1e9, 1),
+                                     **({"dense_us": round(sum(base["dense_us"][i] for i in gr), 2)}
+                                        if base.get("dense_us") else {})})
+        if base.get("dense_ms") is not None:
+            detail["speedup_vs_dense_grouped"] = round(base["dense_ms"] / (sum(statistics.mean(x) for x in grp_ms)), 3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -448,7 +522,8 @@ def run_gpu(args):
                           "parallelism": (f"output-feature sharded x{world} + NCCL all-gather of Y^T" if out_mode else
                                           f"token-sharded x{world}") if world > 1 else "single GPU",
                           "l2": "flushed between timed steps (256 MB write, then a 256 MB read so its write-back happens before the timing)",
-                          "launch": "timed steps replay one CUDA graph of the step; e2e launches eagerly"},
+                          "launch": "timed steps replay one CUDA graph of the step; e2e launches eagerly",
+                          **({"spmm_groups": ["+".join(layers[i]["name"] for i in gr) for gr in groups]} if grouped else {})},
                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "roofline": roofline,
                "cpu_baseline": cpu, "detail": detail}
         print(json.dumps(out), flush=True)

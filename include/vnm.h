@@ -168,6 +168,22 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
                     vnm_dtype y_dtype, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
 
 size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T);
+
+/* n INDEPENDENT vnm_spmm problems sharing T and y_dtype (a grouped SpMM, e.g. the q / k / v projections or the
+ * gate / up projections of one decode step — layers whose inputs do not depend on each other's outputs):
+ * entry i has the meaning of vnm_spmm(XT[i], ldx[i], T, P[i], YT[i], ldy[i], y_dtype, ...).  Consecutive groups
+ * of up to 4 problems that all take the small-T plan (1 <= T <= 32, V >= 16) with one V class (all V >= 64, or
+ * equal V) run as ONE launch of the small-T kernel over the concatenated (problem, row group, stage) unit list —
+ * one prologue, one pipeline fill and one stream-K tail for the group instead of one per layer; any other group
+ * runs as one vnm_spmm per problem, in order, on `stream`.  Results are identical to n vnm_spmm calls up to the
+ * fp32 summation order of the K pieces (deterministic for a given batch).  workspace: as for vnm_spmm, sized by
+ * vnm_spmm_batched_workspace_bytes (one workspace serves the whole call).  Errors: VNM_ERR_ARG (n < 1 or n > 64,
+ * NULL arrays), else the first invalid entry's vnm_spmm status (nothing launched).                       */
+vnm_status vnm_spmm_batched(int32_t n, const uint16_t* const* XT, const int64_t* ldx, int32_t T,
+                            const vnm_packed* const* P, void* const* YT, const int64_t* ldy, vnm_dtype y_dtype,
+                            void* workspace, size_t workspace_bytes, vnm_stream_t stream);
+size_t vnm_spmm_batched_workspace_bytes(int32_t n, const vnm_geom* const* g, int32_t T);
+
 /* Zero-fill a vnm_spmm workspace (asynchronous on stream).  VNM_ERR_ARG if ws is NULL with bytes > 0.     */
 vnm_status vnm_spmm_workspace_init(void* ws, size_t bytes, vnm_stream_t stream);
 

@@ -318,6 +318,70 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+vnm_status vnm_spmm_batched(int32_t n, const uint16_t* const* XT, const int64_t* ldx, int32_t T,
+                            const vnm_packed* const* P, void* const* YT, const int64_t* ldy, vnm_dtype y_dtype,
+                            void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
+    if (n < 1 || n > 64 || !XT || !ldx || !P || !YT || !ldy) return VNM_ERR_ARG;
+    if (y_dtype != VNM_F32 && y_dtype != VNM_BF16) return VNM_ERR_ARG;
+    if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
+    // validate every problem as vnm_spmm does before launching anything
+    for (int i = 0; i < n; ++i) {
+        if (!P[i]) return VNM_ERR_ARG;
+        const vnm_geom* g = &P[i]->g;
+        vnm_status s = check_geom(g);
+        if (s) return s;
+        if ((s = check_packed(P[i], g))) return s;
+        if (T < 0 || ldx[i] < T || ldy[i] < T) return VNM_ERR_SHAPE;
+        if (T == 0 || g->rows == 0) continue;
+        if (!YT[i] || (g->cols > 0 && !XT[i])) return VNM_ERR_ARG;
+        if ((XT[i] && !aligned16(XT[i])) || !aligned16(YT[i]) || (ldx[i] % 8) != 0 || (ldy[i] % 8) != 0) return VNM_ERR_ALIGN;
+    }
+    // groups of up to 4 consecutive problems in one small-T launch when they all take the small-T plan (T <= 32:
+    // the window form is never used there); anything else is one vnm_spmm per problem (same stream order)
+    for (int c = 0; c < n; c += 4) {
+        const int m = n - c < 4 ? n - c : 4;
+        const vnm_geom* gs[4];
+        vnm::SpmmLaunch Ls[4];
+        int live = 0;
+        bool one = true;
+        for (int i = c; i < c + m; ++i) {
+            if (T == 0 || P[i]->g.rows == 0) continue;
+            gs[live] = &P[i]->g;
+            Ls[live] = vnm::SpmmLaunch{P[i], XT[i], ldx[i], T, YT[i], ldy[i], y_dtype, workspace, workspace ? workspace_bytes : 0};
+            if (P[i]->g.nb_pad == 0) one = false;  // (K = 0: vnm_spmm writes zeros)
+            ++live;
+        }
+        if (live == 0) continue;
+        one = one && live > 1 && vnm::spmm_smallt_batch_applies(gs, live, T);
+        if (one) {
+            const vnm_status s = from_launch(vnm::launch_spmm_smallt_batch(Ls, live, reinterpret_cast<cudaStream_t>(stream)));
+            if (s) return s;
+            continue;
+        }
+        for (int i = c; i < c + m; ++i) {
+            const vnm_status s = vnm_spmm(XT[i], ldx[i], T, P[i], YT[i], ldy[i], y_dtype, workspace, workspace_bytes, stream);
+            if (s) return s;
+        }
+    }
+    return VNM_OK;
+}
+
+size_t vnm_spmm_batched_workspace_bytes(int32_t n, const vnm_geom* const* g, int32_t T) {
+    if (n < 1 || n > 64 || !g || T < 0) return 0;
+    size_t b = 0;
+    for (int c = 0; c < n; c += 4) {
+        const int m = n - c < 4 ? n - c : 4;
+        for (int i = c; i < c + m; ++i) {
+            if (!g[i] || check_geom(g[i]) != VNM_OK) return 0;
+            const size_t o = vnm_spmm_workspace_bytes(g[i], T);
+            b = o > b ? o : b;
+        }
+        const size_t o = vnm::spmm_smallt_batch_workspace_bytes(g + c, m, T);
+        b = o > b ? o : b;
+    }
+    return b;
+}
+
 vnm_status vnm_spmm_workspace_init(void* ws, size_t bytes, vnm_stream_t stream) {
     if (bytes == 0) return VNM_OK;
     if (!ws) return VNM_ERR_ARG;

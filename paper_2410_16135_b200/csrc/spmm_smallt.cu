@@ -72,39 +72,64 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 
-struct StArgs {
-    const uint16_t* XT;
-    const uint32_t* meta;
-    const uint8_t* col_idx;
-    int64_t ldx;
-    int32_t cols, ld_meta, nb_pad, n_vb;
+constexpr int kMaxProb = 4;  // problems per launch (vnm_spmm_batched)
+
+// one problem of the launch (its own weights, X^T, Y^T; the same T, y dtype and V class as the others)
+struct StProb {
     void* YT;
     int64_t ldy;
-    float* ws;           // partials [n_rp][maxseg][128][TP] fp32 (after the ticket region)
-    uint32_t* tickets;   // [kTicketWords], zero at launch; every launch leaves them zero
-    int32_t T, y_bf16, rows, rows_p, V, M, n_ks, n_st, n_rp, units, grid, maxseg;
-    int32_t S;           // ring slots
-    int32_t nph;         // consumer phases in use: 4, or S when S < 4 (S is a multiple of nph)
-    int32_t rg_mode;     // 1: shares are whole row groups (no workspace: no piece is ever cut between CTAs)
+    int32_t rows, rows_p, V, M, n_st, n_rp;
     int32_t c_rows;      // A_i1 rows (V-blocks) per unit: max(1, 128 / V)
-    int32_t x_rows;      // X^T slice rows (32 M channels)
     int32_t x_pack;      // > 1: X^T viewed as 128-byte lines of x_pack = 64 / ldx channels (SW128); 1: one row per channel
     int32_t x_l8;        // ldx / 8 (16-byte chunks per channel in the packed view)
     int32_t x_pack_log2;
-    int32_t x_box, x_nbox;        // rows of the view per TMA box (<= 256), boxes per slice
-    uint32_t x_box_bytes;         // shared-memory bytes per box
-    uint32_t x_bytes;    // slice bytes in shared memory (rounded to 1 KB)
-    uint32_t slot_bytes, tx_bytes, c_bytes;
+    int32_t x_box, x_nbox;  // rows of the view per TMA box (<= 256), boxes per slice
+    uint32_t x_box_bytes;   // shared-memory bytes per box
+    uint32_t tx_bytes, c_bytes;
+};
+
+// the problems' tensor maps: [problem][A_n, X^T, A_i2, A_i1]
+struct StMaps {
+    CUtensorMap m[kMaxProb][4];
+};
+
+struct StArgs {
+    float* ws;           // partials [row groups][maxseg][128][TP] fp32 (after the ticket region)
+    uint32_t* tickets;   // [kTicketWords] per row group (all problems), zero at launch; every launch leaves them zero
+    int32_t T, units, grid, maxseg, n_rg;
+    int32_t n_prob;
+    int32_t ub[kMaxProb + 1];  // first unit of problem i (ub[n_prob] = units); units are problem-major
+    int32_t gb[kMaxProb + 1];  // first row group of problem i in the launch-wide numbering (tickets, partials)
+    int32_t S;           // ring slots
+    int32_t nph;         // consumer phases in use (4, 3 or 2; S is a multiple of nph)
+    int32_t rg_mode;     // 1: shares are whole row groups (no workspace: no piece is ever cut between CTAs)
+    uint32_t x_bytes;    // X^T slice bytes per slot (the largest problem's, rounded to 1 KB)
+    uint32_t slot_bytes;
     int32_t trace;
     int32_t abl;  // VNM_ABL timing ablations (-DVNM_ABLATIONS builds only; results invalid): 1 consumers skip the
                   // MMA work, 2 no X^T slice loads, 8 no A_i2 / A_i1 loads
+    StProb pr[kMaxProb];
 };
 
+__device__ __forceinline__ int prob_of(const StArgs& a, int u) {  // problem holding (launch-wide) unit u
+    int i = 0;
+#pragma unroll
+    for (int k = 1; k < kMaxProb; ++k)
+        if (k < a.n_prob && u >= a.ub[k]) i = k;
+    return i;
+}
 __device__ __forceinline__ int unit_owner(const StArgs& a, int u) {  // CTA whose share contains unit u
     return static_cast<int>((static_cast<long long>(u + 1) * a.grid - 1) / a.units);
 }
 __device__ __forceinline__ int share_begin(const StArgs& a, int b) {  // first unit of CTA b's share
-    if (a.rg_mode) return static_cast<int>(static_cast<long long>(b) * a.n_rp / a.grid) * a.n_st;
+    if (a.rg_mode) {  // whole row groups: the first unit of launch-wide row group G
+        const int G = static_cast<int>(static_cast<long long>(b) * a.n_rg / a.grid);
+        int i = 0;
+#pragma unroll
+        for (int k = 1; k < kMaxProb; ++k)
+            if (k < a.n_prob && G >= a.gb[k]) i = k;
+        return G >= a.n_rg ? a.units : a.ub[i] + (G - a.gb[i]) * a.pr[i].n_st;
+    }
     return static_cast<int>(static_cast<long long>(b) * a.units / a.grid);
 }
 
@@ -145,27 +170,30 @@ __device__ __forceinline__ uint32_t xoff(int r, int n) {
 // Called by the 256 consumer threads (cons: named barrier 1) for the share's last piece, and by the fix-up warp
 // (__syncwarp) for the others.
 template <int TP, bool kBf16, int kNthr>
-__device__ __forceinline__ void finish_piece(const StArgs& a, int rp, int pu0, int pu1, float* redb, int tid,
+__device__ __forceinline__ void finish_piece(const StArgs& a, int pi, int rp, int pu0, int pu1, float* redb, int tid,
                                              uint32_t t_early, uint32_t& flag) {
     auto sync = [&] {
         if constexpr (kNthr == 32) __syncwarp();
         else asm volatile("bar.sync 1, %0;" ::"n"(kNthr) : "memory");
     };
     constexpr int kN4 = kRowsU * TP / 4;  // float4 groups of a piece
+    const StProb& pp = a.pr[pi];
     const int row0 = rp * kRowsU;
+    const int rg_u0 = a.ub[pi] + rp * pp.n_st;  // the row group's first (launch-wide) unit
+    const int G = a.gb[pi] + rp;                // its launch-wide index (ticket, partials)
     float4* red4 = reinterpret_cast<float4*>(redb);
-    const bool whole = pu0 == rp * a.n_st && pu1 == (rp + 1) * a.n_st;
+    const bool whole = pu0 == rg_u0 && pu1 == rg_u0 + pp.n_st;
     if (!whole) {
-        const int own0 = unit_owner(a, rp * a.n_st);
-        const int nseg = unit_owner(a, rp * a.n_st + a.n_st - 1) - own0 + 1;
+        const int own0 = unit_owner(a, rg_u0);
+        const int nseg = unit_owner(a, rg_u0 + pp.n_st - 1) - own0 + 1;
         const int me = static_cast<int>(blockIdx.x) - own0;
-        float* wsr = a.ws + static_cast<int64_t>(rp) * a.maxseg * kRowsU * TP;
+        float* wsr = a.ws + static_cast<int64_t>(G) * a.maxseg * kRowsU * TP;
         // are all the other pieces in already (the ticket read when the piece began, else read once more now)?
         // then this CTA is the last one and finishes without publishing its own piece; otherwise publish + count
         if (tid == 0) {
             uint32_t t = t_early;
             if (t != ~0u && t != static_cast<uint32_t>(nseg - 1))
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(a.tickets + rp) : "memory");
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(a.tickets + G) : "memory");
             flag = t == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
         }
         sync();
@@ -175,7 +203,7 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int rp, int pu0, i
             sync();
             if (tid == 0) {
                 uint32_t old;
-                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.tickets + rp) : "memory");
+                asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.tickets + G) : "memory");
                 flag = old == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
             }
             sync();
@@ -227,7 +255,7 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int rp, int pu0, i
                 if (i0 + k * kNthr < kN4) red4[i0 + k * kNthr] = sum[k];
         }
         sync();
-        if (tid == 0) a.tickets[rp] = 0u;  // ready for the next launch (stream order)
+        if (tid == 0) a.tickets[G] = 0u;  // ready for the next launch (stream order)
     }
     // Y^T rows row0 .. +127, tokens [0, T): one 16-byte group (8 bf16 / 4 fp32 tokens) per thread and step
     constexpr int kEl = kBf16 ? 8 : 4;
@@ -235,9 +263,9 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int rp, int pu0, i
     for (int i = tid; i < kRowsU * kGroups; i += kNthr) {
         const int r = i / kGroups, t0 = (i % kGroups) * kEl;
         const int grow = row0 + r;
-        if (grow >= a.rows || t0 >= a.T) continue;
+        if (grow >= pp.rows || t0 >= a.T) continue;
         const float* v = redb + r * TP + t0;
-        uint8_t* dst = static_cast<uint8_t*>(a.YT) + (static_cast<int64_t>(grow) * a.ldy + t0) * (kBf16 ? 2 : 4);
+        uint8_t* dst = static_cast<uint8_t*>(pp.YT) + (static_cast<int64_t>(grow) * pp.ldy + t0) * (kBf16 ? 2 : 4);
         if (t0 + kEl <= a.T) {
             uint32_t w[4];
             if constexpr (kBf16) {
@@ -266,9 +294,7 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int rp, int pu0, i
 // NT8: token tiles of 8 computed (T <= 8 NT8); VSET: V-blocks per 64-row half (64 / V for V <= 64, else 1)
 template <int NT8, int VSET, bool kBf16>
 __global__ void __launch_bounds__(kThreads, 1)
-    vnm_spmm_smallt_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_x,
-                           const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_c,
-                           const StArgs a) {
+    vnm_spmm_smallt_kernel(const __grid_constant__ StMaps maps, const __grid_constant__ StArgs a) {
     constexpr int TP = NT8 == 1 ? 8 : (NT8 == 2 ? 16 : 32);  // tokens per X^T slice row in shared memory
     extern __shared__ __align__(1024) uint8_t smem[];
     // [A_i2 box ring: kMB x 16 KB][slot s: A_n 16 KB | X^T slice x_bytes | A_i1 c_rows x 128 B]
@@ -305,10 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_mbar_init();
     }
     if (warp == kProd && lane == 0) {
-        tma_prefetch_desc(&tm_a);
-        tma_prefetch_desc(&tm_x);
-        tma_prefetch_desc(&tm_m);
-        tma_prefetch_desc(&tm_c);
+        for (int i = 0; i < a.n_prob; ++i)
+            for (int j = 0; j < 4; ++j) tma_prefetch_desc(&maps.m[i][j]);
     }
     __syncthreads();
     grid_dep_wait();    // the previous kernel's outputs (this layer's X^T, packed weights) are visible
@@ -323,34 +347,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             // [128 rows][8 units x 4 words] (128-byte swizzle) from the first unit of each piece (row group of the
             // share) on, in a ring of kMB boxes; box k is issued with the first unit that reads it
             int k = 0, pend = u0;  // next box; first unit past the last issued box
-            int rp = u0 / a.n_st, st = u0 - rp * a.n_st, s = 0, par = 0;  // (incremental: no divisions per unit)
+            int pi = prob_of(a, u0);
+            const StProb* pp = &a.pr[pi];
+            const CUtensorMap* tm = maps.m[pi];
+            int rp = (u0 - a.ub[pi]) / pp->n_st, st = u0 - a.ub[pi] - rp * pp->n_st, s = 0, par = 0;  // (incremental)
             for (int u = u0, q = 0; u < u1; ++u, ++q) {
                 if (u == pend) {
-                    const int pu1 = min(u1, (rp + 1) * a.n_st);
+                    const int pu1 = min(u1, a.ub[pi] + (rp + 1) * pp->n_st);
                     const int ms = k % kMB;
                     mbar_wait(&mempty[ms], ((k / kMB) & 1) ^ 1);
                     mbar_arrive_expect_tx(&mfull[ms], kMBoxBytes);
-                    tma_load_2d(mbox + ms * kMBoxBytes, &tm_m, kKS * st, rp * kRowsU, &mfull[ms]);
+                    tma_load_2d(mbox + ms * kMBoxBytes, &tm[2], kKS * st, rp * kRowsU, &mfull[ms]);
                     pend = min(pu1, u + kMBoxUnits);
                     ++k;
                 }
                 mbar_wait(&empty[s], par ^ 1);
                 if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][0] = gtime();
                 uint8_t* base = slots + s * a.slot_bytes;
-                mbar_arrive_expect_tx(&full[s], (a.abl & 2) ? kABytes + a.c_bytes : a.tx_bytes);
-                tma_load_2d(base, &tm_a, st * 2 * kBlkU, rp * kRowsU, &full[s]);
-                const int y0 = (st * kBlkU * a.M) >> a.x_pack_log2;  // first row of the slice in the X^T view
-                for (int b = 0; b < ((a.abl & 2) ? 0 : a.x_nbox); ++b)
-                    tma_load_2d(base + kABytes + b * a.x_box_bytes, &tm_x, 0, y0 + b * a.x_box, &full[s]);
-                tma_load_2d(base + kABytes + a.x_bytes, &tm_c, st * kBlkU, (rp * kRowsU) / a.V, &full[s]);
+                mbar_arrive_expect_tx(&full[s], (a.abl & 2) ? kABytes + pp->c_bytes : pp->tx_bytes);
+                tma_load_2d(base, &tm[0], st * 2 * kBlkU, rp * kRowsU, &full[s]);
+                const int y0 = (st * kBlkU * pp->M) >> pp->x_pack_log2;  // first row of the slice in the X^T view
+                for (int b = 0; b < ((a.abl & 2) ? 0 : pp->x_nbox); ++b)
+                    tma_load_2d(base + kABytes + b * pp->x_box_bytes, &tm[1], 0, y0 + b * pp->x_box, &full[s]);
+                tma_load_2d(base + kABytes + a.x_bytes, &tm[3], st * kBlkU, (rp * kRowsU) / pp->V, &full[s]);
                 if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][3] = gtime();
                 if (++s == a.S) {
                     s = 0;
                     par ^= 1;
                 }
-                if (++st == a.n_st) {
+                if (++st == pp->n_st) {
                     st = 0;
-                    ++rp;
+                    if (++rp == pp->n_rp && u + 1 < u1) {  // next problem
+                        rp = 0;
+                        ++pi;
+                        pp = &a.pr[pi];
+                        tm = maps.m[pi];
+                    }
                 }
             }
         }
@@ -361,10 +393,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ fix-up warp: every piece but the last
         int jp = 0;
         for (int pu0 = u0; pu0 < u1; ++jp) {
-            const int rp = pu0 / a.n_st, pu1 = min(u1, (rp + 1) * a.n_st);
+            const int pi = prob_of(a, pu0), rp = (pu0 - a.ub[pi]) / a.pr[pi].n_st;
+            const int pu1 = min(u1, a.ub[pi] + (rp + 1) * a.pr[pi].n_st);
             if (pu1 == u1) break;  // the share's last piece: the consumers finish it
             mbar_wait(&pfull[jp & 1], (jp >> 1) & 1);
-            finish_piece<TP, kBf16, 32>(a, rp, pu0, pu1, red + (jp & 1) * (kRowsU * TP), lane, ~0u, flags[1]);
+            finish_piece<TP, kBf16, 32>(a, pi, rp, pu0, pu1, red + (jp & 1) * (kRowsU * TP), lane, ~0u, flags[1]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&pempty[jp & 1]);
             pu0 = pu1;
@@ -392,12 +425,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     int jp = 0;  // piece index (the fix-up warp's numbering)
     for (int pu0 = u0; pu0 < u1;) {
-        const int rp = pu0 / a.n_st;
-        const int pu1 = min(u1, (rp + 1) * a.n_st);
+        const int pi = prob_of(a, pu0);
+        const StProb& pp = a.pr[pi];
+        const int rg_u0 = a.ub[pi] + (pu0 - a.ub[pi]) / pp.n_st * pp.n_st;  // the row group's first unit
+        const int rp = (rg_u0 - a.ub[pi]) / pp.n_st;
+        const int pu1 = min(u1, rg_u0 + pp.n_st);
+        // this problem's geometry for the k-step loop
+        const int M = pp.M, c_rows = pp.c_rows, x_pack = pp.x_pack, x_pack_log2 = pp.x_pack_log2, x_l8 = pp.x_l8;
         // the share's last piece of a cut row group: read its ticket now (acquire); used when the piece is done
         uint32_t t_early = ~0u;
-        if (pu1 == u1 && !(pu0 == rp * a.n_st && pu1 == (rp + 1) * a.n_st) && cons_tid == 0 && !a.rg_mode)
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t_early) : "l"(a.tickets + rp) : "memory");
+        if (pu1 == u1 && !(pu0 == rg_u0 && pu1 == rg_u0 + pp.n_st) && cons_tid == 0 && !a.rg_mode)
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t_early) : "l"(a.tickets + a.gb[pi] + rp) : "memory");
 
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
@@ -405,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int n = 0; n < NT8; ++n)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) acc[mt][n][k] = 0.f;
-        const bool half_ok = rp * kRowsU + 64 * h < a.rows_p;
+        const bool half_ok = rp * kRowsU + 64 * h < pp.rows_p;
         // this phase's units of the piece: u = u0 + q, q = p (mod nph); phases p >= nph have none
         const int nph = a.nph;
         int u = p < nph ? pu0 + ((p - (pu0 - u0)) % nph + nph) % nph : pu1;
@@ -446,20 +484,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int ks = 0; ks < kKS; ++ks)
 #pragma unroll
                     for (int v = 0; v < VSET; ++v) {
-                        const int crow = a.c_rows == 1 ? 0 : h * VSET + v;
+                        const int crow = c_rows == 1 ? 0 : h * VSET + v;
                         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cwv[ks][v]) : "r"(sC + crow * kCRow + 4 * (8 * ks + (lane >> 2))));
                     }
                 // B of k-step ks: lane i addresses gathered K-row i = block 8 ks + i / 4, A_i1 position i % 4
                 auto load_b = [&](int ks, uint32_t (&B)[VSET][NT8][4]) {
 #pragma unroll
                     for (int v = 0; v < VSET; ++v) {
-                        const int xr = (8 * ks + (lane >> 2)) * a.M + static_cast<int>((cwv[ks][v] >> (8 * (lane & 3))) & 0xFFu);
+                        const int xr = (8 * ks + (lane >> 2)) * M + static_cast<int>((cwv[ks][v] >> (8 * (lane & 3))) & 0xFFu);
 #pragma unroll
                         for (int n = 0; n < NT8; ++n) {
                             uint32_t off;
-                            if (a.x_pack > 1) {  // X^T viewed as 128-byte lines of x_pack channels (SW128)
-                                const int line = xr >> a.x_pack_log2;
-                                const int ch = (xr & (a.x_pack - 1)) * a.x_l8 + n;
+                            if (x_pack > 1) {  // X^T viewed as 128-byte lines of x_pack channels (SW128)
+                                const int line = xr >> x_pack_log2;
+                                const int ch = (xr & (x_pack - 1)) * x_l8 + n;
                                 off = 128u * line + 16u * ((ch ^ line) & 7);
                             } else {
                                 off = xoff<TP>(xr, n);
@@ -528,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!last_piece) {
             if (cons_tid == 0) mbar_arrive(&pfull[jp & 1]);
         } else {
-            finish_piece<TP, kBf16, 32 * kCons>(a, rp, pu0, pu1, redb, cons_tid, t_early, flags[0]);
+            finish_piece<TP, kBf16, 32 * kCons>(a, pi, rp, pu0, pu1, redb, cons_tid, t_early, flags[0]);
         }
         ++jp;
         pu0 = pu1;
@@ -536,33 +574,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tr) g_st_t[3][blockIdx.x] = gtime();
 }
 
-struct StPlan {
-    int n_rp, n_ks, n_st, units, grid, maxseg, S, nph, tp, c_rows, x_rows, x_pack, x_box, x_nbox;
-    uint32_t x_box_bytes, x_bytes, slot_bytes;
-    size_t smem, ws_bytes;
+struct StProbPlan {
+    int n_rp, n_st, c_rows, x_pack, x_box, x_nbox;
+    uint32_t x_box_bytes, x_bytes;
 };
 
-// ldx: X^T's leading dimension (0: assume ldx == TP, the dense case; only the X^T view / box shape depend on it)
-StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
+struct StPlan {
+    int n, units, n_rg, grid, maxseg, S, nph, tp, c_rows;
+    int ub[kMaxProb + 1], gb[kMaxProb + 1];
+    StProbPlan pr[kMaxProb];
+    uint32_t x_bytes, slot_bytes;
+    size_t smem, ws_bytes;
+    bool ok;
+};
+
+// n problems of one launch (the same T; units problem-major).  ldx[i]: X^T_i's leading dimension (nullptr or 0:
+// assume ldx == TP, the dense case; only the X^T view / box shape depend on it)
+StPlan make_plan(const vnm_geom* const* gs, const int64_t* ldx, int n, int32_t T) {
     StPlan p{};
-    p.n_rp = (g.rows_p + kRowsU - 1) / kRowsU;
-    p.n_ks = g.nb_pad / 8;
-    p.n_st = (p.n_ks + kKS - 1) / kKS;
-    p.units = p.n_rp * p.n_st;
-    p.grid = p.units < num_sms() ? p.units : num_sms();
+    p.n = n;
     p.tp = T <= 8 ? 8 : (T <= 16 ? 16 : 32);
-    p.c_rows = g.V >= kRowsU ? 1 : kRowsU / g.V;
-    p.x_rows = kBlkU * g.M;
-    // X^T slice by TMA: with a dense X^T (ldx == TP) the slice rows are contiguous, so it is viewed as 128-byte
-    // lines of 64 / TP channels (4x fewer, 4x longer TMA rows at TP = 16; SW128); otherwise one row per channel
-    if (ldx == 0) ldx = p.tp;
-    p.x_pack = (ldx == p.tp && g.cols % (64 / p.tp) == 0) ? 64 / p.tp : 1;
-    const int vrows = p.x_rows / p.x_pack;                  // rows of the X^T view per slice
-    const uint32_t row_bytes = p.x_pack > 1 ? 128u : static_cast<uint32_t>(p.tp * 2);
-    p.x_nbox = (vrows + 255) / 256;
-    p.x_box = ((vrows + p.x_nbox - 1) / p.x_nbox + 7) / 8 * 8;  // whole 8-row swizzle atoms per box
-    p.x_box_bytes = static_cast<uint32_t>(p.x_box) * row_bytes;
-    p.x_bytes = (p.x_nbox * p.x_box_bytes + 1023) / 1024 * 1024;
+    p.ok = n >= 1 && n <= kMaxProb && T >= 1 && T <= 32;
+    if (!p.ok) return p;
+    int vset0 = 0;
+    for (int i = 0; i < n; ++i) {
+        const vnm_geom& g = *gs[i];
+        StProbPlan& q = p.pr[i];
+        const int vset = g.V >= 64 ? 1 : (g.V > 0 ? 64 / g.V : 0);
+        if (g.V < 16 || g.nb_pad == 0 || g.rows_p == 0 || (i > 0 && vset != vset0)) {
+            p.ok = false;
+            return p;
+        }
+        vset0 = vset;
+        q.n_rp = (g.rows_p + kRowsU - 1) / kRowsU;
+        q.n_st = (g.nb_pad / 8 + kKS - 1) / kKS;
+        q.c_rows = g.V >= kRowsU ? 1 : kRowsU / g.V;
+        // X^T slice by TMA: with a dense X^T (ldx == TP) the slice rows are contiguous, so it is viewed as 128-byte
+        // lines of 64 / TP channels (4x fewer, 4x longer TMA rows at TP = 16; SW128); otherwise one row per channel
+        const int64_t lx = (ldx && ldx[i]) ? ldx[i] : p.tp;
+        q.x_pack = (lx == p.tp && g.cols % (64 / p.tp) == 0) ? 64 / p.tp : 1;
+        const int vrows = kBlkU * g.M / q.x_pack;  // rows of the X^T view per slice
+        const uint32_t row_bytes = q.x_pack > 1 ? 128u : static_cast<uint32_t>(p.tp * 2);
+        q.x_nbox = (vrows + 255) / 256;
+        q.x_box = ((vrows + q.x_nbox - 1) / q.x_nbox + 7) / 8 * 8;  // whole 8-row swizzle atoms per box
+        q.x_box_bytes = static_cast<uint32_t>(q.x_box) * row_bytes;
+        q.x_bytes = (q.x_nbox * q.x_box_bytes + 1023) / 1024 * 1024;
+        p.ub[i] = p.units;
+        p.gb[i] = p.n_rg;
+        p.units += q.n_rp * q.n_st;
+        p.n_rg += q.n_rp;
+        p.x_bytes = q.x_bytes > p.x_bytes ? q.x_bytes : p.x_bytes;
+        p.c_rows = q.c_rows > p.c_rows ? q.c_rows : p.c_rows;
+    }
+    p.ub[n] = p.units;
+    p.gb[n] = p.n_rg;
+    p.grid = p.units < num_sms() ? p.units : num_sms();
     p.slot_bytes = (kABytes + p.x_bytes + p.c_rows * kCRow + 1023) / 1024 * 1024;
     const size_t fixed = static_cast<size_t>(kMB) * kMBoxBytes + 2 * static_cast<size_t>(kRowsU) * p.tp * 4 +
                          (2 * 16 + 2 * kMB + 4) * 8 + 64;
@@ -576,32 +642,34 @@ StPlan make_plan(const vnm_geom& g, int32_t T, int64_t ldx = 0) {
     // keeps a warp ~0.4 us busy against the producer's ~0.5 us per unit, profiles/r02c_trace_up.txt).
     {
         int best_s = 0, best_n = 1;
-        for (int n = kPhases; n >= 2; --n)
-            if (p.S - p.S % n > best_s) {
-                best_s = p.S - p.S % n;
-                best_n = n;
+        for (int k = kPhases; k >= 2; --k)
+            if (p.S - p.S % k > best_s) {
+                best_s = p.S - p.S % k;
+                best_n = k;
             }
         p.nph = best_n;
         p.S = best_s;
     }
     p.smem = static_cast<size_t>(p.S) * p.slot_bytes + fixed;
     p.maxseg = 1;
-    for (int rp = 0; rp < p.n_rp; ++rp) {
-        const long long x0 = static_cast<long long>(rp) * p.n_st, x1 = x0 + p.n_st - 1;
-        const int o0 = static_cast<int>(((x0 + 1) * p.grid - 1) / p.units);
-        const int o1 = static_cast<int>(((x1 + 1) * p.grid - 1) / p.units);
-        if (o1 - o0 + 1 > p.maxseg) p.maxseg = o1 - o0 + 1;
-    }
-    p.ws_bytes = kTicketWords * 4 + static_cast<size_t>(p.n_rp) * p.maxseg * kRowsU * p.tp * 4;
+    for (int i = 0; i < n; ++i)
+        for (int rp = 0; rp < p.pr[i].n_rp; ++rp) {
+            const long long x0 = p.ub[i] + static_cast<long long>(rp) * p.pr[i].n_st, x1 = x0 + p.pr[i].n_st - 1;
+            const int o0 = static_cast<int>(((x0 + 1) * p.grid - 1) / p.units);
+            const int o1 = static_cast<int>(((x1 + 1) * p.grid - 1) / p.units);
+            if (o1 - o0 + 1 > p.maxseg) p.maxseg = o1 - o0 + 1;
+        }
+    p.ws_bytes = kTicketWords * 4 + static_cast<size_t>(p.n_rg) * p.maxseg * kRowsU * p.tp * 4;
+    p.ok = p.S >= 2 && p.n_rg <= static_cast<int>(kTicketWords);
     return p;
 }
 
 template <int NT8, int VSET>
-int launch_nt(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUtensorMap* tm, cudaStream_t st) {
-    auto k = L.y_dtype == VNM_BF16 ? vnm_spmm_smallt_kernel<NT8, VSET, true> : vnm_spmm_smallt_kernel<NT8, VSET, false>;
+int launch_nt(vnm_dtype y_dtype, const StPlan& p, const StArgs& a, const StMaps& maps, cudaStream_t st) {
+    auto k = y_dtype == VNM_BF16 ? vnm_spmm_smallt_kernel<NT8, VSET, true> : vnm_spmm_smallt_kernel<NT8, VSET, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)) != cudaSuccess)
         return kLaunchCudaError;
-    cudaError_t e = launch_pdl(true, k, dim3(p.grid), dim3(kThreads), p.smem, st, tm[0], tm[1], tm[2], tm[3], a);
+    cudaError_t e = launch_pdl(true, k, dim3(a.grid), dim3(kThreads), p.smem, st, maps, a);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && a.trace) {
@@ -609,7 +677,7 @@ int launch_nt(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUten
         cudaStreamSynchronize(st);
         cudaMemcpyFromSymbol(h, g_st_t, sizeof(h));
         unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0}, mn[4] = {~0ull, ~0ull, ~0ull, ~0ull};
-        const int n = p.grid < 1024 ? p.grid : 1024;
+        const int n = a.grid < 1024 ? a.grid : 1024;
         for (int i = 0; i < n; ++i) t0 = h[0][i] < t0 ? h[0][i] : t0;
         for (int j = 0; j < 4; ++j)
             for (int i = 0; i < n; ++i) {
@@ -618,14 +686,14 @@ int launch_nt(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUten
                 mn[j] = v < mn[j] ? v : mn[j];
             }
         fprintf(stderr, "smallt grid %d S %d units %d slot %u B: entry %llu..%llu  prologue %llu..%llu  first %llu..%llu  "
-                        "done %llu..%llu ns\n", p.grid, p.S, p.units, p.slot_bytes, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2],
+                        "done %llu..%llu ns\n", a.grid, p.S, p.units, p.slot_bytes, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2],
                 mn[3], mx[3]);
         if (a.trace == 2) {
             static unsigned long long u[160][32][4];
             cudaMemcpyFromSymbol(u, g_st_u, sizeof(u));
             for (int i = 0; i < n && i < 160; ++i) {
-                const int nu = static_cast<int>(static_cast<long long>(i + 1) * p.units / p.grid -
-                                                static_cast<long long>(i) * p.units / p.grid);
+                const int nu = static_cast<int>(static_cast<long long>(i + 1) * p.units / a.grid -
+                                                static_cast<long long>(i) * p.units / a.grid);
                 fprintf(stderr, "cta %3d done %6llu:", i, h[3][i] - t0);
                 for (int q = 0; q < nu && q < 32; ++q)
                     fprintf(stderr, " [%llu %llu %llu %llu]", (u[i][q][0] - t0) / 10, (u[i][q][3] - t0) / 10,
@@ -638,101 +706,129 @@ int launch_nt(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUten
 }
 
 template <int VSET>
-int launch_v(const SpmmLaunch& L, const StPlan& p, const StArgs& a, const CUtensorMap* tm, cudaStream_t st) {
-    const int nt8 = (L.T + 7) / 8;
-    if (nt8 <= 1) return launch_nt<1, VSET>(L, p, a, tm, st);
-    if (nt8 == 2) return launch_nt<2, VSET>(L, p, a, tm, st);
-    if (nt8 == 3) return launch_nt<3, VSET>(L, p, a, tm, st);
-    return launch_nt<4, VSET>(L, p, a, tm, st);
+int launch_v(int32_t T, vnm_dtype y_dtype, const StPlan& p, const StArgs& a, const StMaps& maps, cudaStream_t st) {
+    const int nt8 = (T + 7) / 8;
+    if (nt8 <= 1) return launch_nt<1, VSET>(y_dtype, p, a, maps, st);
+    if (nt8 == 2) return launch_nt<2, VSET>(y_dtype, p, a, maps, st);
+    if (nt8 == 3) return launch_nt<3, VSET>(y_dtype, p, a, maps, st);
+    return launch_nt<4, VSET>(y_dtype, p, a, maps, st);
+}
+
+StPlan plan_of(const SpmmLaunch* Ls, int n, bool use_ldx) {
+    const vnm_geom* gs[kMaxProb] = {};
+    int64_t lx[kMaxProb] = {};
+    if (n < 1 || n > kMaxProb) return StPlan{};
+    for (int i = 0; i < n; ++i) {
+        gs[i] = &Ls[i].P->g;
+        lx[i] = use_ldx ? Ls[i].ldx : 0;
+        if (Ls[i].T != Ls[0].T || Ls[i].y_dtype != Ls[0].y_dtype) return StPlan{};
+    }
+    return make_plan(gs, lx, n, Ls[0].T);
 }
 
 }  // namespace
 
 bool spmm_smallt_applies(const vnm_geom& g, int32_t T) {
     if (T < 1 || T > 32 || g.V < 16 || g.nb_pad == 0) return false;
-    const StPlan p = make_plan(g, T);
-    return p.S >= 2 && p.n_rp <= static_cast<int>(kTicketWords);
+    const vnm_geom* gs[1] = {&g};
+    return make_plan(gs, nullptr, 1, T).ok;
 }
 
 size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T) {
-    return spmm_smallt_applies(g, T) ? make_plan(g, T).ws_bytes : 0;
+    const vnm_geom* gs[1] = {&g};
+    return spmm_smallt_applies(g, T) ? make_plan(gs, nullptr, 1, T).ws_bytes : 0;
 }
 
-int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) {
-    const vnm_geom& g = L.P->g;
-    if (!spmm_smallt_applies(g, L.T)) return kLaunchUnsupported;
-    const StPlan p = make_plan(g, L.T, L.ldx);
+bool spmm_smallt_batch_applies(const vnm_geom* const* gs, int n, int32_t T) {
+    if (n < 1 || n > kMaxProb) return false;
+    for (int i = 0; i < n; ++i)
+        if (!spmm_smallt_applies(*gs[i], T)) return false;
+    return make_plan(gs, nullptr, n, T).ok;
+}
+
+size_t spmm_smallt_batch_workspace_bytes(const vnm_geom* const* gs, int n, int32_t T) {
+    return spmm_smallt_batch_applies(gs, n, T) ? make_plan(gs, nullptr, n, T).ws_bytes : 0;
+}
+
+int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, cudaStream_t stream) {
+    const StPlan p = plan_of(Ls, n, true);
+    if (!p.ok) return kLaunchUnsupported;
+    for (int i = 0; i < n; ++i)
+        if (!spmm_smallt_applies(Ls[i].P->g, Ls[i].T)) return kLaunchUnsupported;
+    const SpmmLaunch& L0 = Ls[0];
     StArgs a{};
     // without a workspace (or a too small one) every CTA takes whole row groups: nothing is cut, no tickets
-    a.rg_mode = (!L.workspace || L.workspace_bytes < p.ws_bytes) ? 1 : 0;
-    StPlan q = p;
-    if (a.rg_mode) q.grid = p.n_rp < num_sms() ? p.n_rp : num_sms();
-    a.YT = L.YT;
-    a.ldy = L.ldy;
-    a.tickets = a.rg_mode ? nullptr : static_cast<uint32_t*>(L.workspace);
-    a.ws = a.rg_mode ? nullptr : reinterpret_cast<float*>(static_cast<uint8_t*>(L.workspace) + kTicketWords * 4);
-    a.T = L.T;
-    a.y_bf16 = L.y_dtype == VNM_BF16;
-    a.rows = g.rows;
-    a.rows_p = g.rows_p;
-    a.V = g.V;
-    a.M = g.M;
-    a.n_ks = p.n_ks;
-    a.n_st = p.n_st;
-    a.n_rp = p.n_rp;
+    a.rg_mode = (!L0.workspace || L0.workspace_bytes < p.ws_bytes) ? 1 : 0;
+    a.grid = a.rg_mode ? (p.n_rg < num_sms() ? p.n_rg : num_sms()) : p.grid;
+    a.tickets = a.rg_mode ? nullptr : static_cast<uint32_t*>(L0.workspace);
+    a.ws = a.rg_mode ? nullptr : reinterpret_cast<float*>(static_cast<uint8_t*>(L0.workspace) + kTicketWords * 4);
+    a.T = L0.T;
     a.units = p.units;
-    a.grid = q.grid;
+    a.n_rg = p.n_rg;
     a.maxseg = p.maxseg;
+    a.n_prob = n;
+    for (int i = 0; i <= n; ++i) {
+        a.ub[i] = p.ub[i];
+        a.gb[i] = p.gb[i];
+    }
     a.S = p.S;
     a.nph = p.nph;
-    a.c_rows = p.c_rows;
-    a.x_rows = p.x_rows;
-    a.x_pack = p.x_pack;
-    a.x_l8 = static_cast<int32_t>(L.ldx / 8);
-    a.x_pack_log2 = p.x_pack == 8 ? 3 : p.x_pack == 4 ? 2 : p.x_pack == 2 ? 1 : 0;
-    a.x_box = p.x_box;
-    a.x_nbox = p.x_nbox;
-    a.x_box_bytes = p.x_box_bytes;
     a.x_bytes = p.x_bytes;
     a.slot_bytes = p.slot_bytes;
-    a.c_bytes = p.c_rows * kCRow;
-    a.tx_bytes = kABytes + static_cast<uint32_t>(p.x_nbox) * p.x_box_bytes + a.c_bytes;
-    a.XT = L.XT;
-    a.meta = L.P->meta;
-    a.col_idx = L.P->col_idx;
-    a.ldx = L.ldx;
-    a.cols = g.cols;
-    a.ld_meta = g.ld_meta;
-    a.nb_pad = g.nb_pad;
-    a.n_vb = g.rows_p / g.V;
     a.trace = VNM_ENV_INT("VNM_SPMM_TRACE", 0);
     a.abl = VNM_ABLATION_FLAGS();
-    // A_n [rows_p][ld_val] bf16, boxes [128 rows][64 values]; X^T as lines of x_pack channels [cols / x_pack][64]
-    // (SW128) or [cols][T] (boxes TP wide, 32B / 64B swizzle).  Past an edge boxes are zero-filled (rows past
-    // rows_p, pad k-steps, channels past cols, tokens past T).
-    CUtensorMap tm[4];
-    const CUtensorMapSwizzle xsw = p.x_pack > 1 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                  : (p.tp == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
-                                               : (p.tp == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B));
-    const bool okx = p.x_pack > 1
-        ? encode_2d(&tm[1], L.XT, 64, static_cast<uint64_t>(g.cols / p.x_pack), 128, 64, static_cast<uint32_t>(p.x_box),
-                    CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw)
-        : encode_2d(&tm[1], L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
-                    static_cast<uint32_t>(p.tp), static_cast<uint32_t>(p.x_box), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw);
-    // A_i2 [rows_p][ld_meta] u32, boxes [128 rows][32 words] (SW128; past n_ks: zero, never read); A_i1 as u32
-    // [rows_p / V][nb_pad], boxes [c_rows][32 words]
-    if (!okx || !encode_2d(&tm[0], L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
-                           static_cast<uint64_t>(g.ld_val) * 2, 64, kRowsU) ||
-        !encode_2d(&tm[2], L.P->meta, static_cast<uint64_t>(g.ld_meta), static_cast<uint64_t>(g.rows_p),
-                   static_cast<uint64_t>(g.ld_meta) * 4, 32, kRowsU, CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_2d(&tm[3], L.P->col_idx, static_cast<uint64_t>(g.nb_pad), static_cast<uint64_t>(g.rows_p / g.V),
-                   static_cast<uint64_t>(g.nb_pad) * 4, kBlkU, static_cast<uint32_t>(p.c_rows), CU_TENSOR_MAP_DATA_TYPE_UINT32,
-                   CU_TENSOR_MAP_SWIZZLE_NONE))
-        return kLaunchCudaError;
-    const int vset = g.V >= 64 ? 1 : 64 / g.V;
-    if (vset == 1) return launch_v<1>(L, q, a, tm, stream);
-    if (vset == 2) return launch_v<2>(L, q, a, tm, stream);
-    return launch_v<4>(L, q, a, tm, stream);
+    StMaps maps;
+    for (int i = 0; i < n; ++i) {
+        const SpmmLaunch& L = Ls[i];
+        const vnm_geom& g = L.P->g;
+        const StProbPlan& q = p.pr[i];
+        StProb& pr = a.pr[i];
+        pr.YT = L.YT;
+        pr.ldy = L.ldy;
+        pr.rows = g.rows;
+        pr.rows_p = g.rows_p;
+        pr.V = g.V;
+        pr.M = g.M;
+        pr.n_st = q.n_st;
+        pr.n_rp = q.n_rp;
+        pr.c_rows = q.c_rows;
+        pr.x_pack = q.x_pack;
+        pr.x_l8 = static_cast<int32_t>(L.ldx / 8);
+        pr.x_pack_log2 = q.x_pack == 8 ? 3 : q.x_pack == 4 ? 2 : q.x_pack == 2 ? 1 : 0;
+        pr.x_box = q.x_box;
+        pr.x_nbox = q.x_nbox;
+        pr.x_box_bytes = q.x_box_bytes;
+        pr.c_bytes = q.c_rows * kCRow;
+        pr.tx_bytes = kABytes + static_cast<uint32_t>(q.x_nbox) * q.x_box_bytes + pr.c_bytes;
+        // A_n [rows_p][ld_val] bf16, boxes [128 rows][64 values]; X^T as lines of x_pack channels [cols / x_pack][64]
+        // (SW128) or [cols][T] (boxes TP wide, 32B / 64B swizzle).  Past an edge boxes are zero-filled (rows past
+        // rows_p, pad k-steps, channels past cols, tokens past T).
+        CUtensorMap* tm = maps.m[i];
+        const CUtensorMapSwizzle xsw = q.x_pack > 1 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                      : (p.tp == 8 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                                   : (p.tp == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B));
+        const bool okx = q.x_pack > 1
+            ? encode_2d(&tm[1], L.XT, 64, static_cast<uint64_t>(g.cols / q.x_pack), 128, 64, static_cast<uint32_t>(q.x_box),
+                        CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw)
+            : encode_2d(&tm[1], L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), static_cast<uint64_t>(L.ldx) * 2,
+                        static_cast<uint32_t>(p.tp), static_cast<uint32_t>(q.x_box), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xsw);
+        // A_i2 [rows_p][ld_meta] u32, boxes [128 rows][32 words] (SW128; past n_ks: zero, never read); A_i1 as u32
+        // [rows_p / V][nb_pad], boxes [c_rows][32 words]
+        if (!okx || !encode_2d(&tm[0], L.P->values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
+                               static_cast<uint64_t>(g.ld_val) * 2, 64, kRowsU) ||
+            !encode_2d(&tm[2], L.P->meta, static_cast<uint64_t>(g.ld_meta), static_cast<uint64_t>(g.rows_p),
+                       static_cast<uint64_t>(g.ld_meta) * 4, 32, kRowsU, CU_TENSOR_MAP_DATA_TYPE_UINT32, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !encode_2d(&tm[3], L.P->col_idx, static_cast<uint64_t>(g.nb_pad), static_cast<uint64_t>(g.rows_p / g.V),
+                       static_cast<uint64_t>(g.nb_pad) * 4, kBlkU, static_cast<uint32_t>(q.c_rows), CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                       CU_TENSOR_MAP_SWIZZLE_NONE))
+            return kLaunchCudaError;
+    }
+    const int vset = L0.P->g.V >= 64 ? 1 : 64 / L0.P->g.V;
+    if (vset == 1) return launch_v<1>(L0.T, L0.y_dtype, p, a, maps, stream);
+    if (vset == 2) return launch_v<2>(L0.T, L0.y_dtype, p, a, maps, stream);
+    return launch_v<4>(L0.T, L0.y_dtype, p, a, maps, stream);
 }
+
+int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) { return launch_spmm_smallt_batch(&L, 1, stream); }
 
 }  // namespace vnm

@@ -74,6 +74,11 @@ size_t spmm_workspace_bytes(const vnm_geom& g, int32_t T);
 bool spmm_smallt_applies(const vnm_geom& g, int32_t T);
 size_t spmm_smallt_workspace_bytes(const vnm_geom& g, int32_t T);
 int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream);
+// n (<= 4) independent problems of one T, y dtype and V class in ONE launch (vnm_spmm_batched); the workspace of
+// Ls[0] serves the launch
+bool spmm_smallt_batch_applies(const vnm_geom* const* gs, int n, int32_t T);
+size_t spmm_smallt_batch_workspace_bytes(const vnm_geom* const* gs, int n, int32_t T);
+int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, cudaStream_t stream);
 
 // RIA importance (ria.cu)
 size_t ria_workspace_bytes(int32_t rows, int32_t cols);

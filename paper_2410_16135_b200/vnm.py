@@ -49,7 +49,8 @@ _lib = None
 
 EXPORTS = ["vnm_geometry", "vnm_bytes", "vnm_prune", "vnm_compress", "vnm_prune_compress",
            "vnm_prune_compress_batched", "vnm_pack_tc",
-           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_spmm_workspace_init", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
+           "vnm_spmm", "vnm_spmm_workspace_bytes", "vnm_spmm_workspace_init", "vnm_spmm_batched",
+           "vnm_spmm_batched_workspace_bytes", "vnm_act_norms", "vnm_ria_workspace_bytes", "vnm_ria_score",
            "vnm_permute_gain_workspace_bytes", "vnm_permute_gain", "vnm_permute_gain_out", "vnm_status_string",
            "vnm_launch_count"]
 
@@ -85,6 +86,10 @@ def lib():
             L.vnm_spmm_workspace_bytes.restype = sz
             L.vnm_spmm_workspace_init.argtypes = [P, sz, P]
             L.vnm_spmm_workspace_init.restype = ctypes.c_int
+            L.vnm_spmm_batched.argtypes = [i32, P, P, i32, P, P, P, ctypes.c_int, P, sz, P]
+            L.vnm_spmm_batched.restype = ctypes.c_int
+            L.vnm_spmm_batched_workspace_bytes.argtypes = [i32, P, i32]
+            L.vnm_spmm_batched_workspace_bytes.restype = sz
             L.vnm_act_norms.argtypes = [P, i64, i32, i32, P, P]
             L.vnm_act_norms.restype = ctypes.c_int
             L.vnm_ria_workspace_bytes.argtypes = [i32, i32]
@@ -314,6 +319,62 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
     _check(lib().vnm_spmm(_ptr(XT), XT.stride(0), T, ctypes.byref(cp), _ptr(out), out.stride(0), ydt, ws_ptr,
                           ws_bytes, _stream(XT.device)), "vnm_spmm")
     return out
+
+
+def spmm_batched(XTs: list, Ps: list, T: int, outs: list | None = None, out_dtype: torch.dtype = torch.float32,
+                 workspace: torch.Tensor | None = None) -> list:
+    """vnm_spmm_batched: Y_i^T = W'_i X_i^T for independent problems sharing T (up to 4 small-T problems per
+    launch).  XTs[i]: bf16 [cols_i][ldx_i]; returns the list of Y_i^T (or writes into outs[i])."""
+    n = len(Ps)
+    if len(XTs) != n or (outs is not None and len(outs) != n):
+        raise ValueError("XTs, Ps (and outs) must have the same length")
+    XTs = [_as_bits16(X) for X in XTs]
+    _require_cuda(*XTs, *(outs or []), workspace)
+    dev = XTs[0].device
+    if outs is None:
+        ldy = (T + 7) // 8 * 8
+        outs = [torch.empty((P.g.rows, ldy), dtype=out_dtype, device=dev)[:, :T] for P in Ps]
+    for X, P, Y in zip(XTs, Ps, outs):
+        _ld(X)
+        _ld(Y)
+        if X.shape[0] != P.g.cols or not 0 <= T <= X.shape[1]:
+            raise ValueError(f"XT {tuple(X.shape)} does not fit the weight ({P.g.cols} channels) and T = {T}")
+        if Y.shape[0] < P.g.rows or Y.shape[1] < T:
+            raise ValueError(f"out is {tuple(Y.shape)}, needs at least ({P.g.rows}, {T})")
+        if X.device != dev or Y.device != dev:
+            raise ValueError("every XT / out must be on the same device")
+        if Y.dtype != outs[0].dtype or Y.dtype not in (torch.bfloat16, torch.float32):
+            raise TypeError("Y^T must be fp32 or bf16, the same for every problem")
+    if workspace is None:
+        workspace = spmm_batched_workspace([P.g for P in Ps], T, dev)
+    ws_ptr, ws_bytes = (_ptr(workspace), workspace.numel() * workspace.element_size()) if workspace is not None \
+        else (None, 0)
+    cps = [P.c() for P in Ps]
+    arr = lambda ty, xs: (ty * n)(*xs)
+    ydt = VNM_BF16 if outs[0].dtype == torch.bfloat16 else VNM_F32
+    _check(lib().vnm_spmm_batched(n, arr(ctypes.c_void_p, [_ptr(X) for X in XTs]),
+                                  arr(ctypes.c_int64, [X.stride(0) for X in XTs]), T,
+                                  arr(ctypes.c_void_p, [ctypes.cast(ctypes.pointer(cp), ctypes.c_void_p) for cp in cps]),
+                                  arr(ctypes.c_void_p, [_ptr(Y) for Y in outs]),
+                                  arr(ctypes.c_int64, [Y.stride(0) for Y in outs]), ydt, ws_ptr, ws_bytes,
+                                  _stream(dev)), "vnm_spmm_batched")
+    return outs
+
+
+def spmm_batched_workspace_bytes(gs: list, T: int) -> int:
+    n = len(gs)
+    arr = (ctypes.c_void_p * n)(*[ctypes.cast(ctypes.pointer(g), ctypes.c_void_p) for g in gs])
+    return int(lib().vnm_spmm_batched_workspace_bytes(n, arr, T))
+
+
+def spmm_batched_workspace(gs: list, T: int, device) -> torch.Tensor | None:
+    """An initialised workspace for vnm_spmm_batched over geometries gs at T (None if not used)."""
+    nws = spmm_batched_workspace_bytes(gs, T)
+    if not nws:
+        return None
+    ws = torch.empty(max(nws, 16) // 4, dtype=torch.float32, device=device)
+    _check(lib().vnm_spmm_workspace_init(_ptr(ws), ws.numel() * 4, _stream(device)), "vnm_spmm_workspace_init")
+    return ws
 
 
 def spmm_workspace_bytes(g: Geom, T: int) -> int:

@@ -19,17 +19,26 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(4096, 4096), (11008, 4096), (4096, 11008)]
 
 
-@pytest.mark.parametrize("V,M,T", [(64, 5, 16), (64, 8, 16), (128, 8, 16), (128, 13, 32)])
-def test_decode_step_graph_replays_stay_bit_identical(V, M, T):
-    """(128:2:13 at T = 32: only 3 ring slots fit, so 3 of the 4 consumer phases take units.)"""
+@pytest.mark.parametrize("V,M,T,batched", [(64, 5, 16, False), (64, 8, 16, False), (128, 8, 16, False),
+                                           (128, 13, 32, False), (64, 5, 16, True), (128, 13, 32, True)])
+def test_decode_step_graph_replays_stay_bit_identical(V, M, T, batched):
+    """(128:2:13 at T = 32: only 3 ring slots fit, so 3 of the 4 consumer phases take units.)  batched: the three
+    SpMMs as one vnm_spmm_batched launch (one workspace)."""
     replays, every = 2000, 250
     Ws = [to_dev_bf16(synth.weights(r, c, seed=r + c, kind="outlier")) for r, c in SHAPES]
     Xs = [to_dev_bf16(synth.activations_t(c, T, seed=c)) for r, c in SHAPES]
     Ps = vnm.prune_compress_batched(Ws, V, M)
     Ys = [torch.empty((r, T), dtype=torch.bfloat16, device="cuda") for r, _ in SHAPES]
     wss = [vnm.spmm_workspace(P.g, T, "cuda") for P in Ps]
-    for X, P, Y, ws in zip(Xs, Ps, Ys, wss):
-        vnm.spmm(X, P, T=T, out=Y, workspace=ws)
+    wsb = vnm.spmm_batched_workspace([P.g for P in Ps], T, "cuda")
+
+    def spmms():
+        if batched:
+            vnm.spmm_batched(Xs, Ps, T, outs=Ys, workspace=wsb)
+        else:
+            for X, P, Y, ws in zip(Xs, Ps, Ys, wss):
+                vnm.spmm(X, P, T=T, out=Y, workspace=ws)
+    spmms()
     torch.cuda.synchronize()
     ref = [Y.clone() for Y in Ys]
 
@@ -43,8 +52,7 @@ def test_decode_step_graph_replays_stay_bit_identical(V, M, T):
         st = vnm.lib().vnm_prune_compress_batched(n, b_w, b_lw, None, None, b_po, None,
                                                   ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
         assert st == 0
-        for X, P, Y, ws in zip(Xs, Ps, Ys, wss):
-            vnm.spmm(X, P, T=T, out=Y, workspace=ws)
+        spmms()
     bad = []
     for i in range(replays):
         g.replay()
