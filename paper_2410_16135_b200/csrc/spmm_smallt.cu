@@ -64,7 +64,7 @@ constexpr int kMB = VNM_ST_MB;                       // A_i2 box ring slots
 constexpr uint32_t kCRow = kBlkU * 4;        // A_i1 words of one V-block and unit (128 B)
 
 // VNM_SPMM_TRACE: %globaltimer per CTA — entry, after the prologue, first unit landed, consumers done, exit
-__device__ unsigned long long g_st_t[5][1024];
+__device__ unsigned long long g_st_t[9][1024];  // [4..8]: last piece: reduced, ticket checked, published, folded, stored
 __device__ unsigned long long g_st_u[160][32][4];  // VNM_SPMM_TRACE=2: per unit: slot free, landed, consumed, issued
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -118,19 +118,21 @@ __device__ __forceinline__ int prob_of(const StArgs& a, int u) {  // problem hol
         if (k < a.n_prob && u >= a.ub[k]) i = k;
     return i;
 }
+// (32-bit unsigned arithmetic: the host keeps units x grid and row groups x grid below 2^32; a 64-bit division is a
+// ~0.3 us software routine on the tail's critical path)
 __device__ __forceinline__ int unit_owner(const StArgs& a, int u) {  // CTA whose share contains unit u
-    return static_cast<int>((static_cast<long long>(u + 1) * a.grid - 1) / a.units);
+    return static_cast<int>((static_cast<uint32_t>(u + 1) * static_cast<uint32_t>(a.grid) - 1u) / static_cast<uint32_t>(a.units));
 }
 __device__ __forceinline__ int share_begin(const StArgs& a, int b) {  // first unit of CTA b's share
     if (a.rg_mode) {  // whole row groups: the first unit of launch-wide row group G
-        const int G = static_cast<int>(static_cast<long long>(b) * a.n_rg / a.grid);
+        const int G = static_cast<int>(static_cast<uint32_t>(b) * static_cast<uint32_t>(a.n_rg) / static_cast<uint32_t>(a.grid));
         int i = 0;
 #pragma unroll
         for (int k = 1; k < kMaxProb; ++k)
             if (k < a.n_prob && G >= a.gb[k]) i = k;
         return G >= a.n_rg ? a.units : a.ub[i] + (G - a.gb[i]) * a.pr[i].n_st;
     }
-    return static_cast<int>(static_cast<long long>(b) * a.units / a.grid);
+    return static_cast<int>(static_cast<uint32_t>(b) * static_cast<uint32_t>(a.units) / static_cast<uint32_t>(a.grid));
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -177,6 +179,8 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int pi, int rp, in
         else asm volatile("bar.sync 1, %0;" ::"n"(kNthr) : "memory");
     };
     constexpr int kN4 = kRowsU * TP / 4;  // float4 groups of a piece
+    const bool tr = kNthr > 32 && a.trace && tid == 0 && blockIdx.x < 1024;
+    if (tr) g_st_t[4][blockIdx.x] = gtime();
     const StProb& pp = a.pr[pi];
     const int row0 = rp * kRowsU;
     const int rg_u0 = a.ub[pi] + rp * pp.n_st;  // the row group's first (launch-wide) unit
@@ -188,15 +192,12 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int pi, int rp, in
         const int nseg = unit_owner(a, rg_u0 + pp.n_st - 1) - own0 + 1;
         const int me = static_cast<int>(blockIdx.x) - own0;
         float* wsr = a.ws + static_cast<int64_t>(G) * a.maxseg * kRowsU * TP;
-        // are all the other pieces in already (the ticket read when the piece began, else read once more now)?
-        // then this CTA is the last one and finishes without publishing its own piece; otherwise publish + count
-        if (tid == 0) {
-            uint32_t t = t_early;
-            if (t != ~0u && t != static_cast<uint32_t>(nseg - 1))
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(t) : "l"(a.tickets + G) : "memory");
-            flag = t == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
-        }
+        // were all the other pieces in already when this piece began (t_early, an acquire read then)?  Then this
+        // CTA is the last one and finishes without publishing its own piece; otherwise publish + count.  (No second
+        // read at the end: measured, that L2 round trip (~0.7 us) cost more on the publishing path than it saved.)
+        if (tid == 0) flag = t_early == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
         sync();
+        if (tr) g_st_t[5][blockIdx.x] = gtime();
         if (!flag) {
             float4* mine = reinterpret_cast<float4*>(wsr + static_cast<int64_t>(me) * kRowsU * TP);
             for (int i = tid; i < kN4; i += kNthr) __stcg(mine + i, red4[i]);
@@ -207,6 +208,7 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int pi, int rp, in
                 flag = old == static_cast<uint32_t>(nseg - 1) ? 1u : 0u;
             }
             sync();
+            if (tr) g_st_t[6][blockIdx.x] = gtime();
             if (!flag) return;  // an other CTA finishes the row group
         }
         // the last one: every piece, in the canonical order p_0 + (p_1 + (... + p_{nseg-1})) (this CTA's own from
@@ -255,6 +257,7 @@ __device__ __forceinline__ void finish_piece(const StArgs& a, int pi, int rp, in
                 if (i0 + k * kNthr < kN4) red4[i0 + k * kNthr] = sum[k];
         }
         sync();
+        if (tr) g_st_t[7][blockIdx.x] = gtime();
         if (tid == 0) a.tickets[G] = 0u;  // ready for the next launch (stream order)
     }
     // Y^T rows row0 .. +127, tokens [0, T): one 16-byte group (8 bf16 / 4 fp32 tokens) per thread and step
@@ -660,7 +663,8 @@ StPlan make_plan(const vnm_geom* const* gs, const int64_t* ldx, int n, int32_t T
             if (o1 - o0 + 1 > p.maxseg) p.maxseg = o1 - o0 + 1;
         }
     p.ws_bytes = kTicketWords * 4 + static_cast<size_t>(p.n_rg) * p.maxseg * kRowsU * p.tp * 4;
-    p.ok = p.S >= 2 && p.n_rg <= static_cast<int>(kTicketWords);
+    p.ok = p.S >= 2 && p.n_rg <= static_cast<int>(kTicketWords) &&
+           static_cast<uint64_t>(p.units + 1) * static_cast<uint64_t>(num_sms() + 1) < (1ull << 32);  // 32-bit share math
     return p;
 }
 
@@ -669,11 +673,15 @@ int launch_nt(vnm_dtype y_dtype, const StPlan& p, const StArgs& a, const StMaps&
     auto k = y_dtype == VNM_BF16 ? vnm_spmm_smallt_kernel<NT8, VSET, true> : vnm_spmm_smallt_kernel<NT8, VSET, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)) != cudaSuccess)
         return kLaunchCudaError;
+    if (a.trace) {  // the last-piece stamps are written only by the CTAs that reach them
+        void* sym = nullptr;
+        if (cudaGetSymbolAddress(&sym, g_st_t) == cudaSuccess) cudaMemsetAsync(sym, 0, sizeof(unsigned long long) * 9 * 1024, st);
+    }
     cudaError_t e = launch_pdl(true, k, dim3(a.grid), dim3(kThreads), p.smem, st, maps, a);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess && a.trace) {
-        static unsigned long long h[5][1024];
+        static unsigned long long h[9][1024];
         cudaStreamSynchronize(st);
         cudaMemcpyFromSymbol(h, g_st_t, sizeof(h));
         unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0}, mn[4] = {~0ull, ~0ull, ~0ull, ~0ull};
@@ -694,7 +702,8 @@ int launch_nt(vnm_dtype y_dtype, const StPlan& p, const StArgs& a, const StMaps&
             for (int i = 0; i < n && i < 160; ++i) {
                 const int nu = static_cast<int>(static_cast<long long>(i + 1) * p.units / a.grid -
                                                 static_cast<long long>(i) * p.units / a.grid);
-                fprintf(stderr, "cta %3d done %6llu:", i, h[3][i] - t0);
+                auto rel = [&](int j) { return h[j][i] ? (h[j][i] - t0) / 10 : 0ull; };
+                fprintf(stderr, "cta %3d done %6llu fin [%llu %llu %llu %llu]:", i, h[3][i] - t0, rel(4), rel(5), rel(6), rel(7));
                 for (int q = 0; q < nu && q < 32; ++q)
                     fprintf(stderr, " [%llu %llu %llu %llu]", (u[i][q][0] - t0) / 10, (u[i][q][3] - t0) / 10,
                             (u[i][q][1] - t0) / 10, (u[i][q][2] - t0) / 10);
