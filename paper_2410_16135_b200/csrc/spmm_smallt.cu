@@ -351,12 +351,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             // share) on, in a ring of kMB boxes; box k is issued with the first unit that reads it
             int k = 0, pend = u0;  // next box; first unit past the last issued box
             int pi = prob_of(a, u0);
-            const StProb* pp = &a.pr[pi];
             const CUtensorMap* tm = maps.m[pi];
-            int rp = (u0 - a.ub[pi]) / pp->n_st, st = u0 - a.ub[pi] - rp * pp->n_st, s = 0, par = 0;  // (incremental)
+            // the problem's fields in registers (re-read only at a problem switch: param-space loads through a
+            // dynamic index are on the issue path of every unit otherwise)
+            int n_st, n_rp, M, xpl2, x_nbox, x_box, V, ub;
+            uint32_t tx, c_bytes, xbb;
+            auto load_prob = [&](int i) {
+                const StProb& q = a.pr[i];
+                n_st = q.n_st; n_rp = q.n_rp; M = q.M; xpl2 = q.x_pack_log2; x_nbox = q.x_nbox; x_box = q.x_box;
+                V = q.V; tx = q.tx_bytes; c_bytes = q.c_bytes; xbb = q.x_box_bytes; ub = a.ub[i];
+            };
+            load_prob(pi);
+            int rp = (u0 - ub) / n_st, st = u0 - ub - rp * n_st, s = 0, par = 0;  // (incremental)
             for (int u = u0, q = 0; u < u1; ++u, ++q) {
                 if (u == pend) {
-                    const int pu1 = min(u1, a.ub[pi] + (rp + 1) * pp->n_st);
+                    const int pu1 = min(u1, ub + (rp + 1) * n_st);
                     const int ms = k % kMB;
                     mbar_wait(&mempty[ms], ((k / kMB) & 1) ^ 1);
                     mbar_arrive_expect_tx(&mfull[ms], kMBoxBytes);
@@ -367,23 +376,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&empty[s], par ^ 1);
                 if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][0] = gtime();
                 uint8_t* base = slots + s * a.slot_bytes;
-                mbar_arrive_expect_tx(&full[s], (a.abl & 2) ? kABytes + pp->c_bytes : pp->tx_bytes);
+                mbar_arrive_expect_tx(&full[s], (a.abl & 2) ? kABytes + c_bytes : tx);
                 tma_load_2d(base, &tm[0], st * 2 * kBlkU, rp * kRowsU, &full[s]);
-                const int y0 = (st * kBlkU * pp->M) >> pp->x_pack_log2;  // first row of the slice in the X^T view
-                for (int b = 0; b < ((a.abl & 2) ? 0 : pp->x_nbox); ++b)
-                    tma_load_2d(base + kABytes + b * pp->x_box_bytes, &tm[1], 0, y0 + b * pp->x_box, &full[s]);
-                tma_load_2d(base + kABytes + a.x_bytes, &tm[3], st * kBlkU, (rp * kRowsU) / pp->V, &full[s]);
+                const int y0 = (st * kBlkU * M) >> xpl2;  // first row of the slice in the X^T view
+                for (int b = 0; b < ((a.abl & 2) ? 0 : x_nbox); ++b)
+                    tma_load_2d(base + kABytes + b * xbb, &tm[1], 0, y0 + b * x_box, &full[s]);
+                tma_load_2d(base + kABytes + a.x_bytes, &tm[3], st * kBlkU, (rp * kRowsU) / V, &full[s]);
                 if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][3] = gtime();
                 if (++s == a.S) {
                     s = 0;
                     par ^= 1;
                 }
-                if (++st == pp->n_st) {
+                if (++st == n_st) {
                     st = 0;
-                    if (++rp == pp->n_rp && u + 1 < u1) {  // next problem
+                    if (++rp == n_rp && u + 1 < u1) {  // next problem
                         rp = 0;
                         ++pi;
-                        pp = &a.pr[pi];
+                        load_prob(pi);
                         tm = maps.m[pi];
                     }
                 }
