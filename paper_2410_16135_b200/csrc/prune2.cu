@@ -84,13 +84,15 @@ constexpr int kMaxBatch = 8;
 struct Batch {
     int32_t n;
     int32_t tile0[kMaxBatch + 1];
-    int32_t any_score, any_mask;
+    int32_t any_score, any_mask, any_tc;
     Maps tm[kMaxBatch];
     Prune2Args a[kMaxBatch];
 };
 
-template <int V, int M, int NW>
-__global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const __grid_constant__ Batch B) {
+// MINB: CTAs per SM the register budget is sized for (8-warp CTAs: 3, or 4 when no window form is written —
+// the window-form staging is then not allocated and 4 CTAs fit in shared memory)
+template <int V, int M, int NW, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_constant__ Batch B) {
     constexpr int kWarps = NW, kThreads = 32 * NW;
     constexpr int TC = kCB * M;  // tile columns (<= 256)
     constexpr int P = TC / 2;    // words per W row in shared memory
@@ -102,8 +104,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
     // two tile buffers (W [+ score]) for the TMA double buffer, the output staging, then the scratch
     const uint32_t buf_bytes = kWBytes + (B.any_score ? kSBytes : 0);
     uint32_t* sVal = reinterpret_cast<uint32_t*>(smem + 2 * buf_bytes);    // [V][kCB] A_n pairs
-    uint2* sTcv = reinterpret_cast<uint2*>(sVal + V * kCB);                 // [V][kCB] window values (M > 4)
-    uint32_t* sMet = reinterpret_cast<uint32_t*>(sTcv + V * kCB);           // [V][4] A_i2 words
+    uint2* sTcv = reinterpret_cast<uint2*>(sVal + V * kCB);                 // [V][kCB] window values (M > 4; any_tc)
+    uint32_t* sMet = reinterpret_cast<uint32_t*>(sTcv + (B.any_tc ? V * kCB : 0));  // [V][4] A_i2 words
     float* sL = reinterpret_cast<float*>(sMet + V * 4);                     // [TC] column L1
     uint32_t* sKp = reinterpret_cast<uint32_t*>(sL + 256);                  // [kCB] kept columns, 8 bits each
     uint32_t* sUni = sKp + kCB;                                             // [kCB] kept positions carrying bits
@@ -418,10 +420,10 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 3 : 1) prune2_kernel(const 
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-template <int V, int M, int NW>
+template <int V, int M, int NW, int MINB>
 cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     constexpr int kThreads = 32 * NW;
-    auto k = prune2_kernel<V, M, NW>;
+    auto k = prune2_kernel<V, M, NW, MINB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -442,14 +444,14 @@ cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int V, int NW>
+template <int V, int NW, int MINB>
 cudaError_t launch_m(int M, const Batch& B, size_t smem, cudaStream_t st) {
     switch (M) {
-        case 4: return launch2<V, 4, NW>(B, smem, st);
-        case 5: return launch2<V, 5, NW>(B, smem, st);
-        case 6: return launch2<V, 6, NW>(B, smem, st);
-        case 7: return launch2<V, 7, NW>(B, smem, st);
-        case 8: return launch2<V, 8, NW>(B, smem, st);
+        case 4: return launch2<V, 4, NW, MINB>(B, smem, st);
+        case 5: return launch2<V, 5, NW, MINB>(B, smem, st);
+        case 6: return launch2<V, 6, NW, MINB>(B, smem, st);
+        case 7: return launch2<V, 7, NW, MINB>(B, smem, st);
+        case 8: return launch2<V, 8, NW, MINB>(B, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -457,8 +459,9 @@ cudaError_t launch_m(int M, const Batch& B, size_t smem, cudaStream_t st) {
 template <int V>
 cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
     // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
-    if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16>(M, B, smem, st);
-    return launch_m<V, 8>(M, B, smem, st);
+    if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16, 1>(M, B, smem, st);
+    if (B.any_tc || V > 64) return launch_m<V, 8, 3>(M, B, smem, st);
+    return launch_m<V, 8, 4>(M, B, smem, st);  // no window form: 4 CTAs per SM (measured faster)
 }
 
 }  // namespace
@@ -538,19 +541,20 @@ int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream) {
     Batch B;  // host staging of the kernel parameters (copied into the launch; per call: thread-safe)
     B.n = n;
     B.tile0[0] = 0;
-    B.any_score = B.any_mask = 0;
+    B.any_score = B.any_mask = B.any_tc = 0;
     for (int i = 0; i < n; ++i) {
         if (!setup_problem(Ls[i], B.tm[i], B.a[i], stream)) return kLaunchUnsupported;
         const vnm_geom& g = *Ls[i].g;
         B.tile0[i + 1] = B.tile0[i] + ((g.nb_pad + kCB - 1) / kCB) * (g.rows_p / V);
         B.any_score |= B.a[i].has_score;
         B.any_mask |= Ls[i].mask_out != nullptr;
+        B.any_tc |= B.a[i].has_tc;
     }
     const int tile_cols = kCB * M;
     const size_t buf = static_cast<size_t>(V) * tile_cols * 2 + (B.any_score ? static_cast<size_t>(V) * tile_cols * 4 : 0);
-    const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (4 + 8) + static_cast<size_t>(V) * 16 + 256 * 4 +
-                        2 * kCB * 4 + 64 * 8 + (B.any_mask ? static_cast<size_t>(V) * kCB * 4 : 0) +
-                        2 * static_cast<size_t>(V) * kCB;
+    const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (B.any_tc ? 4 + 8 : 4) + static_cast<size_t>(V) * 16 +
+                        256 * 4 + 2 * kCB * 4 + 64 * 8 + (B.any_mask ? static_cast<size_t>(V) * kCB * 4 : 0) +
+                        (B.any_tc ? 2 : 1) * static_cast<size_t>(V) * kCB;
     if (smem > kMaxSmem) return kLaunchUnsupported;
     cudaError_t e;
     switch (V) {
