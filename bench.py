@@ -232,16 +232,20 @@ def run_gpu(args):
     # launch groups: independent layers as one vnm_spmm_batched call (workloads with "groups"; token mode)
     groups = wl.get("groups") if not out_mode else None
     groups = groups or [[i] for i in range(len(layers))]
+    # every group after the first is launched with VNM_SPMM_WEIGHTS_READY: its weights were written by the prune
+    # pass, which completed before the previous group's SpMM began (include/vnm.h); the small-T launches then issue
+    # their first weight loads before waiting for that SpMM
     gargs = []
-    for gr in groups:
-        if len(gr) == 1:
+    for gi, gr in enumerate(groups):
+        if out_mode:
             gargs.append(None)
             continue
         ls = [layers[i] for i in gr]
-        wsg = vnm.spmm_batched_workspace([l["P"].g for l in ls], T, dev)
+        wsg = vnm.spmm_batched_workspace([l["P"].g for l in ls], T, dev) if len(gr) > 1 else ls[0]["ws"]
         cpg = [l["P"].c() for l in ls]
         k = len(ls)
-        gargs.append(dict(n=k, cp=cpg, ws=wsg,
+        flags = vnm.VNM_SPMM_WEIGHTS_READY if gi > 0 and not args.no_weights_ready else 0
+        gargs.append(dict(n=k, cp=cpg, ws=wsg, flags=flags,
                           X=(ctypes.c_void_p * k)(*[l["X"].data_ptr() for l in ls]),
                           ldx=(ctypes.c_int64 * k)(*[l["X"].stride(0) for l in ls]),
                           P=(ctypes.c_void_p * k)(*[ctypes.cast(ctypes.pointer(c), ctypes.c_void_p) for c in cpg]),
@@ -259,13 +263,14 @@ def run_gpu(args):
         assert st == 0, vnm.status_string(st)
 
     def spmm_group(gi):
-        """The layers of group gi: one vnm_spmm call, or one vnm_spmm_batched call (independent layers)."""
+        """The layers of group gi: one vnm_spmm_batched call (independent layers; a single layer: the same plan as
+        vnm_spmm, with the weights-ready flag)."""
         a = gargs[gi]
         if a is None:
             spmm(layers[groups[gi][0]])
             return
         ws = a["ws"]
-        st = L.vnm_spmm_batched(a["n"], a["X"], a["ldx"], T, a["P"], a["Y"], a["ldy"], vnm.VNM_BF16,
+        st = L.vnm_spmm_batched(a["n"], a["X"], a["ldx"], T, a["P"], a["Y"], a["ldy"], vnm.VNM_BF16, a["flags"],
                                 ctypes.c_void_p(ws.data_ptr()) if ws is not None else None,
                                 ws.numel() * 4 if ws is not None else 0,
                                 ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
@@ -698,6 +703,8 @@ def main():
                     help="multi-GPU partitioning: token sharding (weak scaling, no collective) or V-block-aligned "
                          "output sharding + NCCL all-gather of Y^T (strong scaling)")
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-weights-ready", action="store_true",
+                    help="launch every SpMM group without VNM_SPMM_WEIGHTS_READY (comparison)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-tokens", type=int, default=1024)

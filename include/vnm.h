@@ -177,11 +177,17 @@ size_t vnm_spmm_workspace_bytes(const vnm_geom* g, int32_t T);
  * one prologue, one pipeline fill and one stream-K tail for the group instead of one per layer; any other group
  * runs as one vnm_spmm per problem, in order, on `stream`.  Results are identical to n vnm_spmm calls up to the
  * fp32 summation order of the K pieces (deterministic for a given batch).  workspace: as for vnm_spmm, sized by
- * vnm_spmm_batched_workspace_bytes (one workspace serves the whole call).  Errors: VNM_ERR_ARG (n < 1 or n > 64,
- * NULL arrays), else the first invalid entry's vnm_spmm status (nothing launched).                       */
+ * vnm_spmm_batched_workspace_bytes (one workspace serves the whole call).
+ * flags: 0, or VNM_SPMM_WEIGHTS_READY — the caller guarantees every P[i]'s arrays were completely written before
+ * the kernel that precedes this call on `stream` began (e.g. weights pruned once, or at least two launches
+ * earlier): the small-T launch then issues the weight loads of its first pipeline fill before waiting for that
+ * kernel (programmatic dependent launch), hiding them behind its tail; X^T, Y^T and the workspace are still only
+ * touched after the wait.  Errors: VNM_ERR_ARG (n < 1 or n > 64, NULL arrays, unknown flag bits), else the first
+ * invalid entry's vnm_spmm status (nothing launched).                                                   */
+#define VNM_SPMM_WEIGHTS_READY 1u
 vnm_status vnm_spmm_batched(int32_t n, const uint16_t* const* XT, const int64_t* ldx, int32_t T,
                             const vnm_packed* const* P, void* const* YT, const int64_t* ldy, vnm_dtype y_dtype,
-                            void* workspace, size_t workspace_bytes, vnm_stream_t stream);
+                            uint32_t flags, void* workspace, size_t workspace_bytes, vnm_stream_t stream);
 size_t vnm_spmm_batched_workspace_bytes(int32_t n, const vnm_geom* const* g, int32_t T);
 
 /* Zero-fill a vnm_spmm workspace (asynchronous on stream).  VNM_ERR_ARG if ws is NULL with bytes > 0.     */

@@ -320,8 +320,9 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
 
 vnm_status vnm_spmm_batched(int32_t n, const uint16_t* const* XT, const int64_t* ldx, int32_t T,
                             const vnm_packed* const* P, void* const* YT, const int64_t* ldy, vnm_dtype y_dtype,
-                            void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
+                            uint32_t flags, void* workspace, size_t workspace_bytes, vnm_stream_t stream) {
     if (n < 1 || n > 64 || !XT || !ldx || !P || !YT || !ldy) return VNM_ERR_ARG;
+    if (flags & ~static_cast<uint32_t>(VNM_SPMM_WEIGHTS_READY)) return VNM_ERR_ARG;
     if (y_dtype != VNM_F32 && y_dtype != VNM_BF16) return VNM_ERR_ARG;
     if (workspace && !aligned16(workspace)) return VNM_ERR_ALIGN;
     // validate every problem as vnm_spmm does before launching anything
@@ -352,9 +353,10 @@ vnm_status vnm_spmm_batched(int32_t n, const uint16_t* const* XT, const int64_t*
             ++live;
         }
         if (live == 0) continue;
-        one = one && live > 1 && vnm::spmm_smallt_batch_applies(gs, live, T);
+        one = one && vnm::spmm_smallt_batch_applies(gs, live, T);
         if (one) {
-            const vnm_status s = from_launch(vnm::launch_spmm_smallt_batch(Ls, live, reinterpret_cast<cudaStream_t>(stream)));
+            const vnm_status s =
+                from_launch(vnm::launch_spmm_smallt_batch(Ls, live, flags, reinterpret_cast<cudaStream_t>(stream)));
             if (s) return s;
             continue;
         }

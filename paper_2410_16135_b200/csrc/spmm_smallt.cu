@@ -103,6 +103,7 @@ struct StArgs {
     int32_t S;           // ring slots
     int32_t nph;         // consumer phases in use (4, 3 or 2; S is a multiple of nph)
     int32_t rg_mode;     // 1: shares are whole row groups (no workspace: no piece is ever cut between CTAs)
+    int32_t wready;      // VNM_SPMM_WEIGHTS_READY: weight TMAs of the first ring fill before griddepcontrol.wait
     uint32_t x_bytes;    // X^T slice bytes per slot (the largest problem's, rounded to 1 KB)
     uint32_t slot_bytes;
     int32_t trace;
@@ -338,7 +339,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 4; ++j) tma_prefetch_desc(&maps.m[i][j]);
     }
     __syncthreads();
-    grid_dep_wait();    // the previous kernel's outputs (this layer's X^T, packed weights) are visible
+    // the previous kernel's outputs (this layer's X^T, packed weights, the workspace) are visible; with
+    // weights_ready the producer waits later, after issuing the weights of its first units (below)
+    if (!(warp == kProd && a.wready)) grid_dep_wait();
     grid_dep_launch();  // the next kernel may take SMs as this grid's CTAs exit
     if (tr) g_st_t[1][blockIdx.x] = gtime();
 
@@ -363,7 +366,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             load_prob(pi);
             int rp = (u0 - ub) / n_st, st = u0 - ub - rp * n_st, s = 0, par = 0;  // (incremental)
+            // weights_ready (vnm_spmm_batched flag): the packed weights were written before the previous kernel
+            // began, so the first ring fill's weight boxes (A_n, A_i2, A_i1) are issued BEFORE waiting for that
+            // kernel (they stream in during its tail); their X^T slices follow the wait
+            int npre = a.wready ? min(a.S, u1 - u0) : 0;
+            int dx_s[16], dx_y0[16], dx_pi[16];
+            auto flush_pre = [&](int n) {  // wait for the previous kernel, then the X^T slices of units [0, n)
+                grid_dep_wait();
+                for (int j = 0; j < n; ++j) {
+                    const StProb& pj = a.pr[dx_pi[j]];
+                    uint8_t* bj = slots + dx_s[j] * a.slot_bytes;
+                    for (int b = 0; b < ((a.abl & 2) ? 0 : pj.x_nbox); ++b)
+                        tma_load_2d(bj + kABytes + b * pj.x_box_bytes, &maps.m[dx_pi[j]][1], 0, dx_y0[j] + b * pj.x_box,
+                                    &full[dx_s[j]]);
+                }
+            };
             for (int u = u0, q = 0; u < u1; ++u, ++q) {
+                // a third A_i2 box needs a ring slot the consumers release only after units that need X^T: end
+                // the pre-wait phase first (short row groups)
+                if (q < npre && u == pend && k >= kMB) {
+                    flush_pre(q);
+                    npre = q;
+                }
                 if (u == pend) {
                     const int pu1 = min(u1, ub + (rp + 1) * n_st);
                     const int ms = k % kMB;
@@ -378,10 +402,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* base = slots + s * a.slot_bytes;
                 mbar_arrive_expect_tx(&full[s], (a.abl & 2) ? kABytes + c_bytes : tx);
                 tma_load_2d(base, &tm[0], st * 2 * kBlkU, rp * kRowsU, &full[s]);
-                const int y0 = (st * kBlkU * M) >> xpl2;  // first row of the slice in the X^T view
-                for (int b = 0; b < ((a.abl & 2) ? 0 : x_nbox); ++b)
-                    tma_load_2d(base + kABytes + b * xbb, &tm[1], 0, y0 + b * x_box, &full[s]);
                 tma_load_2d(base + kABytes + a.x_bytes, &tm[3], st * kBlkU, (rp * kRowsU) / V, &full[s]);
+                const int y0 = (st * kBlkU * M) >> xpl2;  // first row of the slice in the X^T view
+                if (q < npre) {  // X^T after the wait
+                    dx_s[q] = s;
+                    dx_y0[q] = y0;
+                    dx_pi[q] = pi;
+                    if (q == npre - 1) flush_pre(npre);
+                } else {
+                    for (int b = 0; b < ((a.abl & 2) ? 0 : x_nbox); ++b)
+                        tma_load_2d(base + kABytes + b * xbb, &tm[1], 0, y0 + b * x_box, &full[s]);
+                }
                 if (a.trace == 2 && blockIdx.x < 160 && q < 32) g_st_u[blockIdx.x][q][3] = gtime();
                 if (++s == a.S) {
                     s = 0;
@@ -773,7 +804,7 @@ size_t spmm_smallt_batch_workspace_bytes(const vnm_geom* const* gs, int n, int32
     return spmm_smallt_batch_applies(gs, n, T) ? make_plan(gs, nullptr, n, T).ws_bytes : 0;
 }
 
-int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, cudaStream_t stream) {
+int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, uint32_t flags, cudaStream_t stream) {
     const StPlan p = plan_of(Ls, n, true);
     if (!p.ok) return kLaunchUnsupported;
     for (int i = 0; i < n; ++i)
@@ -795,6 +826,7 @@ int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, cudaStream_t stream) {
         a.gb[i] = p.gb[i];
     }
     a.S = p.S;
+    a.wready = (flags & 1u) ? 1 : 0;
     a.nph = p.nph;
     a.x_bytes = p.x_bytes;
     a.slot_bytes = p.slot_bytes;
@@ -852,6 +884,6 @@ int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, cudaStream_t stream) {
     return launch_v<4>(L0.T, L0.y_dtype, p, a, maps, stream);
 }
 
-int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) { return launch_spmm_smallt_batch(&L, 1, stream); }
+int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream) { return launch_spmm_smallt_batch(&L, 1, 0u, stream); }
 
 }  // namespace vnm

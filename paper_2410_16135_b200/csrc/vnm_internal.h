@@ -78,7 +78,8 @@ int launch_spmm_smallt(const SpmmLaunch& L, cudaStream_t stream);
 // Ls[0] serves the launch
 bool spmm_smallt_batch_applies(const vnm_geom* const* gs, int n, int32_t T);
 size_t spmm_smallt_batch_workspace_bytes(const vnm_geom* const* gs, int n, int32_t T);
-int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, cudaStream_t stream);
+// flags & 1: the packed weights were written before the previous kernel on the stream began (VNM_SPMM_WEIGHTS_READY)
+int launch_spmm_smallt_batch(const SpmmLaunch* Ls, int n, uint32_t flags, cudaStream_t stream);
 
 // RIA importance (ria.cu)
 size_t ria_workspace_bytes(int32_t rows, int32_t cols);

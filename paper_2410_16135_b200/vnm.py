@@ -86,7 +86,7 @@ def lib():
             L.vnm_spmm_workspace_bytes.restype = sz
             L.vnm_spmm_workspace_init.argtypes = [P, sz, P]
             L.vnm_spmm_workspace_init.restype = ctypes.c_int
-            L.vnm_spmm_batched.argtypes = [i32, P, P, i32, P, P, P, ctypes.c_int, P, sz, P]
+            L.vnm_spmm_batched.argtypes = [i32, P, P, i32, P, P, P, ctypes.c_int, ctypes.c_uint32, P, sz, P]
             L.vnm_spmm_batched.restype = ctypes.c_int
             L.vnm_spmm_batched_workspace_bytes.argtypes = [i32, P, i32]
             L.vnm_spmm_batched_workspace_bytes.restype = sz
@@ -321,10 +321,14 @@ def spmm(XT: torch.Tensor, P: Packed, T: int | None = None, out: torch.Tensor | 
     return out
 
 
+VNM_SPMM_WEIGHTS_READY = 1
+
+
 def spmm_batched(XTs: list, Ps: list, T: int, outs: list | None = None, out_dtype: torch.dtype = torch.float32,
-                 workspace: torch.Tensor | None = None) -> list:
+                 workspace: torch.Tensor | None = None, weights_ready: bool = False) -> list:
     """vnm_spmm_batched: Y_i^T = W'_i X_i^T for independent problems sharing T (up to 4 small-T problems per
-    launch).  XTs[i]: bf16 [cols_i][ldx_i]; returns the list of Y_i^T (or writes into outs[i])."""
+    launch).  XTs[i]: bf16 [cols_i][ldx_i]; returns the list of Y_i^T (or writes into outs[i]).  weights_ready:
+    VNM_SPMM_WEIGHTS_READY (the packed weights were written before the previous kernel on the stream began)."""
     n = len(Ps)
     if len(XTs) != n or (outs is not None and len(outs) != n):
         raise ValueError("XTs, Ps (and outs) must have the same length")
@@ -356,7 +360,8 @@ def spmm_batched(XTs: list, Ps: list, T: int, outs: list | None = None, out_dtyp
                                   arr(ctypes.c_int64, [X.stride(0) for X in XTs]), T,
                                   arr(ctypes.c_void_p, [ctypes.cast(ctypes.pointer(cp), ctypes.c_void_p) for cp in cps]),
                                   arr(ctypes.c_void_p, [_ptr(Y) for Y in outs]),
-                                  arr(ctypes.c_int64, [Y.stride(0) for Y in outs]), ydt, ws_ptr, ws_bytes,
+                                  arr(ctypes.c_int64, [Y.stride(0) for Y in outs]), ydt,
+                                  VNM_SPMM_WEIGHTS_READY if weights_ready else 0, ws_ptr, ws_bytes,
                                   _stream(dev)), "vnm_spmm_batched")
     return outs
 
