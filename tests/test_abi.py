@@ -130,3 +130,31 @@ def test_ria_argument_errors():
     assert L.vnm_act_norms(P(16), 4, 3, 8, P(16), None) == vnm.VNM_ERR_SHAPE  # ldx < T
     assert L.vnm_act_norms(P(16), 8, 3, 8, None, None) == vnm.VNM_ERR_ARG
     assert L.vnm_act_norms(P(18), 8, 3, 8, P(16), None) == vnm.VNM_ERR_ALIGN
+
+
+def test_spmm_batched_argument_errors_and_workspace():
+    """vnm_spmm_batched validates before launching (no GPU needed) and sizes one workspace for the whole call."""
+    L = vnm.lib()
+    g = vnm.geometry(4096, 4096, 64, 5)
+    fake = 1 << 20  # never dereferenced: validation fails first (array pointers fake and aligned)
+    c = vnm.CPacked()
+    c.g = g
+    c.values = c.col_idx = c.meta = fake
+    arr = lambda ty, xs: (ty * len(xs))(*xs)
+    P = arr(ctypes.c_void_p, [ctypes.cast(ctypes.pointer(c), ctypes.c_void_p).value])
+    X = arr(ctypes.c_void_p, [fake])
+    Y = arr(ctypes.c_void_p, [fake])
+    ld = arr(ctypes.c_int64, [16])
+    # n out of range, NULL arrays, unknown flag bits
+    assert L.vnm_spmm_batched(0, X, ld, 16, P, Y, ld, vnm.VNM_BF16, 0, None, 0, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_spmm_batched(65, X, ld, 16, P, Y, ld, vnm.VNM_BF16, 0, None, 0, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_spmm_batched(1, None, ld, 16, P, Y, ld, vnm.VNM_BF16, 0, None, 0, None) == vnm.VNM_ERR_ARG
+    assert L.vnm_spmm_batched(1, X, ld, 16, P, Y, ld, vnm.VNM_BF16, 2, None, 0, None) == vnm.VNM_ERR_ARG
+    # per-entry checks as vnm_spmm: T > ldx, misaligned Y
+    assert L.vnm_spmm_batched(1, X, arr(ctypes.c_int64, [8]), 16, P, Y, ld, vnm.VNM_BF16, 0, None, 0, None) == vnm.VNM_ERR_SHAPE
+    assert L.vnm_spmm_batched(1, X, ld, 16, P, arr(ctypes.c_void_p, [fake + 2]), ld, vnm.VNM_BF16, 0, None, 0,
+                              None) == vnm.VNM_ERR_ALIGN
+    # one workspace for the group >= every member's own
+    gs = [vnm.geometry(4096, 4096, 64, 5), vnm.geometry(11008, 4096, 64, 5), vnm.geometry(4096, 11008, 64, 5)]
+    b = vnm.spmm_batched_workspace_bytes(gs, 16)
+    assert b >= max(vnm.spmm_workspace_bytes(x, 16) for x in gs) > 0
