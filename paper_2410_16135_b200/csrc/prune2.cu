@@ -460,8 +460,10 @@ template <int V>
 cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
     // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
     if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16, 1>(M, B, smem, st);
-    if (B.any_tc || V > 64) return launch_m<V, 8, 3>(M, B, smem, st);
-    return launch_m<V, 8, 4>(M, B, smem, st);  // no window form: 4 CTAs per SM (measured faster)
+    if constexpr (V <= 64) {
+        if (!B.any_tc) return launch_m<V, 8, 4>(M, B, smem, st);  // no window form: 4 CTAs per SM (measured faster)
+    }
+    return launch_m<V, 8, 3>(M, B, smem, st);
 }
 
 }  // namespace
