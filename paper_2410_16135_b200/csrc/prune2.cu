@@ -91,7 +91,9 @@ struct Batch {
 
 // MINB: CTAs per SM the register budget is sized for (8-warp CTAs: 3, or 4 when no window form is written —
 // the window-form staging is then not allocated and 4 CTAs fit in shared memory)
-template <int V, int M, int NW, int MINB>
+// LEAN: no score, no mask, no window form anywhere in the batch (the decode / deployment case): those paths
+// compile out of the per-row loop (fewer branches and parameter loads per weight; the kernel is issue-bound)
+template <int V, int M, int NW, int MINB, bool LEAN>
 __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_constant__ Batch B) {
     constexpr int kWarps = NW, kThreads = 32 * NW;
     constexpr int TC = kCB * M;  // tile columns (<= 256)
@@ -167,7 +169,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         const int p = info.x, bx = info.y, by = info.z;
         const Prune2Args& a = B.a[p];
         const Maps& tm = B.tm[p];
-        const bool has_score = a.has_score, tc = a.has_tc;
+        const bool has_score = !LEAN && a.has_score, tc = !LEAN && a.has_tc;
+        uint32_t* const mask_out = LEAN ? nullptr : a.mask_out;
         const int b0 = bx * kCB, r0 = by * V;
         PTRACE(1)
         const uint32_t* sW = reinterpret_cast<const uint32_t*>(smem + bi * buf_bytes);
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                 sTcv[r * kCB + b] = pk;
                 sTcn[r * kCB + b] = static_cast<uint8_t>(e.y);
             }
-            if (a.mask_out) {  // mask bits of pad blocks (columns >= cols_p) stay 0
+            if (mask_out) {  // mask bits of pad blocks (columns >= cols_p) stay 0
                 const uint32_t cl = __byte_perm(kp, 0u, 0x4440u | plo), ch = __byte_perm(kp, 0u, 0x4440u | phi);
                 sBits[r * kCB + b] = b0 + b < a.nb ? (1u << cl) | (1u << ch) : 0u;
             }
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                         make_uint4(w4[0], w4[1], w4[2], w4[3]);
             }
         }
-        if (a.mask_out) {
+        if (mask_out) {
             const int w0 = b0 * M / 32;
             constexpr int mwords = TC / 32;
             const int nw = min(mwords, a.ld_mask - w0);
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                     const int sh = bl * M - lo_col;
                     word |= sh >= 0 ? (sh < 32 ? bits << sh : 0u) : bits >> (-sh);
                 }
-                a.mask_out[static_cast<int64_t>(r0 + r) * a.ld_mask + w0 + w] = word;
+                mask_out[static_cast<int64_t>(r0 + r) * a.ld_mask + w0 + w] = word;
             }
         }
         // ---- TMA tensor stores of the staged tile (clipped at nb_pad / rows by the tensor maps)
@@ -420,10 +423,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-template <int V, int M, int NW, int MINB>
+template <int V, int M, int NW, int MINB, bool LEAN = false>
 cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     constexpr int kThreads = 32 * NW;
-    auto k = prune2_kernel<V, M, NW, MINB>;
+    auto k = prune2_kernel<V, M, NW, MINB, LEAN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -444,14 +447,14 @@ cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int V, int NW, int MINB>
+template <int V, int NW, int MINB, bool LEAN = false>
 cudaError_t launch_m(int M, const Batch& B, size_t smem, cudaStream_t st) {
     switch (M) {
-        case 4: return launch2<V, 4, NW, MINB>(B, smem, st);
-        case 5: return launch2<V, 5, NW, MINB>(B, smem, st);
-        case 6: return launch2<V, 6, NW, MINB>(B, smem, st);
-        case 7: return launch2<V, 7, NW, MINB>(B, smem, st);
-        case 8: return launch2<V, 8, NW, MINB>(B, smem, st);
+        case 4: return launch2<V, 4, NW, MINB, LEAN>(B, smem, st);
+        case 5: return launch2<V, 5, NW, MINB, LEAN>(B, smem, st);
+        case 6: return launch2<V, 6, NW, MINB, LEAN>(B, smem, st);
+        case 7: return launch2<V, 7, NW, MINB, LEAN>(B, smem, st);
+        case 8: return launch2<V, 8, NW, MINB, LEAN>(B, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -461,6 +464,7 @@ cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
     // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
     if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16, 1>(M, B, smem, st);
     if constexpr (V <= 64) {
+        if (!B.any_tc && !B.any_score && !B.any_mask) return launch_m<V, 8, 4, true>(M, B, smem, st);
         if (!B.any_tc) return launch_m<V, 8, 4>(M, B, smem, st);  // no window form: 4 CTAs per SM (measured faster)
     }
     return launch_m<V, 8, 3>(M, B, smem, st);
