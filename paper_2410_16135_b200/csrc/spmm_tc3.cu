@@ -304,6 +304,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tmem_wait_ld();
             }
         };
+        // the same in two halves: TMEM loads issued (no wait), then wait + pack — so the loads of chunk c + kEq run
+        // under the stores of chunk c
+        auto ld_issue = [&](uint32_t taddr, int c, uint32_t (&v)[64]) {
+            if constexpr (kBf16) {
+                tmem_ld_32x32b_x32(taddr + c * 64, v);
+                tmem_ld_32x32b_x32(taddr + c * 64 + 32, v + 32);  // past NT: other columns, never stored
+            } else {
+                tmem_ld_32x32b_x32(taddr + c * 32, v);
+            }
+        };
+        auto ld_finish = [&](const uint32_t (&v)[64], uint32_t (&w)[32]) {
+            tmem_wait_ld();
+            if constexpr (kBf16) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
+                    w[k] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) w[k] = v[k];
+            }
+        };
         auto release = [&](int acc) {
             tc_fence_before();
             __syncwarp();
@@ -385,11 +408,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             } else {
                 const int last = half < kNch ? ((kNch - 1 - half) / kEq) * kEq + half : -1;  // this warp's last chunk
                 if (last < 0) release(acc);  // no chunk for this warp in this tile
+                uint32_t v[64], w[32];
+                if (half < kNch) ld_issue(taddr, half, v);
 #pragma unroll 1
                 for (int c = half; c < kNch; c += kEq) {
-                    uint32_t w[32];
-                    drain(taddr, c, w);
+                    ld_finish(v, w);
                     if (c == last) release(acc);
+                    else ld_issue(taddr, c + kEq, v);  // the next chunk's TMEM loads under this chunk's stores
                     store(rt, c, w);
                 }
             }
