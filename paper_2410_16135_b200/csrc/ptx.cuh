@@ -391,6 +391,36 @@ __device__ __forceinline__ void tmem_cp_elect(uint32_t taddr, uint64_t d) {
         asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p tcgen05.cp.cta_group::2.128x128b [%0], %1;\n\t}" ::"r"(taddr), "l"(d)
                      : "memory");
 }
+// tcgen05.cp 128x256b (128 rows x 32 B of a shared-memory operand described by d -> 8 TMEM columns), elected lane
+template <int CG>
+__device__ __forceinline__ void tmem_cp256_elect(uint32_t taddr, uint64_t d) {
+    if constexpr (CG == 1)
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr), "l"(d)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t@p tcgen05.cp.cta_group::2.128x256b [%0], %1;\n\t}" ::"r"(taddr), "l"(d)
+                     : "memory");
+}
+// mma_sp_stage with A in TMEM (TS form): MMA i of the stage reads A at TMEM column a + 8 i (16 compressed bf16 per row)
+__device__ __forceinline__ void mma_sp_stage_ts_pair(uint32_t d, uint32_t a, uint64_t bd, uint64_t b_step, uint32_t e,
+                                                     uint32_t idesc0, uint32_t idesc1, uint32_t accumulate, uint32_t n) {
+    asm volatile(
+        "{\n\t.reg .pred p, p3, acc, one;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3, e2;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "setp.ne.b32 acc, %6, 0;\n\t"
+        "setp.eq.b32 one, 0, 0;\n\t"
+        "setp.gt.and.u32 p3, %8, 2, p;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+        "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"
+        "add.u32 e2, %3, 2;\n\t"
+        "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [%1], %2, [%3], %4, acc;\n\t"
+        "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [a1], b1, [%3], %5, one;\n\t"
+        "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [a2], b2, [e2], %4, one;\n\t"
+        "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [a3], b3, [e2], %5, one;\n\t"
+        "}" ::"r"(d),
+        "r"(a), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n)
+        : "memory");
+}
 // commit of the pair's tcgen05 ops, multicast to the CTAs of `mask`, elected lane of a converged warp
 __device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar, uint16_t mask) {
     asm volatile(

@@ -60,6 +60,8 @@ struct Tc3Args {
     int32_t a_res;       // 1: A + metadata resident; 0: streamed per stage
     int32_t rp_per;      // resident: pairs per row pair;  streaming: total pairs
     int32_t peek;        // windows cross stage boundaries (5 <= M <= 7: an 8-channel window is wider than a block)
+    int32_t ts;          // 1: resident A copied once into TMEM (tcgen05.cp) and the MMAs read it from there (TS form);
+                         // NT = 256 (one accumulator) only: TMEM = accumulator | A (32 columns per chunk) | metadata
     int32_t ovh;         // 1: every slot also holds the next stage's first 8 rows (loaded twice; no cross-stage
                          // wait, no shadow); 0: K-ring with the MMA waiting for the next stage too
     int32_t slot_rows;   // rows per slot: rows_stage (+ 8 with ovh and peek)
@@ -226,13 +228,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t idesc1 = idesc_bf16(256, NT, true, 1, true);
             const uint64_t b_step = (a.M == 4 ? 32u : 4u * a.M) * 128u >> 4;  // B descriptor advance per MMA
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
+            const uint32_t meta_col = a.ts ? NT + 32u * a.n_chunk : kMetaCol;   // metadata after A in the TS form
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0, c_full0 = 0;
             for (; tile3(a, cid, tl, rp, tt); ++tl) {
-                if (a.a_res && tl == 0) {  // resident metadata -> TMEM columns kMetaCol + 4c (both CTAs)
+                if (a.a_res && tl == 0) {  // resident metadata -> TMEM columns meta_col + 4c (both CTAs)
                     mbar_wait(res_full, 0);
                     tc_fence_after();
                     for (int c = 0; c < a.n_chunk; ++c)
-                        tmem_cp_elect<2>(tmem + kMetaCol + 4 * c, sdesc(smem_u32(sE + c * kEBytes), 16, 128, 0));
+                        tmem_cp_elect<2>(tmem + meta_col + 4 * c, sdesc(smem_u32(sE + c * kEBytes), 16, 128, 0));
+                    if (a.ts)  // resident A -> TMEM columns NT + 8 mi (MMA mi's 128 rows x 16 compressed values)
+                        for (int c = 0; c < a.n_chunk; ++c)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                tmem_cp256_elect<2>(tmem + NT + 32 * c + 8 * i,
+                                                    sdesc(smem_u32(sA + c * kABytes), 16, 1024, kLayoutSW128) + 2 * i);
                 }
                 const int acc = kNacc == 2 ? (tl & 1) : 0;
                 const int use = kNacc == 2 ? (tl >> 1) : tl;  // uses of this accumulator so far
@@ -257,13 +266,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     uint32_t e;
                     if (a.a_res) {
                         ad = sdesc(smem_u32(sA + (mi0 >> 2) * kABytes), 16, 1024, kLayoutSW128) + 2 * (mi0 & 3);
-                        e = tmem + kMetaCol + 4 * (mi0 >> 2) + (mi0 & 2);
+                        e = tmem + meta_col + 4 * (mi0 >> 2) + (mi0 & 2);
                     } else {  // this slot's chunk: metadata into the slot's TMEM columns first (tensor-pipe order)
-                        e = tmem + kMetaCol + 4 * s;
+                        e = tmem + meta_col + 4 * s;
                         tmem_cp_elect<2>(e, sdesc(smem_u32(sE + s * kEBytes), 16, 128, 0));
                         ad = sdesc(smem_u32(sA + s * kABytes), 16, 1024, kLayoutSW128);
                     }
-                    mma_sp_stage<2>(tmem + acc * NT, ad, bd, b_step, e, idesc0, idesc1, st > 0 ? 1u : 0u, n);
+                    if (a.ts)
+                        mma_sp_stage_ts_pair(tmem + acc * NT, tmem + NT + 8 * mi0, bd, b_step, e, idesc0, idesc1,
+                                             st > 0 ? 1u : 0u, n);
+                    else
+                        mma_sp_stage<2>(tmem + acc * NT, ad, bd, b_step, e, idesc0, idesc1, st > 0 ? 1u : 0u, n);
                     mma_commit_pair_elect(&empty[s], 0x3);
                 }
                 mma_commit_pair_elect(&tmem_full[acc], 0x3);
@@ -448,6 +461,8 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
               res + 2u * (4 * a.slot_rows + 8) * 128u + fixed <= kMaxSmem;
     if (want_res == 1 && !a.a_res) return kLaunchUnsupported;
     if (!a.a_res && a.ms != 4) return kLaunchUnsupported;  // streamed A arrives in 4-MMA chunks
+    // TS form: resident A and one accumulator, TMEM = NT + 32 columns per A chunk + 4 per metadata chunk
+    if (!a.a_res || kNacc != 1 || NT + 36 * a.n_chunk > 512) a.ts = 0;
     // ring slots: as many as fit (bytes in flight hide the load latency), at least 3
     int S = 0;
     for (int s = 8; s >= 3 && !S; --s) {
@@ -532,6 +547,7 @@ int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream) {
     a.n_rp = (a.n_rt + 1) / 2;
     a.peek = g.M >= 5 && g.M <= 7;
     a.ovh = VNM_ENV_INT("VNM_TC3_OVH", 1) ? 1 : 0;
+    a.ts = 0;
     const int res = mode < 0 ? 1 : mode;
     // resident A: 4 MMAs per stage (16 blocks), 2 when a 4-MMA stage would be large (M >= 7: >= 112 rows)
     a.ms = g.M >= 7 && res ? 2 : 4;
@@ -542,6 +558,13 @@ int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream) {
     // NT = 256 (one accumulator) when T is a multiple of 256 and A streams (long K: the per-tile hand-off is
     // amortised), else NT = 224 (two accumulators)
     int nt = (mode == 0 && L.T % 256 == 0) ? 256 : 224;
+    // opt-in (VNM_TC3_TS=1): resident A in TMEM (TS form, one accumulator, NT = 256) — the MMAs stop reading A
+    // from shared memory; parity-tested, but measured no faster in the bench's cold steps (warm: ~3 %), so off by
+    // default (profiles/r02_experiments.md)
+    if (mode != 0 && L.T % 256 == 0 && VNM_ENV_INT("VNM_TC3_TS", 0) && 256 + 36 * a.n_chunk <= 512) {
+        nt = 256;
+        a.ts = 1;
+    }
     if (const int v = VNM_ENV_INT("VNM_TC3_NT", 0)) nt = v;
     const int want = mode < 0 ? -1 : res;
     auto launch = [&](int w) {
