@@ -11,8 +11,9 @@ V = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 shapes = [(4096, 4096), (11008, 4096), (4096, 11008)]
 Ps = [vnm.prune_compress(to_dev_bf16(synth.weights(r, c, seed=r + c)), V, M) for r, c in shapes]
-Xs = [to_dev_bf16(synth.activations_t(c, T, seed=c)) for r, c in shapes]
-Ys = [torch.empty((r, T), dtype=torch.bfloat16, device="cuda") for r, c in shapes]
+ldx = (T + 7) // 8 * 8  # leading dimensions padded to 16 bytes (the ABI's alignment rule)
+Xs = [to_dev_bf16(synth.activations_t(c, T, seed=c, ld=ldx))[:, :T] for r, c in shapes]
+Ys = [torch.empty((r, ldx), dtype=torch.bfloat16, device="cuda")[:, :T] for r, c in shapes]
 wss = [vnm.spmm_workspace(P.g, T, "cuda") for P in Ps]
 wsb = vnm.spmm_batched_workspace([P.g for P in Ps], T, "cuda")
 sep = lambda: [vnm.spmm(X, P, T=T, out=Y, workspace=w) for X, P, Y, w in zip(Xs, Ps, Ys, wss)]
