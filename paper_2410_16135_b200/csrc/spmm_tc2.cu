@@ -55,7 +55,7 @@ struct Tc2Args {
     int32_t trace;       // VNM_SPMM_TRACE: per-CTA wait / busy cycle counters into g_tc2_t
     int32_t pf;          // L2 prefetch distance in stages (0: none): X^T streamed from HBM (long K, large T)
     int32_t abl;         // VNM_ABL (timing ablations only, results invalid): 1 no epilogue, 2 no Y stores,
-                         // 4 no X^T loads, 8 no metadata copies after the first stage
+                         // 4 no X^T loads, 8 no metadata copies after the first stage, 16 no A loads (streaming)
 };
 
 // VNM_SPMM_TRACE counters per CTA: MMA wait full, MMA wait tmem_empty, MMA loop total, producer wait empty,
@@ -201,8 +201,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     if (a.a_res) {
                         if (leader) mbar_arrive_expect_tx(&full[s], 2 * a.b_bytes);
                     } else {
-                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * (kABytes + kEBytes + a.b_bytes));
-                        tma_load_2d_pair(base, &tmap_a, st * 64, rt * 128, &full[s]);
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * ((a.abl & 16 ? 0u : kABytes) + kEBytes + a.b_bytes));
+                        if (!(a.abl & 16)) tma_load_2d_pair(base, &tmap_a, st * 64, rt * 128, &full[s]);
                         tma_load_2d_pair(base + e_off, &tmap_e, 0, (rte * a.n_stage + st) * 128, &full[s]);
                     }
                     tma_load_2d_pair(base + b_off, &tmap_b, n0, st * a.rows_stage, &full[s]);
