@@ -51,10 +51,10 @@ for _m in (4, 5, 6, 7, 8, 16):
     WORKLOADS[f"llama_mlp_m{_m}"] = dict(V=64, M=_m, T=2048, cfg=5, layers=[("up", 11008, 4096), ("down", 4096, 11008)])
 # NEXT-1: the paper's V = 128 points (tab:bs-sped) on the Llama2-7B layers, decode and prefill
 _LLAMA = [("q", 4096, 4096), ("up", 11008, 4096), ("down", 4096, 11008)]
-for _m in (5, 8, 13):
+for _m in (5, 8, 9, 10, 11, 13):
     WORKLOADS[f"llama_decode_v128_m{_m}"] = dict(V=128, M=_m, T=16, cfg=4, layers=_LLAMA)
     WORKLOADS[f"llama_prefill_v128_m{_m}"] = dict(V=128, M=_m, T=2048, cfg=4, layers=_LLAMA)
-for _m in (4, 5, 6, 7, 8, 16):
+for _m in (4, 5, 6, 7, 8, 9, 10, 11, 13, 16):
     WORKLOADS[f"llama_mlp_v128_m{_m}"] = dict(V=128, M=_m, T=2048, cfg=5, layers=[("up", 11008, 4096), ("down", 4096, 11008)])
 
 
@@ -160,7 +160,7 @@ def run_gpu(args):
     # ---- synthetic inputs (host, seeded per rank), then resident copies in HBM
     layers = []
     out_mode = args.mode == "out"
-    use_tc0 = T > 64 and (M <= 8 or M % 4 == 0) and 32 <= V <= 128
+    use_tc0 = T > 64 and vnm.tc_applies(V, M)
     for li, (name, rows_full, cols) in enumerate(wl["layers"]):
         # token mode: every rank its own tokens (seeded per rank) and a full weight; out mode: the same weight
         # and tokens on every rank, rank r owns a V-block-aligned row shard (whole 128-row tiles for the
@@ -207,7 +207,7 @@ def run_gpu(args):
 
     import ctypes
 
-    use_tc = T > 64 and (M <= 8 or M % 4 == 0) and 32 <= V <= 128
+    use_tc = T > 64 and vnm.tc_applies(V, M)
     if use_tc:  # window-form buffers, written by vnm_prune_compress in the same pass (include/vnm.h)
         for l in layers:
             nv, nm = vnm.tc_bytes(l["P"].g)

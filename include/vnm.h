@@ -86,7 +86,12 @@ typedef struct {
      * For M % 4 == 0 with M > 8 (e.g. 64:2:16) the tensor-core form is the NATURAL 2:4 form instead: a
      * block is a whole number of 4-channel groups, so each group holds at most the row's 2 nonzeros and the
      * masked W is 2:4-sparse in channel order; values_tc / meta_tc are the M = 4 layouts above over the
-     * groups (2 values per group, zero-completed; nb_pad -> ceil(cols_p/4 / 8)*8 groups).              */
+     * groups (2 values per group, zero-completed; nb_pad -> ceil(cols_p/4 / 8)*8 groups).
+     * For the other 8 < M < 16 (e.g. the paper's 128:2:9 / 10 / 11 / 13, tab:bs-sped P:656-665) it is the
+     * WINDOW-16 form: every block is a 16-row window of X^T (the block's M channels and 16-M of the next) as
+     * four 2:4 groups, zero-completed like the window form; MMA 2j + h reads the half-windows h (groups 2h,
+     * 2h+1) of blocks 4j .. 4j+3, so n_mma_w = nb_pad/2 and values_tc holds 8 values per block (half 0 of
+     * blocks 4j.. at MMA 2j, half 1 at MMA 2j + 1), meta_tc the same lane layout.  Packed after the pass.   */
     uint16_t* values_tc;
     uint32_t* meta_tc;
 } vnm_packed;
@@ -96,7 +101,8 @@ typedef struct {
 vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_geom* out);
 
 /* Bytes of one buffer for geometry g: which = 0 values, 1 col_idx, 2 meta, 3 mask, 4 values_tc, 5 meta_tc
- * (4 and 5 are 0 when the tensor-core form does not apply: V < 32, V > 128 or M > 8).  0 on bad input.          */
+ * (4 and 5 are 0 when the tensor-core form does not apply: V < 32, V > 128, or M > 16 with M % 4 != 0).
+ * 0 on bad input.                                                                                     */
 size_t vnm_bytes(const vnm_geom* g, int which);
 
 /* S_{V:N:M} (§3) -> mask bits.
@@ -118,8 +124,9 @@ vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, co
                         vnm_packed* out, int32_t* d_status, vnm_stream_t stream);
 
 /* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.
- * If out->values_tc / out->meta_tc are set (32 <= V <= 128, and M <= 8 or M % 4 == 0) the tensor-core form is
- * written too: the window form in the same pass (M <= 8), the natural 2:4 form by a second launch (M % 4 == 0)
+ * If out->values_tc / out->meta_tc are set (32 <= V <= 128, and M < 16 or M % 4 == 0) the tensor-core form is
+ * written too: the window form in the same pass (M <= 8), the natural 2:4 form (M % 4 == 0) or the window-16
+ * form (other M < 16) by a second launch
  * (identical to vnm_pack_tc of the result).                                                             */
 vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
                               const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
@@ -135,7 +142,7 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
                                       uint32_t* const* mask, vnm_stream_t stream);
 
 /* Fill P->values_tc / P->meta_tc (caller-allocated, vnm_bytes 4 / 5) from the canonical A_n / A_i1 / A_i2
- * of P.  VNM_ERR_UNSUPPORTED unless 32 <= V <= 128 and (M <= 8 or M % 4 == 0); VNM_ERR_ARG if a tc pointer
+ * of P.  VNM_ERR_UNSUPPORTED unless 32 <= V <= 128 and (M < 16 or M % 4 == 0); VNM_ERR_ARG if a tc pointer
  * is NULL.                                                                                            */
 vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
 
@@ -146,7 +153,8 @@ vnm_status vnm_pack_tc(const vnm_packed* P, vnm_stream_t stream);
  *       ldy % 8 == 0, ldy >= T; only rows < g.rows and columns < T are written.
  * bf16 x bf16 products, fp32 accumulation on the sparse tensor cores (tcgen05.mma.sp).
  * Supported: 1 <= T <= 32 with V >= 16 and any M; V = 64, 128, 256 with any M at any T (e.g. the paper's 128:2:M,
- * SURVEY §8(f) NEXT-1); 32 <= V <= 128 at any T when the tensor-core form is present (M <= 8, or M % 4 == 0);
+ * SURVEY §8(f) NEXT-1); 32 <= V <= 128 at any T when the tensor-core form is present (M < 16, or M % 4 == 0;
+ * the window-16 form with a Y^T row that is not a multiple of 16 bytes takes the small-T / gather plan);
  * VNM_ERR_UNSUPPORTED otherwise.
  * Plans: tensor-core form present and T > 64 (or V != 64 beyond the small-T range) -> a window-form kernel (dense
  * X^T tiles by TMA; a Y^T row of T tokens that is not a multiple of 16 bytes takes the pair kernel whose stores are

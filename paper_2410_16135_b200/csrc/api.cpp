@@ -94,8 +94,13 @@ vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_ge
 // Natural 2:4 tensor-core form (M % 4 == 0, M > 8; include/vnm.h): the masked W is 2:4-sparse in the natural
 // channel order, so the window-form kernels run it as the M = 4 layout over 4-channel groups.
 static bool nat24(const vnm_geom* g) { return g->M > 8 && g->M % 4 == 0 && g->V >= 32 && g->V <= 128; }
-// the tensor-core form applies: window form (M <= 8) or natural 2:4 form
-static bool tc_geom(const vnm_geom* g) { return g->V >= 32 && g->V <= 128 && (g->M <= 8 || g->M % 4 == 0); }
+// Window-16 form (8 < M < 16, M % 4 != 0; include/vnm.h): 16-channel windows, two MMAs per 4 blocks — e.g. the
+// paper's 128:2:9 / 10 / 11 / 13 (tab:bs-sped) at prefill sizes
+static bool w16(const vnm_geom* g) { return g->M > 8 && g->M < 16 && g->M % 4 != 0 && g->V >= 32 && g->V <= 128; }
+// the tensor-core form applies: window form (M <= 8), natural 2:4 form (M % 4 == 0) or window-16 form
+static bool tc_geom(const vnm_geom* g) {
+    return g->V >= 32 && g->V <= 128 && (g->M <= 8 || g->M % 4 == 0 || w16(g));
+}
 // the M = 4 view of a natural-2:4 geometry: blocks = 4-channel groups
 static vnm_geom view4(const vnm_geom& g) {
     vnm_geom v = g;
@@ -121,7 +126,8 @@ size_t vnm_bytes(const vnm_geom* g, int which) {
             const size_t rows_w = (rp + 127) / 128 * 128;
             const vnm_geom gv = nat24(g) ? view4(*g) : *g;
             const size_t bpm = gv.M == 4 ? 8 : 4;
-            const size_t n_mma = static_cast<size_t>(gv.nb_pad) / bpm;
+            // window-16 form: two MMAs (half-windows) per 4 blocks
+            const size_t n_mma = w16(g) ? static_cast<size_t>(gv.nb_pad) / 2 : static_cast<size_t>(gv.nb_pad) / bpm;
             const size_t n_stage = (n_mma + 3) / 4;
             return which == 4 ? rows_w * 16 * n_mma * 2 : rows_w / 128 * n_stage * 128 * 4 * 4;
         }
@@ -176,13 +182,15 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
         if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;  // the natural 2:4 form packed after the pass (M % 4 == 0)
         if (!out->values_tc || !out->meta_tc) return VNM_ERR_ARG;
         if (!aligned16(out->values_tc) || !aligned16(out->meta_tc)) return VNM_ERR_ALIGN;
-        if (!nat24(g)) {
+        if (!nat24(g) && !w16(g)) {
             L.values_tc = out->values_tc;
             L.meta_tc = out->meta_tc;
         }
     }
     const vnm_status st = from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
-    if (st || !out->values_tc || !nat24(g)) return st;
+    if (st || !out->values_tc) return st;
+    if (w16(g)) return from_launch(vnm::launch_pack_tc(*out, reinterpret_cast<cudaStream_t>(stream)));
+    if (!nat24(g)) return st;
     return from_launch(vnm::launch_pack_nat24(*out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -212,7 +220,7 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
             if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;
             if (!out[i]->values_tc || !out[i]->meta_tc) return VNM_ERR_ARG;
             if (!aligned16(out[i]->values_tc) || !aligned16(out[i]->meta_tc)) return VNM_ERR_ALIGN;
-            if (!nat24(g)) {
+            if (!nat24(g) && !w16(g)) {
                 L.values_tc = out[i]->values_tc;
                 L.meta_tc = out[i]->meta_tc;
             }
@@ -234,9 +242,11 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
         const vnm_status s = from_launch(vnm::launch_prune_pack(Ls[i], st));
         if (s) return s;
     }
-    for (int i = 0; i < n; ++i)  // natural 2:4 tensor-core forms, packed after the pass
-        if (out[i]->values_tc && nat24(&out[i]->g) && out[i]->g.rows_p > 0 && out[i]->g.nb_pad > 0) {
-            const vnm_status s = from_launch(vnm::launch_pack_nat24(*out[i], st));
+    for (int i = 0; i < n; ++i)  // natural 2:4 and window-16 tensor-core forms, packed after the pass
+        if (out[i]->values_tc && (nat24(&out[i]->g) || w16(&out[i]->g)) && out[i]->g.rows_p > 0 &&
+            out[i]->g.nb_pad > 0) {
+            const vnm_status s = from_launch(nat24(&out[i]->g) ? vnm::launch_pack_nat24(*out[i], st)
+                                                                : vnm::launch_pack_tc(*out[i], st));
             if (s) return s;
         }
     return VNM_OK;
@@ -300,8 +310,11 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
         // is not a multiple of 16 bytes (T % 8 bf16 / T % 4 fp32) would get up to 7 tokens past T written.  Those
         // shapes take the resident / streamed pair kernel (st.global with element-wise tails; tests/test_gpu_bounds.py).
         const bool ragged = (static_cast<int64_t>(T) * (y_dtype == VNM_BF16 ? 2 : 4)) % 16 != 0;
-        const bool tc3 = ragged || (force ? force >= 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192));
-        if (ragged) {
+        // the window-16 form runs in the single-CTA / pair kernels only (the resident pair kernel has no
+        // half-window stepping): a ragged Y^T row then takes the small-T or gather plan below
+        const bool win16 = g->M > 8;
+        const bool tc3 = !win16 && (ragged || (force ? force >= 3 : (g->M >= 5 && g->M <= 6 && n_rt >= 6 && n_mma <= 32 && T >= 8192)));
+        if (ragged && !win16) {
             const int rc = vnm::launch_spmm_tc3(L, -1, reinterpret_cast<cudaStream_t>(stream));
             if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
             return VNM_ERR_UNSUPPORTED;
@@ -310,9 +323,13 @@ vnm_status vnm_spmm(const uint16_t* XT, int64_t ldx, int32_t T, const vnm_packed
             const int rc = vnm::launch_spmm_tc3(L, force == 4 ? 0 : (force == 3 ? -1 : 1), reinterpret_cast<cudaStream_t>(stream));
             if (rc != vnm::kLaunchUnsupported) return from_launch(rc);
         }
-        const bool pair = force ? force == 2 : (n_stage >= 12 && n_rt % 2 == 0);
-        if (pair) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
-        return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
+        if (!(win16 && ragged)) {
+            const int n_stage16 = win16 ? (g->nb_pad / 2 + 3) / 4 : n_stage;
+            const bool pair = force ? force == 2 : (n_stage16 >= 12 && n_rt % 2 == 0);
+            if (pair) return from_launch(vnm::launch_spmm_tc2(L, reinterpret_cast<cudaStream_t>(stream)));
+            return from_launch(vnm::launch_spmm_tc(L, reinterpret_cast<cudaStream_t>(stream)));
+        }
+        if (!small && g->V != 64 && g->V != 128 && g->V != 256) return VNM_ERR_UNSUPPORTED;
     }
     if (small) return from_launch(vnm::launch_spmm_smallt(L, reinterpret_cast<cudaStream_t>(stream)));
     return from_launch(vnm::launch_spmm(L, reinterpret_cast<cudaStream_t>(stream)));

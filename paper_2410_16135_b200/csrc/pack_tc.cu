@@ -6,6 +6,10 @@
 // (block columns c0 < c1) sit at their own positions; each group is completed to exactly two entries with
 // zero values at the lowest free positions.  For M = 4 two blocks form one 8-channel window and the form is
 // A_n / A_i2 unchanged (col_idx is always 0,1,2,3).
+//
+// Window-16 form, 8 < M <= 16 with M % 4 != 0 (include/vnm.h): block b becomes the 16 channels [b*M, b*M + 16)
+// as four 2:4 groups; MMA 2j + h covers the half-windows h (groups 2h, 2h+1 = channels 8h .. 8h+7) of blocks
+// 4j .. 4j+3, so its B operand is the window-form one (K-group stride M rows) started 8h rows further.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -22,6 +26,7 @@ struct PackTcArgs {
     uint16_t* values_tc;
     uint32_t* meta_tc;
     int32_t V, M, rows_p, rows_w, nb_pad, ld_val, ld_meta, n_mma, n_stage, ld_tc;
+    int32_t w16;  // window-16 form (8 < M <= 16)
 };
 
 // the 8-nibble metadata word of MMA `mi` for row r (rows >= rows_p: zero weights, nibble 0x4)
@@ -30,6 +35,19 @@ __device__ uint32_t mma_word(const PackTcArgs& a, int r, int mi) {
     if (a.M == 4) return a.meta[static_cast<int64_t>(r) * a.ld_meta + mi];
     uint32_t w = 0;
     const uint8_t* ci_row = a.col_idx + static_cast<int64_t>(r / a.V) * a.nb_pad * 4;
+    if (a.w16) {  // MMA mi = 2j + h: half-windows h of blocks 4j .. 4j+3
+        const int j = mi >> 1, h = mi & 1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int b = 4 * j + i;
+            if (b >= a.nb_pad) { w |= 0x44u << (8 * i); continue; }
+            const uint32_t nib = (a.meta[static_cast<int64_t>(r) * a.ld_meta + b / 8] >> (4 * (b % 8))) & 0xFu;
+            const uint8_t* ci = ci_row + b * 4;
+            const int c0 = ci[nib & 3u], c1 = ci[nib >> 2];
+            w |= ((tc_encode_block16(c0, c1, 0, 0).nibs >> (8 * h)) & 0xFFu) << (8 * i);
+        }
+        return w;
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int b = 4 * mi + i;
@@ -51,6 +69,28 @@ __global__ void pack_tc_values_kernel(const PackTcArgs a) {
         uint32_t v = 0;
         if (r < a.rows_p) v = reinterpret_cast<const uint32_t*>(a.values + static_cast<int64_t>(r) * a.ld_val)[b];
         reinterpret_cast<uint32_t*>(a.values_tc + static_cast<int64_t>(r) * a.ld_tc)[b] = v;
+        return;
+    }
+    if (a.w16) {  // 8 values: half h -> MMA 2(b/4) + h, slots 4(b%4) .. +3
+        uint16_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (r < a.rows_p) {
+            const uint32_t nib = (a.meta[static_cast<int64_t>(r) * a.ld_meta + b / 8] >> (4 * (b % 8))) & 0xFu;
+            const uint8_t* ci = a.col_idx + (static_cast<int64_t>(r / a.V) * a.nb_pad + b) * 4;
+            const int c0 = ci[nib & 3u], c1 = ci[nib >> 2];
+            const uint16_t v0 = a.values[static_cast<int64_t>(r) * a.ld_val + 2 * b];
+            const uint16_t v1 = a.values[static_cast<int64_t>(r) * a.ld_val + 2 * b + 1];
+            const TcBlock16 t = tc_encode_block16(c0, c1, v0, v1);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = t.val[q];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint2 pk;
+            pk.x = static_cast<uint32_t>(o[4 * h]) | (static_cast<uint32_t>(o[4 * h + 1]) << 16);
+            pk.y = static_cast<uint32_t>(o[4 * h + 2]) | (static_cast<uint32_t>(o[4 * h + 3]) << 16);
+            *reinterpret_cast<uint2*>(a.values_tc + static_cast<int64_t>(r) * a.ld_tc + 16 * (2 * (b / 4) + h) +
+                                      4 * (b % 4)) = pk;
+        }
         return;
     }
     uint16_t out[4] = {0, 0, 0, 0};
@@ -267,7 +307,8 @@ int launch_pack_tc(const vnm_packed& P, cudaStream_t stream) {
     a.nb_pad = g.nb_pad;
     a.ld_val = g.ld_val;
     a.ld_meta = g.ld_meta;
-    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+    a.w16 = g.M > 8;
+    a.n_mma = a.w16 ? g.nb_pad / 2 : g.nb_pad / (g.M == 4 ? 8 : 4);
     a.n_stage = (a.n_mma + 3) / 4;
     a.ld_tc = 16 * a.n_mma;
     const int64_t nv = static_cast<int64_t>(a.rows_w) * a.nb_pad;

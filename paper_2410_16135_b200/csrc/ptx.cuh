@@ -342,7 +342,7 @@ namespace vnm {
 // n (2 or 4) sparse MMAs k = 0..n-1: A descriptor + 2 (32 B) per k, B descriptor + b_step per k, metadata
 // column e for k < 2 and e + 2 for k >= 2, id2 = k & 1 (idesc0 / idesc1); `accumulate` applies to k = 0.
 template <int CG>
-__device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t bd, uint64_t b_step, uint32_t e,
+__device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t bd, uint64_t b_step, uint64_t b_step2, uint32_t e,
                                              uint32_t idesc0, uint32_t idesc1, uint32_t accumulate, uint32_t n) {
     static_assert(CG == 1 || CG == 2, "cta_group");
     if constexpr (CG == 1) {
@@ -353,14 +353,14 @@ __device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t b
             "setp.eq.b32 one, 0, 0;\n\t"
             "setp.gt.and.u32 p3, %8, 2, p;\n\t"
             "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
-            "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"
+            "add.s64 b1, %2, %7;\n\tadd.s64 b2, %2, %9;\n\tadd.s64 b3, b2, %7;\n\t"
             "add.u32 e2, %3, 2;\n\t"
             "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%3], %4, acc;\n\t"
             "@p tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a1, b1, [%3], %5, one;\n\t"
             "@p3 tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a2, b2, [e2], %4, one;\n\t"
             "@p3 tcgen05.mma.sp.cta_group::1.kind::f16 [%0], a3, b3, [e2], %5, one;\n\t"
             "}" ::"r"(d),
-            "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n)
+            "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n), "l"(b_step2)
             : "memory");
     } else {
         asm volatile(
@@ -370,16 +370,24 @@ __device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t b
             "setp.eq.b32 one, 0, 0;\n\t"
             "setp.gt.and.u32 p3, %8, 2, p;\n\t"
             "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
-            "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"
+            "add.s64 b1, %2, %7;\n\tadd.s64 b2, %2, %9;\n\tadd.s64 b3, b2, %7;\n\t"
             "add.u32 e2, %3, 2;\n\t"
             "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%3], %4, acc;\n\t"
             "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a1, b1, [%3], %5, one;\n\t"
             "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a2, b2, [e2], %4, one;\n\t"
             "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a3, b3, [e2], %5, one;\n\t"
             "}" ::"r"(d),
-            "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n)
+            "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n), "l"(b_step2)
             : "memory");
     }
+}
+// the window form: MMA i of the stage reads B at bd + i * b_step.  The window-16 form (8 < M < 16) interleaves two
+// steps: MMAs 0 / 1 read the two half-windows of one block group (bd, bd + b_step = +8 rows), MMAs 2 / 3 those of
+// the next (bd + b_step2, + b_step)
+template <int CG>
+__device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t bd, uint64_t b_step, uint32_t e,
+                                             uint32_t idesc0, uint32_t idesc1, uint32_t accumulate, uint32_t n) {
+    mma_sp_stage<CG>(d, ad, bd, b_step, 2 * b_step, e, idesc0, idesc1, accumulate, n);
 }
 // tcgen05.cp 128x128b (smem [128 rows][16 B] -> TMEM), elected lane of a converged warp
 template <int CG>

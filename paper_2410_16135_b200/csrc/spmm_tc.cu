@@ -138,7 +138,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int q = 0, tl = 0;
         const uint32_t idesc0 = idesc_bf16(128, NT, true, 0, true);
         const uint32_t idesc1 = idesc_bf16(128, NT, true, 1, true);
-        const uint64_t b_step = (a.M == 4 ? 32u : 4u * a.M) * 128u >> 4;  // B descriptor advance per MMA
+        // B descriptor advance per MMA (window-16 form, M > 8: +8 rows to the second half-windows, then the next
+        // block group 4M rows on: ptx.cuh mma_sp_stage)
+        const uint64_t b_step = (a.M == 4 ? 32u : a.M > 8 ? 8u : 4u * a.M) * 128u >> 4;
+        const uint64_t b_step2 = a.M > 8 ? (4u * a.M * 128u) >> 4 : 2 * b_step;
         const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
         const uint32_t b_lbo = a.rb * 128;
         for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++tl) {
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < RT; ++j)
                     mma_sp_stage<1>(tmem + (acc * RT + j) * NT, sdesc(smem_u32(base + j * kABytes), 16, 1024, kLayoutSW128),
-                                    bd, b_step, meta_s + 4 * j, idesc0, idesc1, st > 0 ? 1u : 0u, n);
+                                    bd, b_step, b_step2, meta_s + 4 * j, idesc0, idesc1, st > 0 ? 1u : 0u, n);
                 mma_commit_elect(&empty[s]);
             }
             mma_commit_elect(&tmem_full[acc]);
@@ -299,8 +302,9 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
     constexpr int kChunks = NT / 64;
     const vnm_geom& g = L.P->g;
     a.n_tt = (L.T + NT - 1) / NT;
-    a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
-    const int need = g.M == 4 ? 128 : 15 * g.M + 8;  // rows one stage's windows touch (block 15: 15M .. 15M+7)
+    // rows one stage's windows touch: window form block 15 (15M .. 15M+7); window-16 form block 7 (7M .. 7M+15)
+    a.rows_stage = g.M == 4 ? 128 : g.M > 8 ? 8 * g.M : 16 * g.M;
+    const int need = g.M == 4 ? 128 : g.M > 8 ? 7 * g.M + 16 : 15 * g.M + 8;
     a.rb = (need + 7) / 8 * 8;
     a.b_stage_bytes = static_cast<uint32_t>(kChunks * a.rb * 128);
     a.stage_bytes = RT * (kABytes + kEBytes) + a.b_stage_bytes;
@@ -344,7 +348,8 @@ int launch_cfg(const SpmmLaunch& L, TcArgs a, cudaStream_t stream) {
 
 int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
-    if (g.V < 32 || g.V > 128 || g.M > 8) return kLaunchUnsupported;  // window form: rows independent of V
+    // window form (M <= 8) / window-16 form (8 < M < 16): rows independent of V
+    if (g.V < 32 || g.V > 128 || g.M > 15) return kLaunchUnsupported;
     TcArgs a;
     a.meta_tc = L.P->meta_tc;
     a.YT = L.YT;
@@ -353,7 +358,7 @@ int launch_spmm_tc(const SpmmLaunch& L, cudaStream_t stream) {
     a.y_bf16 = L.y_dtype == VNM_BF16;
     a.rows = g.rows;
     a.M = g.M;
-    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+    a.n_mma = g.M > 8 ? g.nb_pad / 2 : g.nb_pad / (g.M == 4 ? 8 : 4);
     a.n_stage = (a.n_mma + 3) / 4;
     a.n_rt = (g.rows_p + 127) / 128;
     // Plan (measured, profiles/r01_*): long K (many stages per tile) -> NT = 256, one accumulator (the

@@ -222,7 +222,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
             int q = 0, tl = 0, rp, tt;
             const uint32_t idesc0 = idesc_bf16(256, NT, true, 0, true);
             const uint32_t idesc1 = idesc_bf16(256, NT, true, 1, true);
-            const uint64_t b_step = (a.M == 4 ? 32u : 4u * a.M) * 128u >> 4;  // B descriptor advance per MMA
+            // B descriptor advance per MMA (window-16 form, M > 8: +8 rows to the second half-windows, then the next
+            // block group 4M rows on: ptx.cuh mma_sp_stage)
+            const uint64_t b_step = (a.M == 4 ? 32u : a.M > 8 ? 8u : 4u * a.M) * 128u >> 4;
+            const uint64_t b_step2 = a.M > 8 ? (4u * a.M * 128u) >> 4 : 2 * b_step;
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
             const uint32_t b_lbo = a.rb * 128;
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
@@ -247,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     const uint32_t a0 = a.a_res ? smem_u32(smem + st * kABytes) : smem_u32(base);
                     const int left = a.n_mma - st * 4;
                     mma_sp_stage<2>(d_tmem, sdesc(a0, 16, 1024, kLayoutSW128),
-                                    sdesc(smem_u32(base + b_off), b_lbo, sbo, kLayoutSW128), b_step, meta_s, idesc0,
+                                    sdesc(smem_u32(base + b_off), b_lbo, sbo, kLayoutSW128), b_step, b_step2, meta_s, idesc0,
                                     idesc1, st > 0 ? 1u : 0u, left < 4 ? static_cast<uint32_t>(left) : 4u);
                     mma_commit_pair_elect(&empty[s], 0x3);
                 }
@@ -410,17 +413,19 @@ int launch_nt(const SpmmLaunch& L, Tc2Args a, cudaStream_t stream) {
 // T > 64, 4 <= M <= 8 (window form).  Returns kLaunchUnsupported when the configuration does not fit.
 int launch_spmm_tc2(const SpmmLaunch& L, cudaStream_t stream) {
     const vnm_geom& g = L.P->g;
-    if (g.M > 8) return kLaunchUnsupported;
+    if (g.M > 15) return kLaunchUnsupported;  // M > 8: the window-16 form (include/vnm.h)
     Tc2Args a;
     a.T = L.T;
     a.rows = g.rows;
     a.M = g.M;
-    a.n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+    a.n_mma = g.M > 8 ? g.nb_pad / 2 : g.nb_pad / (g.M == 4 ? 8 : 4);
     a.n_stage = (a.n_mma + 3) / 4;
     a.n_rt = (g.rows_p + 127) / 128;
     a.n_rp = (a.n_rt + 1) / 2;
-    a.rows_stage = g.M == 4 ? 128 : 16 * g.M;
-    const int need = g.M == 4 ? 128 : 15 * g.M + 8;  // X^T rows one stage's windows touch (block 15: 15M .. 15M+7)
+    // X^T rows per stage and rows one stage's windows touch: window form 16 blocks (block 15: 15M .. 15M+7);
+    // window-16 form 8 blocks (block 7: 7M .. 7M+15)
+    a.rows_stage = g.M == 4 ? 128 : g.M > 8 ? 8 * g.M : 16 * g.M;
+    const int need = g.M == 4 ? 128 : g.M > 8 ? 7 * g.M + 16 : 15 * g.M + 8;
     a.rb = (need + 7) / 8 * 8;
     a.b_bytes = static_cast<uint32_t>(2 * a.rb * 128);
     // long K: 256-token tiles, one accumulator (the per-tile hand-off is amortised over many stages);

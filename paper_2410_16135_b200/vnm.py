@@ -180,8 +180,9 @@ class Packed:
 
 
 def tc_applies(V: int, M: int) -> bool:
-    """The tensor-core form exists for this (V, M): window form (M <= 8) or natural 2:4 form (M % 4 == 0)."""
-    return 32 <= V <= 128 and (M <= 8 or M % 4 == 0)
+    """The tensor-core form exists for this (V, M): window form (M <= 8), natural 2:4 form (M % 4 == 0) or
+    window-16 form (8 < M < 16)."""
+    return 32 <= V <= 128 and (M <= 8 or M % 4 == 0 or M < 16)
 
 
 def tc_bytes(g: Geom) -> tuple[int, int]:
@@ -191,7 +192,7 @@ def tc_bytes(g: Geom) -> tuple[int, int]:
 
 def pack_tc(P: Packed) -> Packed:
     """Fill the tensor-core form of P (allocating it on P's device): the window form for 4 <= M <= 8, the
-    natural 2:4 form for M % 4 == 0 (include/vnm.h); 32 <= V <= 128 only."""
+    natural 2:4 form for M % 4 == 0, the window-16 form for the other M < 16 (include/vnm.h); 32 <= V <= 128 only."""
     _require_cuda(P.values)
     nv, nm = tc_bytes(P.g)
     if nv == 0:

@@ -96,11 +96,18 @@ def test_status_codes_without_launch():
     # workspace init: nothing to do for 0 bytes; NULL with bytes is an argument error (no launch)
     assert L.vnm_spmm_workspace_init(None, 0, None) == vnm.VNM_OK
     assert L.vnm_spmm_workspace_init(None, 64, None) == vnm.VNM_ERR_ARG
-    # the tensor-core form exists for M <= 8 (window) and M % 4 == 0 (natural 2:4), not for M = 9 / 13
-    for M, has in [(5, True), (8, True), (12, True), (16, True), (9, False), (13, False)]:
+    # the tensor-core form exists for M <= 8 (window), M % 4 == 0 (natural 2:4) and the other M < 16 (window-16),
+    # not for M = 17 / 18; V outside [32, 128] never
+    for M, has in [(5, True), (8, True), (12, True), (16, True), (9, True), (13, True), (15, True), (17, False),
+                   (18, False), (20, True)]:
         gm = vnm.geometry(256, 1000, 64, M)
         assert (L.vnm_bytes(ctypes.byref(gm), 4) > 0) == has and (L.vnm_bytes(ctypes.byref(gm), 5) > 0) == has
         assert vnm.tc_applies(64, M) == has
+    assert L.vnm_bytes(ctypes.byref(vnm.geometry(256, 1000, 256, 13)), 4) == 0
+    # window-16 form: 8 values per block (two MMAs of 16 values per 4 blocks), meta_tc one word per MMA and lane
+    g13 = vnm.geometry(300, 1000, 128, 13)  # cols_p 1001, nb 77, nb_pad 80, rows_w 384
+    assert L.vnm_bytes(ctypes.byref(g13), 4) == 384 * 16 * 40 * 2
+    assert L.vnm_bytes(ctypes.byref(g13), 5) == 3 * 10 * 128 * 4 * 4
     for s in (0, -1, -2, -3, -4, -5):
         assert vnm.status_string(s)
 
