@@ -41,7 +41,9 @@ namespace {
 
 // NW warps per CTA: 8 (3 CTAs per SM, large weights) or 16 (one tile per CTA for small weights: the per-tile
 // latency halves, the row pass being the longest phase)
-constexpr int kCB = 32;  // column blocks per tile (one per lane in the row pass)
+constexpr int kCB = 32;  // column blocks per tile (one per lane in the row pass) for M <= 8
+// 8 < M <= 16: 16 blocks per tile (tile columns 16M <= 256, one TMA box; the row pass runs 2 rows per warp step)
+__host__ __device__ constexpr int kcb_of(int M) { return M > 8 ? 16 : 32; }
 
 struct Prune2Args {
     uint32_t* mask_out;  // may be null
@@ -96,7 +98,9 @@ struct Batch {
 template <int V, int M, int NW, int MINB, bool LEAN>
 __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_constant__ Batch B) {
     constexpr int kWarps = NW, kThreads = 32 * NW;
-    constexpr int TC = kCB * M;  // tile columns (<= 256)
+    constexpr int kCB = kcb_of(M);  // column blocks per tile (shadows the namespace constant)
+    constexpr int RI = 32 / kCB;    // rows per warp step in the row pass (lane = block + kCB * row)
+    constexpr int TC = kCB * M;     // tile columns (<= 256)
     constexpr int P = TC / 2;    // words per W row in shared memory
     constexpr int RPW = V / kWarps;
     constexpr uint32_t kWBytes = V * TC * 2, kSBytes = V * TC * 4;
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         const int p = info.x, bx = info.y, by = info.z;
         const Prune2Args& a = B.a[p];
         const Maps& tm = B.tm[p];
-        const bool has_score = !LEAN && a.has_score, tc = !LEAN && a.has_tc;
+        const bool has_score = !LEAN && a.has_score, tc = M <= 8 && !LEAN && a.has_tc;
         uint32_t* const mask_out = LEAN ? nullptr : a.mask_out;
         const int b0 = bx * kCB, r0 = by * V;
         PTRACE(1)
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         PTRACE(2)
 
         // ---- top-4 columns per block (lane = block; ties -> smaller column)
-        if (warp == 0) {
+        if (warp == 0 && lane < kCB) {
             const int b = lane;
             float tv[4] = {-1.f, -1.f, -1.f, -1.f};
             int ti[4] = {0, 1, 2, 3};
@@ -251,20 +255,21 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
 
         // ---- rows: lane = block b, this warp's rows r = warp + 8 i.  Pad blocks (b >= nb) hold zero fill
         // and come out as the pad encoding by themselves (kept {0,1,2,3}, rows keep positions 0,1, values 0).
-        const int b = lane;
+        // (kCB = 16, M > 8: lanes 16-31 take the next row of the warp's pair: r = warp + kWarps (2 i + lane / 16))
+        const int b = lane % kCB, rs = lane / kCB;
         const uint32_t kp = sKp[b];
         const int k0 = kp & 0xFF, k1 = (kp >> 8) & 0xFF, k2 = (kp >> 16) & 0xFF, k3 = kp >> 24;
-        const uint16_t* wcol = reinterpret_cast<const uint16_t*>(sW) + b * M + warp * TC;
-        const float* scol = sS + b * M + warp * TC;
+        const uint16_t* wcol = reinterpret_cast<const uint16_t*>(sW) + b * M + (warp + kWarps * rs) * TC;
+        const float* scol = sS + b * M + (warp + kWarps * rs) * TC;
         uint32_t upos = 0;  // kept positions chosen by some row
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            const int r = warp + kWarps * i;
-            const uint16_t* wr = wcol + kWarps * i * TC;
+        for (int i = 0; i < RPW / RI; ++i) {
+            const int r = warp + kWarps * (RI * i + rs);
+            const uint16_t* wr = wcol + kWarps * RI * i * TC;
             const uint32_t w0 = wr[k0], w1 = wr[k1], w2 = wr[k2], w3 = wr[k3];
             uint32_t t1, t2;
             if (has_score) {
-                const float* sr = scol + kWarps * i * TC;
+                const float* sr = scol + kWarps * RI * i * TC;
                 const unsigned long long q0 = (static_cast<unsigned long long>(__float_as_uint(fabsf(sr[k0]))) << 2) | 3u;
                 const unsigned long long q1 = (static_cast<unsigned long long>(__float_as_uint(fabsf(sr[k1]))) << 2) | 2u;
                 const unsigned long long q2 = (static_cast<unsigned long long>(__float_as_uint(fabsf(sr[k2]))) << 2) | 1u;
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         uint32_t ci = ((up & 1u) << k0) | (((up >> 1) & 1u) << k1) | (((up >> 2) & 1u) << k2) | (((up >> 3) & 1u) << k3);
         constexpr uint32_t colmask = (1u << M) - 1u;
         for (int need = 4 - __popc(ci); need > 0; --need) ci |= 1u << (__ffs(~ci & colmask) - 1);
-        if (a.has_values && warp == 0 && b0 + b < a.nb_pad) {
+        if (a.has_values && warp == 0 && lane < kCB && b0 + b < a.nb_pad) {
             uint32_t word = 0, m = ci;
 #pragma unroll
             for (int q = 0; q < 4; ++q) { word |= static_cast<uint32_t>(__ffs(m) - 1) << (8 * q); m &= m - 1; }
@@ -329,8 +334,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                 int pos[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) pos[q] = __popc(ci & ((1u << kc[q]) - 1u));
-                for (int i = 0; i < RPW; ++i) {
-                    const int r = warp + kWarps * i;
+                for (int i = 0; i < RPW / RI; ++i) {
+                    const int r = warp + kWarps * (RI * i + rs);
                     const uint32_t n = sNib[r * kCB + b];
                     const int lo = n & 3, hi = n >> 2;
                     const int plo = lo == 0 ? pos[0] : (lo == 1 ? pos[1] : (lo == 2 ? pos[2] : pos[3]));
@@ -343,10 +348,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         if (threadIdx.x < kCB) sUni[threadIdx.x] = 0u;  // next tile (every read of it is above)
 
         // ---- A_i2 words: 8 nibble bytes -> one word (byte permutes)
-        for (int t = threadIdx.x; t < V * 4; t += kThreads) {
-            const uint2 x = *reinterpret_cast<const uint2*>(sNib + (t >> 2) * kCB + 8 * (t & 3));
+        constexpr int kMW = kCB / 8;  // A_i2 words per row of the tile
+        for (int t = threadIdx.x; t < V * kMW; t += kThreads) {
+            const uint2 x = *reinterpret_cast<const uint2*>(sNib + (t / kMW) * kCB + 8 * (t % kMW));
             const uint32_t lo = x.x | (x.x >> 4), hi = x.y | (x.y >> 4);
-            sMet[t] = __byte_perm(lo, hi, 0x6420);
+            const uint32_t word = __byte_perm(lo, hi, 0x6420);
+            if constexpr (kCB == 32) {
+                sMet[t] = word;
+            } else if (a.has_values && b0 / 8 + t % kMW < a.nb_pad / 8) {  // 16-block tiles: straight to A_i2
+                a.meta[static_cast<int64_t>(r0 + t / kMW) * a.ld_meta + b0 / 8 + t % kMW] = word;
+            }
         }
         const int cbv = min(kCB, a.nb_pad - b0);  // blocks of this tile inside nb_pad (a multiple of 8)
         if (a.has_values && b0 + cbv == a.nb_pad) {  // last column tile: row padding words (Q20)
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         if (threadIdx.x == 0) {
             if (a.has_values) {
                 tma_store_2d(&tm.val, 2 * b0, r0, sVal);
-                tma_store_2d(&tm.met, b0 / 8, r0, sMet);
+                if constexpr (kCB == 32) tma_store_2d(&tm.met, b0 / 8, r0, sMet);
             }
             if (tc) tma_store_2d(&tm.tcv, (M == 4 ? 2 : 4) * b0, r0, M == 4 ? static_cast<const void*>(sVal) : sTcv);
             bulk_commit();
@@ -455,6 +466,14 @@ cudaError_t launch_m(int M, const Batch& B, size_t smem, cudaStream_t st) {
         case 6: return launch2<V, 6, NW, MINB, LEAN>(B, smem, st);
         case 7: return launch2<V, 7, NW, MINB, LEAN>(B, smem, st);
         case 8: return launch2<V, 8, NW, MINB, LEAN>(B, smem, st);
+        case 9: return launch2<V, 9, NW, MINB, LEAN>(B, smem, st);
+        case 10: return launch2<V, 10, NW, MINB, LEAN>(B, smem, st);
+        case 11: return launch2<V, 11, NW, MINB, LEAN>(B, smem, st);
+        case 12: return launch2<V, 12, NW, MINB, LEAN>(B, smem, st);
+        case 13: return launch2<V, 13, NW, MINB, LEAN>(B, smem, st);
+        case 14: return launch2<V, 14, NW, MINB, LEAN>(B, smem, st);
+        case 15: return launch2<V, 15, NW, MINB, LEAN>(B, smem, st);
+        case 16: return launch2<V, 16, NW, MINB, LEAN>(B, smem, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -474,14 +493,17 @@ cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
 
 static bool L_unsupported(const PruneLaunch& L) {
     const vnm_geom& g = *L.g;
-    return L.mask_in || g.V < 32 || g.V > 128 || g.M > 8 || g.rows == 0 || g.cols == 0 ||
-           (L.values_tc && (!L.meta_tc || !L.values));
+    // M > 8: 16-block tiles, canonical outputs only (the window-16 / natural 2:4 forms are packed after the pass;
+    // a 32-bit mask word can straddle two 16M-column tiles, so a mask output takes prune.cu)
+    return L.mask_in || g.V < 32 || g.V > 128 || g.M > 16 || g.rows == 0 || g.cols == 0 ||
+           (L.values_tc && (!L.meta_tc || !L.values)) || (g.M > 8 && (L.values_tc || L.mask_out));
 }
 
 // Per-problem tensor maps and arguments (+ the pad-row memsets of the window form); false: not applicable.
 static bool setup_problem(const PruneLaunch& L, Maps& tm, Prune2Args& a, cudaStream_t stream) {
     const vnm_geom& g = *L.g;
-    if (L.mask_in || g.V < 32 || g.V > 128 || g.M > 8 || g.rows == 0 || g.cols == 0) return false;
+    if (L_unsupported(L)) return false;
+    const int kCB = kcb_of(g.M);
     const bool has_score = L.score != nullptr, tc = L.values_tc != nullptr, vals = L.values != nullptr;
     if (tc && (!L.meta_tc || !vals)) return false;
     const int tile_cols = kCB * g.M;
@@ -500,9 +522,10 @@ static bool setup_problem(const PruneLaunch& L, Maps& tm, Prune2Args& a, cudaStr
         if (!encode_2d(&tm.val, L.values, static_cast<uint64_t>(g.ld_val), static_cast<uint64_t>(g.rows_p),
                        static_cast<uint64_t>(g.ld_val) * 2, 2 * kCB, g.V, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                        CU_TENSOR_MAP_SWIZZLE_NONE) ||
-            !encode_2d(&tm.met, L.meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
-                       static_cast<uint64_t>(g.ld_meta) * 4, kCB / 8, g.V, CU_TENSOR_MAP_DATA_TYPE_UINT32,
-                       CU_TENSOR_MAP_SWIZZLE_NONE))
+            (kCB == 32 &&  // 16-block tiles: 8-byte A_i2 rows, below the TMA box minimum -> stored by the threads
+             !encode_2d(&tm.met, L.meta, static_cast<uint64_t>(g.nb_pad / 8), static_cast<uint64_t>(g.rows_p),
+                        static_cast<uint64_t>(g.ld_meta) * 4, kCB / 8, g.V, CU_TENSOR_MAP_DATA_TYPE_UINT32,
+                        CU_TENSOR_MAP_SWIZZLE_NONE)))
             return false;
     }
     if (tc) {
@@ -551,11 +574,12 @@ int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream) {
     for (int i = 0; i < n; ++i) {
         if (!setup_problem(Ls[i], B.tm[i], B.a[i], stream)) return kLaunchUnsupported;
         const vnm_geom& g = *Ls[i].g;
-        B.tile0[i + 1] = B.tile0[i] + ((g.nb_pad + kCB - 1) / kCB) * (g.rows_p / V);
+        B.tile0[i + 1] = B.tile0[i] + ((g.nb_pad + kcb_of(M) - 1) / kcb_of(M)) * (g.rows_p / V);
         B.any_score |= B.a[i].has_score;
         B.any_mask |= Ls[i].mask_out != nullptr;
         B.any_tc |= B.a[i].has_tc;
     }
+    const int kCB = kcb_of(M);
     const int tile_cols = kCB * M;
     const size_t buf = static_cast<size_t>(V) * tile_cols * 2 + (B.any_score ? static_cast<size_t>(V) * tile_cols * 4 : 0);
     const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (B.any_tc ? 4 + 8 : 4) + static_cast<size_t>(V) * 16 +

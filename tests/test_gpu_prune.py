@@ -349,3 +349,54 @@ def test_batched_eight_entries_vs_oracle():
         assert np.array_equal(u32(mk), mask_ref)
         v, c, m = packed_np(P)
         assert np.array_equal(v, v_ref) and np.array_equal(c, c_ref) and np.array_equal(m, m_ref)
+
+
+def _packed_vs_oracle(P, W, V, M):
+    mask_ref, v_ref, c_ref, m_ref = oracle.prune_pack(W, V, M)
+    v, c, m = packed_np(P)
+    assert np.array_equal(v, v_ref), "A_n values"
+    assert np.array_equal(c, c_ref), "A_i1 col_idx"
+    assert np.array_equal(m, m_ref), "A_i2 meta"
+
+
+@pytest.mark.parametrize("V", [32, 64, 128])
+@pytest.mark.parametrize("M", [9, 10, 11, 12, 13, 14, 15, 16])
+@pytest.mark.parametrize("rows,cols,kind", [(200, 333, "outlier"), (128, 1000, "int"), (256, 517, "wide")])
+def test_prune2_m9_to_16_bitexact(V, M, rows, cols, kind):
+    """prune2 for 8 < M <= 16 (16-block tiles, two rows per warp step in the row pass; the paper's 128:2:9 .. 13
+    points): canonical A_n / A_i1 / A_i2 byte for byte against the oracle, single and batched (no mask
+    output: a mask routes to prune.cu), tie-heavy integers and wide exponents included."""
+    W = synth.weights(rows, cols, seed=rows + cols + V + M, kind=kind)
+    W2 = synth.weights(rows + 64, cols, seed=rows + cols + V + M + 1, kind=kind)
+    Wd, W2d = to_dev_bf16(W), to_dev_bf16(W2)
+    P = vnm.prune_compress(Wd, V, M)
+    B = vnm.prune_compress_batched([Wd, W2d], V, M)
+    torch.cuda.synchronize()
+    _packed_vs_oracle(P, W, V, M)
+    _packed_vs_oracle(B[0], W, V, M)
+    _packed_vs_oracle(B[1], W2, V, M)
+
+
+@pytest.mark.parametrize("V,M", [(128, 13), (128, 9), (64, 11)])
+def test_prune2_m_gt_8_llama_shapes(V, M):
+    """Llama2-7B up / down weights at the paper's V = 128 / M > 8 points through the batched pass (the bench's)."""
+    Ws = [synth.weights(11008, 4096, seed=M, kind="outlier"), synth.weights(4096, 11008, seed=M + 1, kind="outlier")]
+    Ps = vnm.prune_compress_batched([to_dev_bf16(W) for W in Ws], V, M, tc=True)
+    torch.cuda.synchronize()
+    for P, W in zip(Ps, Ws):
+        _packed_vs_oracle(P, W, V, M)
+
+
+def test_prune2_runs_for_m_gt_8():
+    """The M > 8 batched pass really is prune2 (its trace line names it), not the prune.cu fallback."""
+    import os
+    import subprocess
+    import sys
+    code = ("import torch\nfrom paper_2410_16135_b200 import synth, vnm\nfrom tests.gpu_util import to_dev_bf16\n"
+            "W = to_dev_bf16(synth.weights(1024, 4096, seed=1))\n"
+            "vnm.prune_compress_batched([W, W], 128, 13, tc=True)\ntorch.cuda.synchronize()\nprint('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VNM_PRUNE_TRACE="1", PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+    assert "prune2 V=128 M=13" in r.stderr, r.stderr[-2000:]
