@@ -182,15 +182,13 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
         if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;  // the natural 2:4 form packed after the pass (M % 4 == 0)
         if (!out->values_tc || !out->meta_tc) return VNM_ERR_ARG;
         if (!aligned16(out->values_tc) || !aligned16(out->meta_tc)) return VNM_ERR_ALIGN;
-        if (!nat24(g) && !w16(g)) {
+        if (!nat24(g)) {  // window / window-16 form: written by the pass itself
             L.values_tc = out->values_tc;
             L.meta_tc = out->meta_tc;
         }
     }
     const vnm_status st = from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
-    if (st || !out->values_tc) return st;
-    if (w16(g)) return from_launch(vnm::launch_pack_tc(*out, reinterpret_cast<cudaStream_t>(stream)));
-    if (!nat24(g)) return st;
+    if (st || !out->values_tc || !nat24(g)) return st;
     return from_launch(vnm::launch_pack_nat24(*out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -220,7 +218,7 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
             if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;
             if (!out[i]->values_tc || !out[i]->meta_tc) return VNM_ERR_ARG;
             if (!aligned16(out[i]->values_tc) || !aligned16(out[i]->meta_tc)) return VNM_ERR_ALIGN;
-            if (!nat24(g) && !w16(g)) {
+            if (!nat24(g)) {
                 L.values_tc = out[i]->values_tc;
                 L.meta_tc = out[i]->meta_tc;
             }
@@ -242,11 +240,9 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
         const vnm_status s = from_launch(vnm::launch_prune_pack(Ls[i], st));
         if (s) return s;
     }
-    for (int i = 0; i < n; ++i)  // natural 2:4 and window-16 tensor-core forms, packed after the pass
-        if (out[i]->values_tc && (nat24(&out[i]->g) || w16(&out[i]->g)) && out[i]->g.rows_p > 0 &&
-            out[i]->g.nb_pad > 0) {
-            const vnm_status s = from_launch(nat24(&out[i]->g) ? vnm::launch_pack_nat24(*out[i], st)
-                                                                : vnm::launch_pack_tc(*out[i], st));
+    for (int i = 0; i < n; ++i)  // natural 2:4 tensor-core forms, packed after the pass
+        if (out[i]->values_tc && nat24(&out[i]->g) && out[i]->g.rows_p > 0 && out[i]->g.nb_pad > 0) {
+            const vnm_status s = from_launch(vnm::launch_pack_nat24(*out[i], st));
             if (s) return s;
         }
     return VNM_OK;

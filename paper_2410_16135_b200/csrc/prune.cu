@@ -476,6 +476,23 @@ int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
         const int rc = launch_prune2(L, stream);
         if (rc != kLaunchUnsupported) return rc;
     }
+    if (L.values_tc && g.M > 8) {
+        // the window-16 form (8 < M < 16) is written fused by prune2 only: here the canonical arrays first, then
+        // the form packed from them (pack_tc.cu; identical bytes)
+        PruneLaunch Lc = L;
+        Lc.values_tc = nullptr;
+        Lc.meta_tc = nullptr;
+        const int rc = launch_prune_pack(Lc, stream);
+        if (rc) return rc;
+        vnm_packed P;
+        P.g = g;
+        P.values = L.values;
+        P.col_idx = L.col_idx;
+        P.meta = L.meta;
+        P.values_tc = L.values_tc;
+        P.meta_tc = L.meta_tc;
+        return launch_pack_tc(P, stream);
+    }
     const bool from_mask = L.mask_in != nullptr;
     const bool has_score = L.score != nullptr;
     int CB = 0;

@@ -101,6 +101,9 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
     constexpr int kCB = kcb_of(M);  // column blocks per tile (shadows the namespace constant)
     constexpr int RI = 32 / kCB;    // rows per warp step in the row pass (lane = block + kCB * row)
     constexpr int TC = kCB * M;     // tile columns (<= 256)
+    // window-16 form (8 < M < 16, M % 4 != 0; include/vnm.h): 8 values per block, 4 group nibbles (u16)
+    constexpr bool kW16 = M > 8 && M % 4 != 0;
+    constexpr int kTcvWords = kW16 ? 4 : 2;  // 32-bit words of window values per block
     constexpr int P = TC / 2;    // words per W row in shared memory
     constexpr int RPW = V / kWarps;
     constexpr uint32_t kWBytes = V * TC * 2, kSBytes = V * TC * 4;
@@ -111,14 +114,14 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
     const uint32_t buf_bytes = kWBytes + (B.any_score ? kSBytes : 0);
     uint32_t* sVal = reinterpret_cast<uint32_t*>(smem + 2 * buf_bytes);    // [V][kCB] A_n pairs
     uint2* sTcv = reinterpret_cast<uint2*>(sVal + V * kCB);                 // [V][kCB] window values (M > 4; any_tc)
-    uint32_t* sMet = reinterpret_cast<uint32_t*>(sTcv + (B.any_tc ? V * kCB : 0));  // [V][4] A_i2 words
+    uint32_t* sMet = reinterpret_cast<uint32_t*>(sTcv) + (B.any_tc ? V * kCB * kTcvWords : 0);  // [V][4] A_i2 words
     float* sL = reinterpret_cast<float*>(sMet + V * 4);                     // [TC] column L1
     uint32_t* sKp = reinterpret_cast<uint32_t*>(sL + 256);                  // [kCB] kept columns, 8 bits each
     uint32_t* sUni = sKp + kCB;                                             // [kCB] kept positions carrying bits
     uint2* sTab = reinterpret_cast<uint2*>(sUni + kCB);                     // [8 * 8] window-form encodings
     uint32_t* sBits = reinterpret_cast<uint32_t*>(sTab + 64);               // [V][kCB] (mask_out)
     uint8_t* sNib = reinterpret_cast<uint8_t*>(sBits + (B.any_mask ? V * kCB : 0));  // [V][kCB] A_i2 nibbles
-    uint8_t* sTcn = sNib + V * kCB;                                                   // [V][kCB] window nibbles
+    uint8_t* sTcn = sNib + V * kCB;  // [V][kCB] window nibbles (u16 for the window-16 form)
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ int3 sInfo[2];  // (problem, column tile, row tile) of the tile in each buffer, set by its issuer
 
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         const int p = info.x, bx = info.y, by = info.z;
         const Prune2Args& a = B.a[p];
         const Maps& tm = B.tm[p];
-        const bool has_score = !LEAN && a.has_score, tc = M <= 8 && !LEAN && a.has_tc;
+        const bool has_score = !LEAN && a.has_score, tc = (M <= 8 || kW16) && !LEAN && a.has_tc;
         uint32_t* const mask_out = LEAN ? nullptr : a.mask_out;
         const int b0 = bx * kCB, r0 = by * V;
         PTRACE(1)
@@ -297,7 +300,20 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
             upos |= (1u << plo) | (1u << phi);
             sVal[r * kCB + b] = vals;
             sNib[r * kCB + b] = static_cast<uint8_t>(plo | (phi << 2));
-            if (M > 4 && tc) {
+            if (kW16 && tc) {
+                // window-16 form: half h of block b -> MMA 2 (b/4) + h, slots 4 (b%4) .. +3 of its 16 (the tile's
+                // values_tc row is [8 MMAs][16 values]); the 4 group nibbles as one u16
+                const int cl = static_cast<int>(__byte_perm(kp, 0u, 0x4440u | plo));
+                const int ch = static_cast<int>(__byte_perm(kp, 0u, 0x4440u | phi));
+                const TcBlock16 t = tc_encode_block16(cl, ch, static_cast<uint16_t>(vals & 0xFFFFu),
+                                                      static_cast<uint16_t>(vals >> 16));
+                uint16_t* dst = reinterpret_cast<uint16_t*>(sTcv) + r * (8 * kCB) + 32 * (b / 4) + 4 * (b % 4);
+                *reinterpret_cast<uint2*>(dst) = make_uint2(t.val[0] | (static_cast<uint32_t>(t.val[1]) << 16),
+                                                            t.val[2] | (static_cast<uint32_t>(t.val[3]) << 16));
+                *reinterpret_cast<uint2*>(dst + 16) = make_uint2(t.val[4] | (static_cast<uint32_t>(t.val[5]) << 16),
+                                                                 t.val[6] | (static_cast<uint32_t>(t.val[7]) << 16));
+                reinterpret_cast<uint16_t*>(sTcn)[r * kCB + b] = static_cast<uint16_t>(t.nibs);
+            } else if (M > 4 && M <= 8 && tc) {
                 const uint32_t cl = __byte_perm(kp, 0u, 0x4440u | plo), ch = __byte_perm(kp, 0u, 0x4440u | phi);
                 const uint2 e = sTab[cl * 8 + ch];
                 uint2 pk;
@@ -370,7 +386,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
             // selects K-groups 4h..4h+3 of the MMA.  One 16-byte store per (lane, stage) of this tile; MMA
             // slots past the last real MMA get the filler 0x44444444 (as vnm_pack_tc writes).
             const uint8_t* src = M == 4 ? sNib : sTcn;
-            constexpr int bpm = M == 4 ? 8 : 4;     // blocks per MMA
+            const uint16_t* src16 = reinterpret_cast<const uint16_t*>(sTcn);
+            constexpr int bpm = M == 4 ? 8 : (kW16 ? 2 : 4);  // blocks per MMA (window-16: 4 blocks per 2 MMAs)
             constexpr int nst = kCB / (4 * bpm);    // stages per tile (1 or 2)
             const int st0 = b0 / (4 * bpm);
             const int t128 = r0 / 128, l0 = r0 % 128;
@@ -384,7 +401,12 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                     const int mi = (st0 + sl) * 4 + k;
                     const int bl0 = (mi - st0 * 4) * bpm;  // first tile-local block of MMA mi
                     uint32_t wa = 0, wb = 0;
-                    if (M == 4) {
+                    if (kW16) {
+                        // tile-local MMA mt = 2 j + hm: byte hm of the nibble words of blocks 4j + 2h, 4j + 2h + 1
+                        const int mt = mi - st0 * 4, bl = 4 * (mt >> 1) + 2 * h, sh = 8 * (mt & 1);
+                        wa = ((src16[ra * kCB + bl] >> sh) & 0xFFu) | (((src16[ra * kCB + bl + 1] >> sh) & 0xFFu) << 8);
+                        wb = ((src16[rb_ * kCB + bl] >> sh) & 0xFFu) | (((src16[rb_ * kCB + bl + 1] >> sh) & 0xFFu) << 8);
+                    } else if (M == 4) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             wa |= static_cast<uint32_t>(src[ra * kCB + bl0 + 4 * h + q]) << (4 * q);
@@ -426,7 +448,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                 tma_store_2d(&tm.val, 2 * b0, r0, sVal);
                 if constexpr (kCB == 32) tma_store_2d(&tm.met, b0 / 8, r0, sMet);
             }
-            if (tc) tma_store_2d(&tm.tcv, (M == 4 ? 2 : 4) * b0, r0, M == 4 ? static_cast<const void*>(sVal) : sTcv);
+            if (tc) tma_store_2d(&tm.tcv, (M == 4 ? 2 : (kW16 ? 8 : 4)) * b0, r0, M == 4 ? static_cast<const void*>(sVal) : sTcv);
             bulk_commit();
         }
         PTRACE(5)
@@ -496,7 +518,7 @@ static bool L_unsupported(const PruneLaunch& L) {
     // M > 8: 16-block tiles, canonical outputs only (the window-16 / natural 2:4 forms are packed after the pass;
     // a 32-bit mask word can straddle two 16M-column tiles, so a mask output takes prune.cu)
     return L.mask_in || g.V < 32 || g.V > 128 || g.M > 16 || g.rows == 0 || g.cols == 0 ||
-           (L.values_tc && (!L.meta_tc || !L.values)) || (g.M > 8 && (L.values_tc || L.mask_out));
+           (L.values_tc && (!L.meta_tc || !L.values)) || (g.M > 8 && (L.mask_out || (L.values_tc && g.M % 4 == 0)));
 }
 
 // Per-problem tensor maps and arguments (+ the pad-row memsets of the window form); false: not applicable.
@@ -529,9 +551,10 @@ static bool setup_problem(const PruneLaunch& L, Maps& tm, Prune2Args& a, cudaStr
             return false;
     }
     if (tc) {
-        n_mma = g.nb_pad / (g.M == 4 ? 8 : 4);
+        const bool w16 = g.M > 8;
+        n_mma = w16 ? g.nb_pad / 2 : g.nb_pad / (g.M == 4 ? 8 : 4);
         ld_tc = 16 * n_mma;
-        const int vpb = g.M == 4 ? 2 : 4;  // window-form values per block
+        const int vpb = g.M == 4 ? 2 : (w16 ? 8 : 4);  // window-form values per block
         if (!encode_2d(&tm.tcv, L.values_tc, static_cast<uint64_t>(ld_tc), static_cast<uint64_t>(g.rows_p),
                        static_cast<uint64_t>(ld_tc) * 2, vpb * kCB, g.V, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                        CU_TENSOR_MAP_SWIZZLE_NONE))
@@ -582,9 +605,11 @@ int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream) {
     const int kCB = kcb_of(M);
     const int tile_cols = kCB * M;
     const size_t buf = static_cast<size_t>(V) * tile_cols * 2 + (B.any_score ? static_cast<size_t>(V) * tile_cols * 4 : 0);
-    const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (B.any_tc ? 4 + 8 : 4) + static_cast<size_t>(V) * 16 +
-                        256 * 4 + 2 * kCB * 4 + 64 * 8 + (B.any_mask ? static_cast<size_t>(V) * kCB * 4 : 0) +
-                        (B.any_tc ? 2 : 1) * static_cast<size_t>(V) * kCB;
+    const bool w16 = M > 8 && M % 4 != 0;
+    const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (B.any_tc ? 4 + (w16 ? 16 : 8) : 4) +
+                        static_cast<size_t>(V) * 16 + 256 * 4 + 2 * kCB * 4 + 64 * 8 +
+                        (B.any_mask ? static_cast<size_t>(V) * kCB * 4 : 0) +
+                        (B.any_tc ? (w16 ? 3 : 2) : 1) * static_cast<size_t>(V) * kCB;
     if (smem > kMaxSmem) return kLaunchUnsupported;
     cudaError_t e;
     switch (V) {
