@@ -126,10 +126,13 @@ def test_shard_boundaries():
 def tc_layout(g):
     """values_tc row length and metadata words per 128-row tile, written out from the include/vnm.h layout
     text (independently of dist.py): window form bpm = 4 blocks per MMA (8 for M = 4); the natural 2:4 form
-    (M % 4 == 0, M > 8) is the M = 4 layout over cols_p / 4 channel groups."""
+    (M % 4 == 0, M > 8) is the M = 4 layout over cols_p / 4 channel groups; the window-16 form (other M < 16) has two
+    MMAs per 4 blocks."""
     if g.M > 8 and g.M % 4 == 0:
         groups = g.cols_p // 4
         n_mma = (groups + 7) // 8 * 8 // 8
+    elif g.M > 8:
+        n_mma = g.nb_pad // 2
     else:
         n_mma = g.nb_pad // (8 if g.M == 4 else 4)
     n_stage = (n_mma + 3) // 4
@@ -138,7 +141,8 @@ def tc_layout(g):
 
 @pytest.mark.parametrize("rows,world,M,cols", [(1152, 2, 5, 384), (11008, 8, 5, 384), (384, 3, 5, 384),
                                                (200, 4, 5, 384), (512, 2, 16, 4096), (11008, 8, 16, 4096),
-                                               (700, 3, 12, 200), (1000, 4, 4, 256), (640, 2, 8, 100)])
+                                               (700, 3, 12, 200), (1000, 4, 4, 256), (640, 2, 8, 100),
+                                               (11008, 8, 13, 4096), (700, 3, 9, 300), (520, 2, 11, 1000)])
 def test_window_form_shards_are_whole_tiles(rows, world, M, cols):
     """With the tensor-core form present, output shards hold whole 128-row tiles and their values_tc /
     meta_tc views start at the shard's tile (include/vnm.h layouts, window and natural 2:4 forms alike);
