@@ -94,6 +94,9 @@ vnm_status vnm_geometry(int32_t rows, int32_t cols, int32_t V, int32_t M, vnm_ge
 // Natural 2:4 tensor-core form (M % 4 == 0, M > 8; include/vnm.h): the masked W is 2:4-sparse in the natural
 // channel order, so the window-form kernels run it as the M = 4 layout over 4-channel groups.
 static bool nat24(const vnm_geom* g) { return g->M > 8 && g->M % 4 == 0 && g->V >= 32 && g->V <= 128; }
+// the tensor-core form is written by the prune pass itself (window, window-16, and the natural 2:4 form at M = 16);
+// the other natural 2:4 forms are packed by a second launch
+static bool tc_fused(const vnm_geom* g) { return !nat24(g) || g->M == 16; }
 // Window-16 form (8 < M < 16, M % 4 != 0; include/vnm.h): 16-channel windows, two MMAs per 4 blocks — e.g. the
 // paper's 128:2:9 / 10 / 11 / 13 (tab:bs-sped) at prefill sizes
 static bool w16(const vnm_geom* g) { return g->M > 8 && g->M < 16 && g->M % 4 != 0 && g->V >= 32 && g->V <= 128; }
@@ -182,13 +185,13 @@ vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score
         if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;  // the natural 2:4 form packed after the pass (M % 4 == 0)
         if (!out->values_tc || !out->meta_tc) return VNM_ERR_ARG;
         if (!aligned16(out->values_tc) || !aligned16(out->meta_tc)) return VNM_ERR_ALIGN;
-        if (!nat24(g)) {  // window / window-16 form: written by the pass itself
+        if (tc_fused(g)) {
             L.values_tc = out->values_tc;
             L.meta_tc = out->meta_tc;
         }
     }
     const vnm_status st = from_launch(vnm::launch_prune_pack(L, reinterpret_cast<cudaStream_t>(stream)));
-    if (st || !out->values_tc || !nat24(g)) return st;
+    if (st || !out->values_tc || tc_fused(g)) return st;
     return from_launch(vnm::launch_pack_nat24(*out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -218,7 +221,7 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
             if (!tc_geom(g)) return VNM_ERR_UNSUPPORTED;
             if (!out[i]->values_tc || !out[i]->meta_tc) return VNM_ERR_ARG;
             if (!aligned16(out[i]->values_tc) || !aligned16(out[i]->meta_tc)) return VNM_ERR_ALIGN;
-            if (!nat24(g)) {
+            if (tc_fused(g)) {
                 L.values_tc = out[i]->values_tc;
                 L.meta_tc = out[i]->meta_tc;
             }
@@ -241,7 +244,7 @@ vnm_status vnm_prune_compress_batched(int32_t n, const uint16_t* const* W, const
         if (s) return s;
     }
     for (int i = 0; i < n; ++i)  // natural 2:4 tensor-core forms, packed after the pass
-        if (out[i]->values_tc && nat24(&out[i]->g) && out[i]->g.rows_p > 0 && out[i]->g.nb_pad > 0) {
+        if (out[i]->values_tc && !tc_fused(&out[i]->g) && out[i]->g.rows_p > 0 && out[i]->g.nb_pad > 0) {
             const vnm_status s = from_launch(vnm::launch_pack_nat24(*out[i], st));
             if (s) return s;
         }

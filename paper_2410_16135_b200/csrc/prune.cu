@@ -477,8 +477,8 @@ int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
         if (rc != kLaunchUnsupported) return rc;
     }
     if (L.values_tc && g.M > 8) {
-        // the window-16 form (8 < M < 16) is written fused by prune2 only: here the canonical arrays first, then
-        // the form packed from them (pack_tc.cu; identical bytes)
+        // the window-16 / M = 16 natural 2:4 forms are written fused by prune2 only: here the canonical arrays
+        // first, then the form packed from them (pack_tc.cu; identical bytes)
         PruneLaunch Lc = L;
         Lc.values_tc = nullptr;
         Lc.meta_tc = nullptr;
@@ -491,7 +491,7 @@ int launch_prune_pack(const PruneLaunch& L, cudaStream_t stream) {
         P.meta = L.meta;
         P.values_tc = L.values_tc;
         P.meta_tc = L.meta_tc;
-        return launch_pack_tc(P, stream);
+        return g.M % 4 == 0 ? launch_pack_nat24(P, stream) : launch_pack_tc(P, stream);
     }
     const bool from_mask = L.mask_in != nullptr;
     const bool has_score = L.score != nullptr;

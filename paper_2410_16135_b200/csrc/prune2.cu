@@ -103,7 +103,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
     constexpr int TC = kCB * M;     // tile columns (<= 256)
     // window-16 form (8 < M < 16, M % 4 != 0; include/vnm.h): 8 values per block, 4 group nibbles (u16)
     constexpr bool kW16 = M > 8 && M % 4 != 0;
-    constexpr int kTcvWords = kW16 ? 4 : 2;  // 32-bit words of window values per block
+    // natural 2:4 form at M = 16 (include/vnm.h): a block is 4 whole groups, 2 values each (= the window-16 group
+    // encoding of a block that fills its window); a 16-block tile is 64 groups = 8 MMAs = 2 stages
+    constexpr bool kN16 = M == 16;
+    constexpr int kTcvWords = (kW16 || kN16) ? 4 : 2;  // 32-bit words of tensor-core values per block
     constexpr int P = TC / 2;    // words per W row in shared memory
     constexpr int RPW = V / kWarps;
     constexpr uint32_t kWBytes = V * TC * 2, kSBytes = V * TC * 4;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         const int p = info.x, bx = info.y, by = info.z;
         const Prune2Args& a = B.a[p];
         const Maps& tm = B.tm[p];
-        const bool has_score = !LEAN && a.has_score, tc = (M <= 8 || kW16) && !LEAN && a.has_tc;
+        const bool has_score = !LEAN && a.has_score, tc = (M <= 8 || kW16 || kN16) && !LEAN && a.has_tc;
         uint32_t* const mask_out = LEAN ? nullptr : a.mask_out;
         const int b0 = bx * kCB, r0 = by * V;
         PTRACE(1)
@@ -300,7 +303,17 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
             upos |= (1u << plo) | (1u << phi);
             sVal[r * kCB + b] = vals;
             sNib[r * kCB + b] = static_cast<uint8_t>(plo | (phi << 2));
-            if (kW16 && tc) {
+            if (kN16 && tc) {
+                // natural 2:4 form, M = 16: groups 4b .. 4b+3 of the row -> values 8b .. 8b+7 of the tile's row
+                const int cl = static_cast<int>(__byte_perm(kp, 0u, 0x4440u | plo));
+                const int ch = static_cast<int>(__byte_perm(kp, 0u, 0x4440u | phi));
+                const TcBlock16 t = tc_encode_block16(cl, ch, static_cast<uint16_t>(vals & 0xFFFFu),
+                                                      static_cast<uint16_t>(vals >> 16));
+                *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(sTcv) + r * (8 * kCB) + 8 * b) =
+                    make_uint4(t.val[0] | (static_cast<uint32_t>(t.val[1]) << 16), t.val[2] | (static_cast<uint32_t>(t.val[3]) << 16),
+                               t.val[4] | (static_cast<uint32_t>(t.val[5]) << 16), t.val[6] | (static_cast<uint32_t>(t.val[7]) << 16));
+                reinterpret_cast<uint16_t*>(sTcn)[r * kCB + b] = static_cast<uint16_t>(t.nibs);
+            } else if (kW16 && tc) {
                 // window-16 form: half h of block b -> MMA 2 (b/4) + h, slots 4 (b%4) .. +3 of its 16 (the tile's
                 // values_tc row is [8 MMAs][16 values]); the 4 group nibbles as one u16
                 const int cl = static_cast<int>(__byte_perm(kp, 0u, 0x4440u | plo));
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
             // slots past the last real MMA get the filler 0x44444444 (as vnm_pack_tc writes).
             const uint8_t* src = M == 4 ? sNib : sTcn;
             const uint16_t* src16 = reinterpret_cast<const uint16_t*>(sTcn);
-            constexpr int bpm = M == 4 ? 8 : (kW16 ? 2 : 4);  // blocks per MMA (window-16: 4 blocks per 2 MMAs)
+            constexpr int bpm = M == 4 ? 8 : ((kW16 || kN16) ? 2 : 4);  // blocks per MMA (window-16: 4 per 2 MMAs)
             constexpr int nst = kCB / (4 * bpm);    // stages per tile (1 or 2)
             const int st0 = b0 / (4 * bpm);
             const int t128 = r0 / 128, l0 = r0 % 128;
@@ -401,7 +414,12 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                     const int mi = (st0 + sl) * 4 + k;
                     const int bl0 = (mi - st0 * 4) * bpm;  // first tile-local block of MMA mi
                     uint32_t wa = 0, wb = 0;
-                    if (kW16) {
+                    if (kN16) {
+                        // MMA mt = groups 8 mt .. 8 mt + 7 = blocks 2 mt, 2 mt + 1; K-groups 4h .. 4h+3 = block 2 mt + h
+                        const int bl = 2 * (mi - st0 * 4) + h;
+                        wa = src16[ra * kCB + bl];
+                        wb = src16[rb_ * kCB + bl];
+                    } else if (kW16) {
                         // tile-local MMA mt = 2 j + hm: byte hm of the nibble words of blocks 4j + 2h, 4j + 2h + 1
                         const int mt = mi - st0 * 4, bl = 4 * (mt >> 1) + 2 * h, sh = 8 * (mt & 1);
                         wa = ((src16[ra * kCB + bl] >> sh) & 0xFFu) | (((src16[ra * kCB + bl + 1] >> sh) & 0xFFu) << 8);
@@ -448,7 +466,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
                 tma_store_2d(&tm.val, 2 * b0, r0, sVal);
                 if constexpr (kCB == 32) tma_store_2d(&tm.met, b0 / 8, r0, sMet);
             }
-            if (tc) tma_store_2d(&tm.tcv, (M == 4 ? 2 : (kW16 ? 8 : 4)) * b0, r0, M == 4 ? static_cast<const void*>(sVal) : sTcv);
+            if (tc) tma_store_2d(&tm.tcv, (M == 4 ? 2 : ((kW16 || kN16) ? 8 : 4)) * b0, r0, M == 4 ? static_cast<const void*>(sVal) : sTcv);
             bulk_commit();
         }
         PTRACE(5)
@@ -518,7 +536,8 @@ static bool L_unsupported(const PruneLaunch& L) {
     // M > 8: 16-block tiles, canonical outputs only (the window-16 / natural 2:4 forms are packed after the pass;
     // a 32-bit mask word can straddle two 16M-column tiles, so a mask output takes prune.cu)
     return L.mask_in || g.V < 32 || g.V > 128 || g.M > 16 || g.rows == 0 || g.cols == 0 ||
-           (L.values_tc && (!L.meta_tc || !L.values)) || (g.M > 8 && (L.mask_out || (L.values_tc && g.M % 4 == 0)));
+           (L.values_tc && (!L.meta_tc || !L.values)) ||
+           (g.M > 8 && (L.mask_out || (L.values_tc && g.M % 4 == 0 && g.M != 16)));
 }
 
 // Per-problem tensor maps and arguments (+ the pad-row memsets of the window form); false: not applicable.
@@ -552,7 +571,8 @@ static bool setup_problem(const PruneLaunch& L, Maps& tm, Prune2Args& a, cudaStr
     }
     if (tc) {
         const bool w16 = g.M > 8;
-        n_mma = w16 ? g.nb_pad / 2 : g.nb_pad / (g.M == 4 ? 8 : 4);
+        // natural 2:4 form (M = 16): MMAs of 8 groups over ceil8(cols_p / 4) groups; window-16: 2 MMAs per 4 blocks
+        n_mma = g.M == 16 ? (g.cols_p / 4 + 7) / 8 : w16 ? g.nb_pad / 2 : g.nb_pad / (g.M == 4 ? 8 : 4);
         ld_tc = 16 * n_mma;
         const int vpb = g.M == 4 ? 2 : (w16 ? 8 : 4);  // window-form values per block
         if (!encode_2d(&tm.tcv, L.values_tc, static_cast<uint64_t>(ld_tc), static_cast<uint64_t>(g.rows_p),
@@ -605,7 +625,7 @@ int launch_prune2_batch(const PruneLaunch* Ls, int n, cudaStream_t stream) {
     const int kCB = kcb_of(M);
     const int tile_cols = kCB * M;
     const size_t buf = static_cast<size_t>(V) * tile_cols * 2 + (B.any_score ? static_cast<size_t>(V) * tile_cols * 4 : 0);
-    const bool w16 = M > 8 && M % 4 != 0;
+    const bool w16 = M > 8 && (M % 4 != 0 || M == 16);  // 8 tensor-core values per block
     const size_t smem = 2 * buf + static_cast<size_t>(V) * kCB * (B.any_tc ? 4 + (w16 ? 16 : 8) : 4) +
                         static_cast<size_t>(V) * 16 + 256 * 4 + 2 * kCB * 4 + 64 * 8 +
                         (B.any_mask ? static_cast<size_t>(V) * kCB * 4 : 0) +
