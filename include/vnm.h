@@ -91,7 +91,7 @@ typedef struct {
      * WINDOW-16 form: every block is a 16-row window of X^T (the block's M channels and 16-M of the next) as
      * four 2:4 groups, zero-completed like the window form; MMA 2j + h reads the half-windows h (groups 2h,
      * 2h+1) of blocks 4j .. 4j+3, so n_mma_w = nb_pad/2 and values_tc holds 8 values per block (half 0 of
-     * blocks 4j.. at MMA 2j, half 1 at MMA 2j + 1), meta_tc the same lane layout.  Packed after the pass.   */
+     * blocks 4j.. at MMA 2j, half 1 at MMA 2j + 1), meta_tc the same lane layout.                          */
     uint16_t* values_tc;
     uint32_t* meta_tc;
 } vnm_packed;
@@ -125,8 +125,8 @@ vnm_status vnm_compress(const uint16_t* W, int64_t ldw, const uint32_t* mask, co
 
 /* Fused vnm_prune + vnm_compress in one pass over W (byte-identical outputs).  mask may be NULL.
  * If out->values_tc / out->meta_tc are set (32 <= V <= 128, and M < 16 or M % 4 == 0) the tensor-core form is
- * written too: the window form in the same pass (M <= 8), the natural 2:4 form (M % 4 == 0) or the window-16
- * form (other M < 16) by a second launch
+ * written too: the window form (M <= 8), the window-16 form (other M < 16) and the natural 2:4 form at M = 16 in
+ * the same pass (32 <= V <= 128), the other natural 2:4 forms (M % 4 == 0) by a second launch
  * (identical to vnm_pack_tc of the result).                                                             */
 vnm_status vnm_prune_compress(const uint16_t* W, int64_t ldw, const float* score, int64_t lds,
                               const vnm_geom* g, vnm_packed* out, uint32_t* mask, vnm_stream_t stream);
