@@ -522,6 +522,8 @@ template <int V>
 cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
     // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
     if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16, 1>(M, B, smem, st);
+    // V = 128: the tile + staging take most of the shared memory, so one CTA per SM — of 16 warps (VNM_PRUNE_NW=8: 8)
+    if (V == 128 && VNM_ENV_INT("VNM_PRUNE_NW", 16) == 16) return launch_m<V, 16, 1>(M, B, smem, st);
     if constexpr (V <= 64) {
         if (!B.any_tc && !B.any_score && !B.any_mask) return launch_m<V, 8, 4, true>(M, B, smem, st);
         if (!B.any_tc) return launch_m<V, 8, 4>(M, B, smem, st);  // no window form: 4 CTAs per SM (measured faster)
