@@ -34,6 +34,9 @@ PLANS = [
     ("window resident pairs", 1536, 384, 64, 5, 8200, True),
     ("natural 2:4", 256, 640, 64, 16, 200, True),
     ("window V=32", 256, 640, 32, 7, 129, True),
+    ("window-16 1-CTA", 200, 333, 128, 13, 136, True),
+    ("window-16 pairs", 256, 1000, 64, 9, 264, True),
+    ("window-16 ragged -> gather", 200, 333, 128, 11, 129, True),
 ]
 
 
@@ -76,9 +79,12 @@ def test_spmm_writes_only_its_region(name, rows, cols, V, M, T, tc, out_dtype):
 
 
 @pytest.mark.parametrize("rows,cols,V,M,tc", [(1152, 384, 64, 5, True), (200, 333, 16, 7, False), (300, 1000, 128, 16, True),
-                                              (70, 23, 64, 8, True), (96, 200, 32, 13, False)])
-def test_prune_compress_writes_only_its_arrays(rows, cols, V, M, tc):
-    """The packed arrays (and the tensor-core form) are written exactly within their documented extents."""
+                                              (70, 23, 64, 8, True), (96, 200, 32, 13, False), (300, 1000, 128, 13, True),
+                                              (200, 500, 64, 9, True), (130, 700, 32, 11, True), (300, 1000, 64, 16, True)])
+@pytest.mark.parametrize("with_mask", [True, False])
+def test_prune_compress_writes_only_its_arrays(rows, cols, V, M, tc, with_mask):
+    """The packed arrays (and the tensor-core form) are written exactly within their documented extents — with a
+    mask output and without (for 8 < M <= 16 the two take different kernels: prune.cu + a pack, prune2 fused)."""
     W = synth.weights(rows, cols, seed=rows * M, kind="wide")
     g = vnm.geometry(rows, cols, V, M)
     sizes = {"values": g.rows_p * g.ld_val * 2, "col_idx": g.rows_p // V * g.nb_pad * 4, "meta": g.rows_p * g.ld_meta * 4,
@@ -97,7 +103,7 @@ def test_prune_compress_writes_only_its_arrays(rows, cols, V, M, tc):
     cp = P.c()
     Wd = to_dev_bf16(W)
     st = vnm.lib().vnm_prune_compress(ctypes.c_void_p(Wd.data_ptr()), Wd.stride(0), None, 0, ctypes.byref(g),
-                                      ctypes.byref(cp), ctypes.c_void_p(mask.data_ptr()),
+                                      ctypes.byref(cp), ctypes.c_void_p(mask.data_ptr()) if with_mask else None,
                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert st == 0
     torch.cuda.synchronize()
@@ -105,8 +111,13 @@ def test_prune_compress_writes_only_its_arrays(rows, cols, V, M, tc):
         tail = bufs[k][n // 4:].cpu().numpy()
         assert (tail == -559038737).all(), f"{k}: written past its extent"
     mask_ref, v_ref, c_ref, m_ref = oracle.prune_pack(W, V, M)
-    assert np.array_equal(mask.cpu().numpy().view(np.uint32), mask_ref)
+    if with_mask:
+        assert np.array_equal(mask.cpu().numpy().view(np.uint32), mask_ref)
+    else:
+        assert (bufs["mask"].cpu().numpy() == -559038737).all(), "mask written without a mask output"
     assert np.array_equal(P.values.view(torch.int16).cpu().numpy().view(np.uint16), v_ref)
+    assert np.array_equal(P.meta.cpu().numpy().view(np.uint32), m_ref)
+    assert np.array_equal(P.col_idx.cpu().numpy(), c_ref)
 
 
 @pytest.mark.parametrize("rows,cols,M,T", [(11008, 4096, 5, 16), (4096, 11008, 5, 8), (4096, 4096, 8, 32), (300, 2000, 13, 3)])
