@@ -381,6 +381,29 @@ __device__ __forceinline__ void mma_sp_stage(uint32_t d, uint64_t ad, uint64_t b
             : "memory");
     }
 }
+#ifdef VNM_ABLATIONS
+// timing ablation only (results invalid): mma_sp_stage<2> with every MMA of the stage reading A at ad + a_step * k
+__device__ __forceinline__ void mma_sp_stage_astep_pair(uint32_t d, uint64_t ad, uint64_t a_step, uint64_t bd,
+                                                        uint64_t b_step, uint32_t e, uint32_t idesc0, uint32_t idesc1,
+                                                        uint32_t accumulate, uint32_t n) {
+    asm volatile(
+        "{\n\t.reg .pred p, p3, acc, one;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b32 e2;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "setp.ne.b32 acc, %6, 0;\n\t"
+        "setp.eq.b32 one, 0, 0;\n\t"
+        "setp.gt.and.u32 p3, %8, 2, p;\n\t"
+        "add.s64 a1, %1, %9;\n\tadd.s64 a2, a1, %9;\n\tadd.s64 a3, a2, %9;\n\t"
+        "add.s64 b1, %2, %7;\n\tadd.s64 b2, b1, %7;\n\tadd.s64 b3, b2, %7;\n\t"
+        "add.u32 e2, %3, 2;\n\t"
+        "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%3], %4, acc;\n\t"
+        "@p tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a1, b1, [%3], %5, one;\n\t"
+        "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a2, b2, [e2], %4, one;\n\t"
+        "@p3 tcgen05.mma.sp.cta_group::2.kind::f16 [%0], a3, b3, [e2], %5, one;\n\t"
+        "}" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(e), "r"(idesc0), "r"(idesc1), "r"(accumulate), "l"(b_step), "r"(n), "l"(a_step)
+        : "memory");
+}
+#endif
 // the window form: MMA i of the stage reads B at bd + i * b_step.  The window-16 form (8 < M < 16) interleaves two
 // steps: MMAs 0 / 1 read the two half-windows of one block group (bd, bd + b_step = +8 rows), MMAs 2 / 3 those of
 // the next (bd + b_step2, + b_step)

@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "ptx.cuh"
 #include "tmap.h"
@@ -229,6 +230,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
             const uint32_t b_lbo = a.rb * 128;
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
+            // The production loop, specialised per mode (RES: A + metadata resident) with nothing else in it — as in
+            // spmm_tc3.cu, where counters and uniform branches around the issue slowed the MMA-only skeleton 1.6x;
+            // the general loop below runs for VNM_SPMM_TRACE and the timing ablations.
+            auto mma_loop = [&](auto res_c) {
+                constexpr bool RES = decltype(res_c)::value;
+                if constexpr (RES) mbar_wait(res_full, 0);
+                for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
+                    const int acc = C::kNACC == 2 ? (tl & 1) : 0;
+                    const uint32_t d_tmem = tmem + acc * NT;
+                    mbar_wait(&tmem_empty[acc], ((C::kNACC == 2 ? tl >> 1 : tl) & 1) ^ 1);
+                    tc_fence_after();
+                    for (int st = 0; st < a.n_stage; ++st, ++q) {
+                        const int s = q % S;
+                        mbar_wait(&full[s], (q / S) & 1);
+                        tc_fence_after();
+                        uint8_t* base = ring + s * a.stage_bytes;
+                        const uint32_t meta_s = tmem + kMetaCol + 4 * s;
+                        const uint32_t e_s = RES ? smem_u32(resE + st * kEBytes) : smem_u32(base + e_off);
+                        tmem_cp_elect<2>(meta_s, sdesc(e_s, 16, 128, 0));
+                        const uint32_t a0 = RES ? smem_u32(smem + st * kABytes) : smem_u32(base);
+                        const int left = a.n_mma - st * 4;
+                        mma_sp_stage<2>(d_tmem, sdesc(a0, 16, 1024, kLayoutSW128),
+                                        sdesc(smem_u32(base + b_off), b_lbo, sbo, kLayoutSW128), b_step, b_step2, meta_s,
+                                        idesc0, idesc1, st > 0 ? 1u : 0u, left < 4 ? static_cast<uint32_t>(left) : 4u);
+                        mma_commit_pair_elect(&empty[s], 0x3);
+                    }
+                    mma_commit_pair_elect(&tmem_full[acc], 0x3);
+                }
+            };
+            if (!a.trace && !(a.abl & 8)) {
+                if (a.a_res) mma_loop(std::true_type{});
+                else mma_loop(std::false_type{});
+            }
             for (; tile_of(a, cid, ncl, tl, rp, tt); ++tl) {
                 if (a.a_res && tl == 0) mbar_wait(res_full, 0);
                 const int acc = C::kNACC == 2 ? (tl & 1) : 0;

@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "ptx.cuh"
 #include "tmap.h"
@@ -76,6 +77,8 @@ struct Tc3Args {
 };
 
 __device__ unsigned long long g_tc3_t[9][160];
+// the general MMA loop runs for the MMA-issue timing ablations (abl is always 0 in production builds)
+#define VNM_ABLATION_FLAGS_DEVICE(args) ((args).abl & (64 | 128))
 
 // tile i of this pair; false past the end.  Resident A: every pair owns one row pair and the row pair's token
 // tiles are dealt round-robin over its pairs.  Streaming: tiles row-pair-major over all pairs (consecutive
@@ -230,7 +233,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t sbo = a.M == 4 ? 1024u : a.M * 128u;                 // K-group (window) stride
             const uint32_t meta_col = a.ts ? NT + 32u * a.n_chunk : kMetaCol;   // metadata after A in the TS form
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0, c_full0 = 0;
-            for (; tile3(a, cid, tl, rp, tt); ++tl) {
+            // The production loop, specialised per mode (RES: A + metadata resident; TS: A read from TMEM) with
+            // nothing else in it: the general loop below (kept for VNM_SPMM_TRACE and the opt-out K-ring peek) ran
+            // the MMA-only skeleton of DeiT-S qkv 1.3-1.6x slower per MMA for the same instructions — uniform
+            // branches and counters around the issue (profiles/r02_experiments.md, re-entry).
+            auto mma_loop = [&](auto res_c, auto ts_c) {
+                constexpr bool RES = decltype(res_c)::value, TS = decltype(ts_c)::value;
+                if constexpr (RES) {
+                    mbar_wait(res_full, 0);  // resident metadata (and A for TS) -> TMEM, both CTAs
+                    tc_fence_after();
+                    for (int c = 0; c < a.n_chunk; ++c)
+                        tmem_cp_elect<2>(tmem + meta_col + 4 * c, sdesc(smem_u32(sE + c * kEBytes), 16, 128, 0));
+                    if constexpr (TS)
+                        for (int c = 0; c < a.n_chunk; ++c)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                tmem_cp256_elect<2>(tmem + NT + 32 * c + 8 * i,
+                                                    sdesc(smem_u32(sA + c * kABytes), 16, 1024, kLayoutSW128) + 2 * i);
+                }
+                const uint64_t a_base = sdesc(smem_u32(sA), 16, 1024, kLayoutSW128);
+                for (; tile3(a, cid, tl, rp, tt); ++tl) {
+                    const int acc = kNacc == 2 ? (tl & 1) : 0;
+                    const int use = kNacc == 2 ? (tl >> 1) : tl;
+                    mbar_wait(&tmem_empty[acc], (use & 1) ^ 1);
+                    tc_fence_after();
+                    for (int st = 0; st < a.n_st; ++st, ++q) {
+                        const int s = q % S;
+                        mbar_wait(&full[s], (q / S) & 1);
+                        tc_fence_after();
+                        const int mi0 = st * a.ms;
+                        const int left = a.n_mma - mi0;
+                        const uint32_t n = static_cast<uint32_t>(left < a.ms ? left : a.ms);
+                        const uint64_t bd =
+                            sdesc(smem_u32(ring + static_cast<uint32_t>(s * a.slot_rows) * 128u), region, sbo, kLayoutSW128);
+                        if constexpr (RES) {
+                            const uint32_t e = tmem + meta_col + 4 * (mi0 >> 2) + (mi0 & 2);
+                            if constexpr (TS)
+                                mma_sp_stage_ts_pair(tmem + acc * NT, tmem + NT + 8 * mi0, bd, b_step, e, idesc0, idesc1,
+                                                     st > 0 ? 1u : 0u, n);
+                            else
+                                mma_sp_stage<2>(tmem + acc * NT, a_base + (((mi0 >> 2) * kABytes) >> 4) + 2 * (mi0 & 3), bd,
+                                                b_step, e, idesc0, idesc1, st > 0 ? 1u : 0u, n);
+                        } else {  // this slot's chunk: metadata into the slot's TMEM columns first (tensor-pipe order)
+                            const uint32_t e = tmem + meta_col + 4 * s;
+                            tmem_cp_elect<2>(e, sdesc(smem_u32(sE + s * kEBytes), 16, 128, 0));
+                            mma_sp_stage<2>(tmem + acc * NT, a_base + ((s * kABytes) >> 4), bd, b_step, e, idesc0, idesc1,
+                                            st > 0 ? 1u : 0u, n);
+                        }
+                        mma_commit_pair_elect(&empty[s], 0x3);
+                    }
+                    mma_commit_pair_elect(&tmem_full[acc], 0x3);
+                }
+            };
+            if (!a.trace && !(a.peek && !a.ovh) && !VNM_ABLATION_FLAGS_DEVICE(a)) {
+                if (a.a_res) {
+                    if (a.ts) mma_loop(std::true_type{}, std::true_type{});
+                    else mma_loop(std::true_type{}, std::false_type{});
+                } else {
+                    mma_loop(std::false_type{}, std::false_type{});
+                }
+                tl = 1 << 30;
+            }
+            for (; tl < (1 << 30) && tile3(a, cid, tl, rp, tt); ++tl) {
                 if (a.a_res && tl == 0) {  // resident metadata -> TMEM columns meta_col + 4c (both CTAs)
                     mbar_wait(res_full, 0);
                     tc_fence_after();
@@ -245,17 +309,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 const int acc = kNacc == 2 ? (tl & 1) : 0;
                 const int use = kNacc == 2 ? (tl >> 1) : tl;  // uses of this accumulator so far
-                c0 = clock64();
+                // (the wait counters read the clock only when tracing: per-stage clock reads in this loop cost the
+                // MMA issue ~1.6x — measured, profiles/r02_experiments.md)
+                if (a.trace) c0 = clock64();
                 mbar_wait(&tmem_empty[acc], (use & 1) ^ 1);
-                c_emp += clock64() - c0;
+                if (a.trace) c_emp += clock64() - c0;
                 tc_fence_after();
                 for (int st = 0; st < a.n_st; ++st, ++q) {
                     const int s = q % S;
-                    c0 = clock64();
+                    if (a.trace) c0 = clock64();
                     mbar_wait(&full[s], (q / S) & 1);
                     if (a.peek && !a.ovh && st + 1 < a.n_st) mbar_wait(&full[(q + 1) % S], ((q + 1) / S) & 1);  // overhang
-                    c_full += clock64() - c0;
-                    if (st == 0) c_full0 += clock64() - c0;
+                    if (a.trace) {
+                        c_full += clock64() - c0;
+                        if (st == 0) c_full0 += clock64() - c0;
+                    }
                     tc_fence_after();
                     const int mi0 = st * a.ms;
                     const int left = a.n_mma - mi0;
@@ -275,13 +343,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (a.ts)
                         mma_sp_stage_ts_pair(tmem + acc * NT, tmem + NT + 8 * mi0, bd, b_step, e, idesc0, idesc1,
                                              st > 0 ? 1u : 0u, n);
+#ifdef VNM_ABLATIONS
+                    else if (a.abl & 64)  // every MMA of the stage reads the stage's first A slice (timing only)
+                        mma_sp_stage_astep_pair(tmem + acc * NT, ad, 0, bd, b_step, e, idesc0, idesc1, st > 0 ? 1u : 0u, n);
+                    else if (a.abl & 128)  // the same issue code with the normal A offsets (control)
+                        mma_sp_stage_astep_pair(tmem + acc * NT, ad, 2, bd, b_step, e, idesc0, idesc1, st > 0 ? 1u : 0u, n);
+#endif
                     else
                         mma_sp_stage<2>(tmem + acc * NT, ad, bd, b_step, e, idesc0, idesc1, st > 0 ? 1u : 0u, n);
                     mma_commit_pair_elect(&empty[s], 0x3);
                 }
                 mma_commit_pair_elect(&tmem_full[acc], 0x3);
             }
-            if (a.trace && lane == 0) {
+            if (a.trace && lane == 0 && tl < (1 << 30)) {
                 g_tc3_t[0][blockIdx.x] = c_full;
                 g_tc3_t[1][blockIdx.x] = c_emp;
                 g_tc3_t[2][blockIdx.x] = clock64() - c_all;

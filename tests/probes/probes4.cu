@@ -229,7 +229,7 @@ namespace vnm {
 namespace {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     bench_stage_pair_kernel(uint32_t n, uint32_t sbo, uint32_t b_step, uint32_t stage_rows, uint32_t ring,
-                            uint32_t stages, int commit, unsigned long long* cycles) {
+                            uint32_t stages, int commit, unsigned long long* cycles, uint32_t lbo) {
     // commit == 2: the tc3 producer / MMA handshake: a producer thread waits empty[s] and arrives on full[s] (no
     // loads), the MMA warp waits full[s] before each stage and commits to empty[s] (both CTAs)
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -238,7 +238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     __shared__ uint32_t tmem_base;
     const uint32_t tid = threadIdx.x, warp = tid / 32;
     const uint32_t rank = cluster_ctarank();
-    for (uint32_t i = tid; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    for (uint32_t i = tid; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;  // (B ring + A)
     fence_proxy_async_smem();
     if (tid == 0) {
         for (int i = 0; i < 8; ++i) {
@@ -281,7 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                 if (commit == 5 && q % 5 != 4) mbar_wait(&fullb[(q + 1) % ring], ((q + 1) / ring) & 1);  // tc3's peek
                 tc_fence_after();
             }
-            const uint64_t bd = sdesc(smem_u32(smem + 81920 + s * stage_rows * 128), 16384, sbo, kLayoutSW128);
+            const uint64_t bd = sdesc(smem_u32(smem + 81920 + s * stage_rows * 128), lbo, sbo, kLayoutSW128);
             const uint64_t ad = a0 + ((q % 5) * 16384 >> 4);
             mma_sp_stage<2>(tb + (q / 5 % 2) * 224 * (n <= 224), ad, bd, b_step >> 4, tb + 480 + 4 * (q % 5), idesc0, idesc1,
                             q % 5 ? 1u : 0u, 4);
@@ -334,7 +334,21 @@ extern "C" int vnm_probe_bench_stage_pair(uint32_t n, uint32_t sbo, uint32_t b_s
     if (cudaFuncSetAttribute(bench_stage_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess)
         return 2;
-    bench_stage_pair_kernel<<<2 * pairs, commit >= 3 ? 320 : 128, smem>>>(n, sbo, b_step, stage_rows, ring, stages, commit, cycles);
+    bench_stage_pair_kernel<<<2 * pairs, commit >= 3 ? 320 : 128, smem>>>(n, sbo, b_step, stage_rows, ring, stages, commit, cycles,
+                                                                          16384u);
+    if (cudaDeviceSynchronize() != cudaSuccess) return 4;
+    return 0;
+}
+// the same with the B operand's chunk stride (UMMA LBO) given: tc3 uses the ring's whole region (ring_rows * 128 B)
+extern "C" int vnm_probe_bench_stage_pair_lbo(uint32_t n, uint32_t sbo, uint32_t b_step, uint32_t stage_rows, uint32_t ring,
+                                              uint32_t stages, int commit, int pairs, unsigned long long* cycles, uint32_t lbo) {
+    using namespace vnm;
+    const size_t smem = 220 * 1024;
+    if (cudaFuncSetAttribute(bench_stage_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return 2;
+    bench_stage_pair_kernel<<<2 * pairs, commit >= 3 ? 320 : 128, smem>>>(n, sbo, b_step, stage_rows, ring, stages, commit, cycles,
+                                                                          lbo);
     if (cudaDeviceSynchronize() != cudaSuccess) return 4;
     return 0;
 }
