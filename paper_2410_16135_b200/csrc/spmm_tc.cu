@@ -32,6 +32,13 @@
 namespace vnm {
 namespace {
 
+// timing-ablation flags (VNM_ABL): a compile-time 0 in production builds, so no ablation test is left in the loops
+#ifdef VNM_ABLATIONS
+#define ABL(args) ((args).abl)
+#else
+#define ABL(args) 0
+#endif
+
 constexpr int kThreads = 256;
 constexpr uint32_t kABytes = 128 * 128;  // 128 rows x 64 bf16
 constexpr uint32_t kEBytes = 128 * 16;   // 128 lanes x 4 words
@@ -109,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = q % S;
                     mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
                     uint8_t* base = smem + s * a.stage_bytes;
-                    if (a.abl & 4) {
+                    if (ABL(a) & 4) {
                         mbar_arrive(&full[s]);
                         continue;
                     }
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 uint8_t* base = smem + s * a.stage_bytes;
                 const uint32_t meta_s = tmem + kMetaCol + 4 * RT * s;
-                if (!(a.abl & 8) || q < S) {
+                if (!(ABL(a) & 8) || q < S) {
 #pragma unroll
                     for (int j = 0; j < RT; ++j)
                         tmem_cp_elect<1>(meta_s + 4 * j, sdesc(smem_u32(base + e_off + j * kEBytes), 16, 128, 0));
@@ -187,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tmem_full[acc], (NACC == 2 ? (tl >> 1) : tl) & 1);
             tc_fence_after();
             if constexpr (NACC == 1 && RT == 1) {
-                if (a.y_bf16 && !(a.abl & 3)) {
+                if (a.y_bf16 && !(ABL(a) & 3)) {
                     // one accumulator: drain the warp's whole 32 x NT block into packed bf16 registers and release
                     // the accumulator BEFORE the stores (the next tile's MMAs no longer wait for the epilogue)
                     constexpr int kC = NT / 64;
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int j = 0; j < RT; ++j) {
                 const int rt = rg * RT + j;
-                if (rt >= a.n_rt || (a.abl & 1)) break;
+                if (rt >= a.n_rt || (ABL(a) & 1)) break;
 #pragma unroll 1
                 for (int c = 0; c < NT && n0 + c < a.T; c += cw) {
                     uint32_t pk[32];
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int k = 0; k < 16; ++k) pk[16 * hh + k] = v[k];
                         }
                     }
-                    if (a.abl & 2) continue;
+                    if (ABL(a) & 2) continue;
                     if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
                     __syncwarp();
 #pragma unroll
