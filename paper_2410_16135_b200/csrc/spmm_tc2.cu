@@ -231,8 +231,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
             const uint32_t b_lbo = a.rb * 128;
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0;
             // The production loop, specialised per mode (RES: A + metadata resident) with nothing else in it — as in
-            // spmm_tc3.cu, where counters and uniform branches around the issue slowed the MMA-only skeleton 1.6x;
-            // the general loop below runs for VNM_SPMM_TRACE and the timing ablations.
+            // spmm_tc3.cu, whose general loop ran the MMA-only skeleton 1.6x slower; the general loop below runs for
+            // VNM_SPMM_TRACE and the timing ablations.
             auto mma_loop = [&](auto res_c) {
                 constexpr bool RES = decltype(res_c)::value;
                 if constexpr (RES) mbar_wait(res_full, 0);

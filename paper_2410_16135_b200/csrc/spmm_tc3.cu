@@ -234,9 +234,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t meta_col = a.ts ? NT + 32u * a.n_chunk : kMetaCol;   // metadata after A in the TS form
             unsigned long long c_full = 0, c_emp = 0, c_all = clock64(), c0, c_full0 = 0;
             // The production loop, specialised per mode (RES: A + metadata resident; TS: A read from TMEM) with
-            // nothing else in it: the general loop below (kept for VNM_SPMM_TRACE and the opt-out K-ring peek) ran
-            // the MMA-only skeleton of DeiT-S qkv 1.3-1.6x slower per MMA for the same instructions — uniform
-            // branches and counters around the issue (profiles/r02_experiments.md, re-entry).
+            // nothing else in it.  The general loop below (kept for VNM_SPMM_TRACE, the opt-out K-ring peek and the
+            // MMA ablations) ran the MMA-only skeleton of DeiT-S qkv 1.6x slower per MMA for the same MMAs; no
+            // single feature of it accounts for that (bisected: profiles/r02_experiments.md, round-2 re-entry).
             auto mma_loop = [&](auto res_c, auto ts_c) {
                 constexpr bool RES = decltype(res_c)::value, TS = decltype(ts_c)::value;
                 if constexpr (RES) {
@@ -309,8 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 const int acc = kNacc == 2 ? (tl & 1) : 0;
                 const int use = kNacc == 2 ? (tl >> 1) : tl;  // uses of this accumulator so far
-                // (the wait counters read the clock only when tracing: per-stage clock reads in this loop cost the
-                // MMA issue ~1.6x — measured, profiles/r02_experiments.md)
+                // (the wait counters read the clock only when tracing)
                 if (a.trace) c0 = clock64();
                 mbar_wait(&tmem_empty[acc], (use & 1) ^ 1);
                 if (a.trace) c_emp += clock64() - c0;
