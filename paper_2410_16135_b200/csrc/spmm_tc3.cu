@@ -61,6 +61,10 @@ struct Tc3Args {
     int32_t a_res;       // 1: A + metadata resident; 0: streamed per stage
     int32_t rp_per;      // resident: pairs per row pair;  streaming: total pairs
     int32_t peek;        // windows cross stage boundaries (5 <= M <= 7: an 8-channel window is wider than a block)
+    int32_t ts_direct;   // with ts: A goes global -> registers -> TMEM (tcgen05.st by the epilogue warps at the start),
+                         // never through shared memory, whose A space becomes more X^T ring slots
+    const uint16_t* values_tc;
+    int32_t ld_tc;
     int32_t ts;          // 1: resident A copied once into TMEM (tcgen05.cp) and the MMAs read it from there (TS form);
                          // NT = 256 (one accumulator) only: TMEM = accumulator | A (32 columns per chunk) | metadata
     int32_t ovh;         // 1: every slot also holds the next stage's first 8 rows (loaded twice; no cross-stage
@@ -111,7 +115,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     static_assert(kW1 > 0 && kW1 <= 64 && kW1 % 16 == 0, "token split");
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = a.S;
-    const int na = a.a_res ? a.n_chunk : S;  // A / metadata chunks held (resident: all; streaming: one per slot)
+    const int na = a.a_res ? (a.ts_direct ? 0 : a.n_chunk) : S;  // A chunks held in shared memory (resident: all;
+                                                                 // streaming: one per slot; A straight to TMEM: none)
     // [A: na x 16 KB][E: na x 2 KB, padded to 1 KB (unless aliased)][X^T ring: 2 token chunks x ring_rows x 128 B]
     // [transpose slots: kEpi x 2 KB][barriers]
     // (resident mode: the metadata staging aliases the epilogue slots — it is read once by tcgen05.cp before the
@@ -121,13 +126,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* ring = smem + na * kABytes + (e_alias ? 0u : (na * kEBytes + 1023) / 1024 * 1024);
     const uint32_t region = a.ring_rows * 128u;  // bytes per token-chunk region
     uint8_t* sY = ring + 2 * region;
-    uint8_t* sE = e_alias ? sY : smem + na * kABytes;
+    uint8_t* sE = e_alias ? sY : smem + na * kABytes;  // (ts_direct requires e_alias: checked on the host)
     uint64_t* full = reinterpret_cast<uint64_t*>(sY + kEpi * kYSlot);
     uint64_t* empty = full + S;
     uint64_t* tmem_full = empty + S;       // [2]
     uint64_t* tmem_empty = tmem_full + 2;  // [2]
     uint64_t* res_full = tmem_empty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 1);
+    uint64_t* a_ready = res_full + 1;  // ts_direct: every epilogue warp of both CTAs has stored its A rows in TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
@@ -151,6 +157,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(&tmem_empty[i], 2 * kEpi);  // epilogue warps x 2 CTAs
         }
         mbar_init(res_full, 1);
+        mbar_init(a_ready, 2 * kEpi);
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
@@ -180,9 +187,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int rt = 2 * rp + static_cast<int>(rank);  // row tiles past n_rt read as zeros (TMA OOB)
                 const int rte = rt < a.n_rt ? rt : 0;             // ... with valid metadata
                 if (a.a_res && i == 0 && pb == 0) {  // the pair's A and metadata, once
-                    if (leader) mbar_arrive_expect_tx(res_full, 2 * a.n_chunk * (kABytes + kEBytes));
+                    if (leader) mbar_arrive_expect_tx(res_full, 2 * a.n_chunk * ((a.ts_direct ? 0u : kABytes) + kEBytes));
                     for (int c = 0; c < a.n_chunk; ++c) {
-                        tma_load_2d_pair(sA + c * kABytes, &tmap_a, c * 64, rt * 128, res_full);
+                        if (!a.ts_direct) tma_load_2d_pair(sA + c * kABytes, &tmap_a, c * 64, rt * 128, res_full);
                         tma_load_2d_pair(sE + c * kEBytes, &tmap_e, 0, (rte * a.n_chunk + c) * 128, res_full);
                     }
                 }
@@ -244,12 +251,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     for (int c = 0; c < a.n_chunk; ++c)
                         tmem_cp_elect<2>(tmem + meta_col + 4 * c, sdesc(smem_u32(sE + c * kEBytes), 16, 128, 0));
-                    if constexpr (TS)
-                        for (int c = 0; c < a.n_chunk; ++c)
+                    if constexpr (TS) {
+                        if (a.ts_direct) {  // the epilogue warps store A into TMEM themselves
+                            mbar_wait(a_ready, 0);
+                            tc_fence_after();
+                        } else {
+                            for (int c = 0; c < a.n_chunk; ++c)
 #pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                tmem_cp256_elect<2>(tmem + NT + 32 * c + 8 * i,
-                                                    sdesc(smem_u32(sA + c * kABytes), 16, 1024, kLayoutSW128) + 2 * i);
+                                for (int i = 0; i < 4; ++i)
+                                    tmem_cp256_elect<2>(tmem + NT + 32 * c + 8 * i,
+                                                        sdesc(smem_u32(sA + c * kABytes), 16, 1024, kLayoutSW128) + 2 * i);
+                        }
+                    }
                 }
                 const uint64_t a_base = sdesc(smem_u32(sA), 16, 1024, kLayoutSW128);
                 for (; tile3(a, cid, tl, rp, tt); ++tl) {
@@ -300,7 +313,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     for (int c = 0; c < a.n_chunk; ++c)
                         tmem_cp_elect<2>(tmem + meta_col + 4 * c, sdesc(smem_u32(sE + c * kEBytes), 16, 128, 0));
-                    if (a.ts)  // resident A -> TMEM columns NT + 8 mi (MMA mi's 128 rows x 16 compressed values)
+                    if (a.ts && a.ts_direct) {
+                        mbar_wait(a_ready, 0);
+                        tc_fence_after();
+                    } else if (a.ts)  // resident A -> TMEM columns NT + 8 mi (MMA mi's 128 rows x 16 compressed values)
                         for (int c = 0; c < a.n_chunk; ++c)
 #pragma unroll
                             for (int i = 0; i < 4; ++i)
@@ -467,6 +483,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
         };
+        if (a.ts_direct) {
+            // A straight into TMEM (TS form): this warp's 32 rows (its lane quadrant), chunks half, half + kEq, ..:
+            // MMA mi's 16 values of a row (32 bytes of values_tc) -> TMEM columns NT + 8 mi .. + 7 of its lane, in
+            // order (the layout tcgen05.cp 128x256b produces from the SW128 tile); row tiles past n_rt get zeros
+            int rp0 = 0, tt0 = 0;
+            const bool any = tile3(a, cid, 0, rp0, tt0);
+            const int rt0 = 2 * rp0 + static_cast<int>(rank);
+            const bool real = any && rt0 < a.n_rt;
+            const uint4* vrow = reinterpret_cast<const uint4*>(a.values_tc + static_cast<int64_t>(rt0 * 128 + 32 * qd + lane) * a.ld_tc);
+            const uint32_t tbase = tmem + ((32 * qd) << 16) + NT;
+            for (int c = half; c < a.n_chunk; c += kEq) {
+                uint4 x[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)  // (a row holds 2 x n_mma of these 16-byte groups)
+                    x[i] = real && 8 * c + i < 2 * a.n_mma ? __ldg(vrow + 8 * c + i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) tmem_st_32x32b_x4(tbase + 32 * c + 4 * i, x[i].x, x[i].y, x[i].z, x[i].w);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader) mbar_arrive(a_ready);
+                else mbar_arrive_remote(a_ready, 0);
+            }
+        }
         for (; tile3(a, cid, tl, rp, tt); ++tl) {
             const int rt = 2 * rp + static_cast<int>(rank);
             const int acc = kNacc == 2 ? (tl & 1) : 0;
@@ -536,10 +578,14 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     if (!a.a_res && a.ms != 4) return kLaunchUnsupported;  // streamed A arrives in 4-MMA chunks
     // TS form: resident A and one accumulator, TMEM = NT + 32 columns per A chunk + 4 per metadata chunk
     if (!a.a_res || kNacc != 1 || NT + 36 * a.n_chunk > 512) a.ts = 0;
+    // TS form with A stored into TMEM by the epilogue warps (no shared-memory copy of A: its space becomes ring
+    // slots); VNM_TC3_TS_STAGED=1 keeps the shared-memory staging + tcgen05.cp
+    a.ts_direct = a.ts && alias && VNM_ENV_INT("VNM_TC3_TS_STAGED", 0) == 0 ? 1 : 0;
+    const uint32_t res_smem = a.ts_direct ? 0u : res;
     // ring slots: as many as fit (bytes in flight hide the load latency), at least 3
     int S = 0;
-    for (int s = 8; s >= 3 && !S; --s) {
-        const uint32_t ab = a.a_res ? res : static_cast<uint32_t>(s) * kABytes + ebytes(s);
+    for (int s = 10; s >= 3 && !S; --s) {
+        const uint32_t ab = a.a_res ? res_smem : static_cast<uint32_t>(s) * kABytes + ebytes(s);
         const bool tmem_ok = kNacc * NT + 4 * (a.a_res ? a.n_chunk : s) <= 512;
         if (tmem_ok && ab + 2u * (s * a.slot_rows + 8) * 128u + fixed <= kMaxSmem) S = s;
     }
@@ -576,7 +622,7 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
         !encode_2d(&ts1, L.XT, static_cast<uint64_t>(L.T), static_cast<uint64_t>(g.cols), xr, kW1, 8))
         return kLaunchCudaError;
     const bool bf = L.y_dtype == VNM_BF16;
-    const int na = a.a_res ? a.n_chunk : S;
+    const int na = a.a_res ? (a.ts_direct ? 0 : a.n_chunk) : S;  // (as the kernel's layout)
     const size_t smem = static_cast<size_t>(na) * kABytes + (a.a_res && alias ? 0u : ebytes(na)) +
                         2u * a.ring_rows * 128u + fixed;
     auto k = bf ? vnm_spmm_tc3_kernel<NT, true> : vnm_spmm_tc3_kernel<NT, false>;
@@ -587,6 +633,8 @@ int launch_nt3(const SpmmLaunch& L, Tc3Args a, int want_res, cudaStream_t stream
     a.Y = L.YT;
     a.ldy = L.ldy;
     a.rows = g.rows;
+    a.values_tc = L.P->values_tc;
+    a.ld_tc = ld_tc;
     cudaError_t e = launch_pdl(false, k, dim3(2 * pairs), dim3(kThreads), smem, stream, ta, te, tb0, tb1, ts0, ts1, a);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -621,6 +669,9 @@ int launch_spmm_tc3(const SpmmLaunch& L, int mode, cudaStream_t stream) {
     a.peek = g.M >= 5 && g.M <= 7;
     a.ovh = VNM_ENV_INT("VNM_TC3_OVH", 1) ? 1 : 0;
     a.ts = 0;
+    a.ts_direct = 0;
+    a.values_tc = nullptr;
+    a.ld_tc = 0;
     const int res = mode < 0 ? 1 : mode;
     // resident A: 4 MMAs per stage (16 blocks), 2 when a 4-MMA stage would be large (M >= 7: >= 112 rows)
     a.ms = g.M >= 7 && res ? 2 : 4;
