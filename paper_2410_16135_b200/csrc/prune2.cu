@@ -93,9 +93,10 @@ struct Batch {
 
 // MINB: CTAs per SM the register budget is sized for (8-warp CTAs: 3, or 4 when no window form is written —
 // the window-form staging is then not allocated and 4 CTAs fit in shared memory)
-// LEAN: no score, no mask, no window form anywhere in the batch (the decode / deployment case): those paths
+// LEAN = 1: no score, no mask, no tensor-core form anywhere in the batch (the decode / deployment case); LEAN = 2: no
+// score, no mask, the tensor-core form as the batch asks (the prefill case): those paths
 // compile out of the per-row loop (fewer branches and parameter loads per weight; the kernel is issue-bound)
-template <int V, int M, int NW, int MINB, bool LEAN>
+template <int V, int M, int NW, int MINB, int LEAN>
 __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_constant__ Batch B) {
     constexpr int kWarps = NW, kThreads = 32 * NW;
     constexpr int kCB = kcb_of(M);  // column blocks per tile (shadows the namespace constant)
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
         const int p = info.x, bx = info.y, by = info.z;
         const Prune2Args& a = B.a[p];
         const Maps& tm = B.tm[p];
-        const bool has_score = !LEAN && a.has_score, tc = (M <= 8 || kW16 || kN16) && !LEAN && a.has_tc;
+        const bool has_score = LEAN == 0 && a.has_score, tc = (M <= 8 || kW16 || kN16) && LEAN != 1 && a.has_tc;
         uint32_t* const mask_out = LEAN ? nullptr : a.mask_out;
         const int b0 = bx * kCB, r0 = by * V;
         PTRACE(1)
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) prune2_kernel(const __grid_cons
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-template <int V, int M, int NW, int MINB, bool LEAN = false>
+template <int V, int M, int NW, int MINB, int LEAN = 0>
 cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     constexpr int kThreads = 32 * NW;
     auto k = prune2_kernel<V, M, NW, MINB, LEAN>;
@@ -498,7 +499,7 @@ cudaError_t launch2(const Batch& B, size_t smem, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int V, int NW, int MINB, bool LEAN = false>
+template <int V, int NW, int MINB, int LEAN = 0>
 cudaError_t launch_m(int M, const Batch& B, size_t smem, cudaStream_t st) {
     switch (M) {
         case 4: return launch2<V, 4, NW, MINB, LEAN>(B, smem, st);
@@ -523,11 +524,17 @@ cudaError_t launch_v2(int M, const Batch& B, size_t smem, cudaStream_t st) {
     // fewer tiles than SMs: one tile per CTA, 16 warps (latency); else 8-warp CTAs, 3 per SM (throughput)
     if (V <= 64 && B.tile0[B.n] < num_sms()) return launch_m<V, 16, 1>(M, B, smem, st);
     // V = 128: the tile + staging take most of the shared memory, so one CTA per SM — of 16 warps (VNM_PRUNE_NW=8: 8)
-    if (V == 128 && VNM_ENV_INT("VNM_PRUNE_NW", 16) == 16) return launch_m<V, 16, 1>(M, B, smem, st);
+    // (no score and no mask: those paths compile out of the per-row loop, LEAN = 2, or 1 without a tensor-core form)
+    const bool nsm = !B.any_score && !B.any_mask && VNM_ENV_INT("VNM_PRUNE_LEAN2", 1);
+    if (V == 128 && VNM_ENV_INT("VNM_PRUNE_NW", 16) == 16) {
+        if (nsm) return B.any_tc ? launch_m<V, 16, 1, 2>(M, B, smem, st) : launch_m<V, 16, 1, 1>(M, B, smem, st);
+        return launch_m<V, 16, 1>(M, B, smem, st);
+    }
     if constexpr (V <= 64) {
-        if (!B.any_tc && !B.any_score && !B.any_mask) return launch_m<V, 8, 4, true>(M, B, smem, st);
+        if (!B.any_tc && nsm) return launch_m<V, 8, 4, 1>(M, B, smem, st);
         if (!B.any_tc) return launch_m<V, 8, 4>(M, B, smem, st);  // no window form: 4 CTAs per SM (measured faster)
     }
+    if (nsm) return launch_m<V, 8, 3, 2>(M, B, smem, st);
     return launch_m<V, 8, 3>(M, B, smem, st);
 }
 
