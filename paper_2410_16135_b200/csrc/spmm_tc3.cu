@@ -81,8 +81,14 @@ struct Tc3Args {
 };
 
 __device__ unsigned long long g_tc3_t[9][160];
-// the general MMA loop runs for the MMA-issue timing ablations (abl is always 0 in production builds)
-#define VNM_ABLATION_FLAGS_DEVICE(args) ((args).abl & (64 | 128))
+// timing-ablation flags (VNM_ABL): a compile-time 0 in production builds, so no ablation test is left in the loops;
+// the general MMA loop runs for the MMA-issue ablations
+#ifdef VNM_ABLATIONS
+#define ABL(args) ((args).abl)
+#else
+#define ABL(args) 0
+#endif
+#define VNM_ABLATION_FLAGS_DEVICE(args) (ABL(args) & (64 | 128))
 
 // tile i of this pair; false past the end.  Resident A: every pair owns one row pair and the row pair's token
 // tiles are dealt round-robin over its pairs.  Streaming: tiles row-pair-major over all pairs (consecutive
@@ -196,10 +202,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int x0 = tt * NT + kNH * static_cast<int>(rank);
                 for (int st = 0; st < a.n_st; ++st, ++q) {
                     const int s = q % S;
-                    c0 = clock64();
+                    if (a.trace) c0 = clock64();
                     mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
-                    c_emp += clock64() - c0;
-                    if (a.abl & 4) {
+                    if (a.trace) c_emp += clock64() - c0;
+                    if (ABL(a) & 4) {
                         if (leader && pb == 0) mbar_arrive(&full[s]);
                         continue;
                     }
@@ -207,18 +213,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     // phase still needs that arrival, and the transaction count is signed)
                     if (pb == 0) {
                         uint32_t tx = a.stage_tx + (s == 0 && !a.ovh ? a.shadow_tx : 0u);
-                        if (a.abl & 16) tx -= 2u * (kABytes + kEBytes);                  // ablation: no A / E loads
-                        if (a.abl & 32) tx = a.a_res ? 0u : 2u * (kABytes + kEBytes);    // ablation: no X^T loads
+                        if (ABL(a) & 16) tx -= 2u * (kABytes + kEBytes);                  // ablation: no A / E loads
+                        if (ABL(a) & 32) tx = a.a_res ? 0u : 2u * (kABytes + kEBytes);    // ablation: no X^T loads
                         if (leader) {
                             if (tx) mbar_arrive_expect_tx(&full[s], tx);
                             else mbar_arrive(&full[s]);
                         }
-                        if (!a.a_res && !(a.abl & 16)) {  // this stage's A / metadata chunk (ms = 4: stage == chunk)
+                        if (!a.a_res && !(ABL(a) & 16)) {  // this stage's A / metadata chunk (ms = 4: stage == chunk)
                             tma_load_2d_pair(sA + s * kABytes, &tmap_a, st * 64, rt * 128, &full[s]);
                             tma_load_2d_pair(sE + s * kEBytes, &tmap_e, 0, (rte * a.n_chunk + st) * 128, &full[s]);
                         }
                     }
-                    if (a.abl & 32) continue;
+                    if (ABL(a) & 32) continue;
                     const int y = st * a.rows_stage;
                     uint8_t* dst = ring + static_cast<uint32_t>(s * a.slot_rows) * 128u + pb * region;
                     tma_load_2d_pair(dst, pb ? &tmap_b1 : &tmap_b0, x0 + 64 * pb, y, &full[s]);
@@ -439,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         };
         auto store = [&](int rt, int c, const uint32_t (&w)[32]) {
             const int t0 = tt * NT + c * kCw;
-            if (rt >= a.n_rt || t0 >= a.T || (a.abl & 2)) return;
+            if (rt >= a.n_rt || t0 >= a.T || (ABL(a) & 2)) return;
             constexpr int kEl = kBf16 ? 8 : 4;  // elements per 16 bytes
             const int t_end = min(a.T, tt * NT + NT);
             const int grow0 = rt * 128 + 32 * qd;
@@ -513,13 +519,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int rt = 2 * rp + static_cast<int>(rank);
             const int acc = kNacc == 2 ? (tl & 1) : 0;
             const int use = kNacc == 2 ? (tl >> 1) : tl;
-            c0 = clock64();
+            if (a.trace) c0 = clock64();
             mbar_wait(&tmem_full[acc], use & 1);
-            c1 = clock64();
-            c_wait += c1 - c0;
+            if (a.trace) {
+                c1 = clock64();
+                c_wait += c1 - c0;
+            }
             tc_fence_after();
             const uint32_t taddr = tmem + ((32 * qd) << 16) + acc * NT;
-            if (a.abl & 1) {
+            if (ABL(a) & 1) {
                 release(acc);
                 continue;
             }
@@ -546,7 +554,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     store(rt, c, w);
                 }
             }
-            c_epi += clock64() - c1;
+            if (a.trace) c_epi += clock64() - c1;
         }
         if (a.trace && warp == 4 && lane == 0) {
             g_tc3_t[4][blockIdx.x] = c_wait;
