@@ -37,6 +37,13 @@
 namespace vnm {
 namespace {
 
+// timing-ablation flags (VNM_ABL): a compile-time 0 in production builds, so no ablation test is left in the loops
+#ifdef VNM_ABLATIONS
+#define ABL(args) ((args).abl)
+#else
+#define ABL(args) 0
+#endif
+
 constexpr uint32_t kABytes = 128 * 128;     // 128 rows x 64 bf16 (SW128)
 constexpr uint32_t kEBytes = 128 * 16;      // 128 lanes x 4 words
 constexpr uint32_t kYSlot = 32 * 128;       // one 32 row x 128 B staging slot (SW128)
@@ -191,19 +198,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                 }
                 for (int st = 0; st < a.n_stage; ++st, ++q) {
                     const int s = q % S;
-                    c0 = clock64();
+                    if (a.trace) c0 = clock64();
                     mbar_wait(&empty[s], ((q / S) & 1) ^ 1);
-                    c_emp += clock64() - c0;
+                    if (a.trace) c_emp += clock64() - c0;
                     uint8_t* base = ring + s * a.stage_bytes;
-                    if (a.abl & 4) {
+                    if (ABL(a) & 4) {
                         if (leader) mbar_arrive(&full[s]);
                         continue;
                     }
                     if (a.a_res) {
                         if (leader) mbar_arrive_expect_tx(&full[s], 2 * a.b_bytes);
                     } else {
-                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * ((a.abl & 16 ? 0u : kABytes) + kEBytes + a.b_bytes));
-                        if (!(a.abl & 16)) tma_load_2d_pair(base, &tmap_a, st * 64, rt * 128, &full[s]);
+                        if (leader) mbar_arrive_expect_tx(&full[s], 2 * ((ABL(a) & 16 ? 0u : kABytes) + kEBytes + a.b_bytes));
+                        if (!(ABL(a) & 16)) tma_load_2d_pair(base, &tmap_a, st * 64, rt * 128, &full[s]);
                         tma_load_2d_pair(base + e_off, &tmap_e, 0, (rte * a.n_stage + st) * 128, &full[s]);
                     }
                     tma_load_2d_pair(base + b_off, &tmap_b, n0, st * a.rows_stage, &full[s]);
@@ -259,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     mma_commit_pair_elect(&tmem_full[acc], 0x3);
                 }
             };
-            if (!a.trace && !(a.abl & 8)) {
+            if (!a.trace && !(ABL(a) & 8)) {
                 if (a.a_res) mma_loop(std::true_type{});
                 else mma_loop(std::false_type{});
             }
@@ -280,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     uint8_t* base = ring + s * a.stage_bytes;
                     const uint32_t meta_s = tmem + kMetaCol + 4 * s;
                     const uint32_t e_s = a.a_res ? smem_u32(resE + st * kEBytes) : smem_u32(base + e_off);
-                    if (!(a.abl & 8) || q < S) tmem_cp_elect<2>(meta_s, sdesc(e_s, 16, 128, 0));
+                    if (!(ABL(a) & 8) || q < S) tmem_cp_elect<2>(meta_s, sdesc(e_s, 16, 128, 0));
                     const uint32_t a0 = a.a_res ? smem_u32(smem + st * kABytes) : smem_u32(base);
                     const int left = a.n_mma - st * 4;
                     mma_sp_stage<2>(d_tmem, sdesc(a0, 16, 1024, kLayoutSW128),
@@ -308,14 +315,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
             const int rt = 2 * rp + static_cast<int>(rank);
             const int t0 = tt * NT + kBChunk * ch;  // first token of this warp's chunk
             const int acc = C::kNACC == 2 ? (tl & 1) : 0;
-            c0 = clock64();
+            if (a.trace) c0 = clock64();
             mbar_wait(&tmem_full[acc], (C::kNACC == 2 ? tl >> 1 : tl) & 1);
-            c1 = clock64();
-            c_wait += c1 - c0;
+            if (a.trace) {
+                c1 = clock64();
+                c_wait += c1 - c0;
+            }
             tc_fence_after();
             const uint32_t taddr = tmem + ((32 * qd) << 16) + acc * NT + kBChunk * ch;
-            const bool store = rt < a.n_rt && t0 < a.T && !(a.abl & 2);
-            if (a.abl & 1) {
+            const bool store = rt < a.n_rt && t0 < a.T && !(ABL(a) & 2);
+            if (ABL(a) & 1) {
                 release(&tmem_empty[acc], lane, leader);
                 continue;
             }
@@ -332,10 +341,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg<NT>::kThreads, 1
                     __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[2 * k]), __uint_as_float(v[2 * k + 1]));
                     pk[k] = *reinterpret_cast<uint32_t*>(&b2);
                 }
-                c0 = clock64();
-                c_drain += c0 - c1;
+                if (a.trace) {
+                    c0 = clock64();
+                    c_drain += c0 - c1;
+                }
                 if (store) stage_store(buf, 1, 0, lane, pk, &tmap_y, t0, rt * 128 + 32 * qd);
-                c_store += clock64() - c0;
+                if (a.trace) c_store += clock64() - c0;
             } else {
                 // fp32 (parity path): two 32-token chunks straight from TMEM; release at the end
 #pragma unroll 1
