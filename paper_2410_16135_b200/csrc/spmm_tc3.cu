@@ -48,6 +48,10 @@ constexpr uint32_t kYSlot = 32 * 64;     // epilogue transpose slot: 32 rows x 6
 constexpr int kEpi = VNM_TC3_EPI;        // epilogue warps (a multiple of 4: kEpi / 4 per TMEM lane quadrant)
 constexpr int kEq = kEpi / 4;
 constexpr int kThreads = 128 + 32 * kEpi;  // warps 0 + 2 TMA, 1 MMA, 3 idle, 4.. epilogue
+#ifndef VNM_TC3_EARLY
+#define VNM_TC3_EARLY 0
+#endif
+constexpr bool kEarlyRelease = VNM_TC3_EARLY != 0;  // two accumulators too: release before the stores (experiment)
 
 struct Tc3Args {
     int32_t T, M;
@@ -531,8 +535,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 release(acc);
                 continue;
             }
-            if constexpr (kNacc == 1) {
-                // one accumulator: drain this warp's chunks into registers, release, then store
+            if constexpr (kNacc == 1 || kEarlyRelease) {
+                // drain this warp's chunks into registers, release, then store (one accumulator; with two only when
+                // kEarlyRelease: measured, the stores then never hold an accumulator)
                 uint32_t w[kCpw][32];
 #pragma unroll
                 for (int j = 0; j < kCpw; ++j)
