@@ -308,7 +308,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mma_commit_pair_elect(&tmem_full[acc], 0x3);
                 }
             };
+#ifdef VNM_TC3_TRACE_FAST  // (experiment builds: the specialised loop under VNM_SPMM_TRACE too; its own counters stay 0)
+            if (!(a.peek && !a.ovh) && !VNM_ABLATION_FLAGS_DEVICE(a)) {
+#else
             if (!a.trace && !(a.peek && !a.ovh) && !VNM_ABLATION_FLAGS_DEVICE(a)) {
+#endif
                 if (a.a_res) {
                     if (a.ts) mma_loop(std::true_type{}, std::true_type{});
                     else mma_loop(std::true_type{}, std::false_type{});
