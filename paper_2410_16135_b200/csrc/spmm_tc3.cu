@@ -472,13 +472,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                  : "memory");
                 __syncwarp();
                 const int cc = lane & 3, tok = th + cc * kEl;
+                // the four shared-memory reads first (volatile asm keeps its order: interleaved with the stores, each
+                // read's latency was exposed once per row group), then the four global stores
+                uint32_t xr[4][4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int r = 8 * j + (lane >> 2);
-                    uint32_t x0, x1, x2, x3;
                     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                 : "=r"(xr[j][0]), "=r"(xr[j][1]), "=r"(xr[j][2]), "=r"(xr[j][3])
                                  : "r"(srow + r * 64 + (((cc ^ (r >> 1)) & 3) << 4)));
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = 8 * j + (lane >> 2);
+                    const uint32_t x0 = xr[j][0], x1 = xr[j][1], x2 = xr[j][2], x3 = xr[j][3];
                     const int grow = grow0 + r;
                     if (grow >= a.rows || tok >= t_end) continue;
                     uint8_t* dst = static_cast<uint8_t*>(a.Y) + (static_cast<int64_t>(grow) * a.ldy + tok) * (kBf16 ? 2 : 4);
